@@ -1,0 +1,221 @@
+"""Pins for oracle/aggregator.py against what the paper fixes (all CPU).
+
+O7 Theorem bound, O8 Lemma (adversarial + tight), O9 worked examples, O10 fill ratio
+(Monte Carlo vs eq:fill-ratio), O11 completeness, O12 packing/LPT brute force, O14 determinism.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import aggregator as agg
+from synth.configs import WORKLOADS, ENCODERS, scaled
+from synth.workload import make_workload, partition_sizes
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+@pytest.mark.parametrize("ex", GOLD["aggregator_examples"], ids=lambda e: e["cite"][:6])
+def test_worked_examples(ex):
+    keys = list(range(len(ex["sizes"])))
+    A = agg.Aggregator(ex["b_min"], ex["b_max"])
+    for k, n in zip(keys, ex["sizes"]):
+        A.add_partition(k, n)
+    assert A.total == ex["residual"]
+    A.finish()
+    got = [{"reason": sb.reason, "total": sb.total, "members": len(sb.keys)} for sb in A.flushes]
+    assert got == ex["expect"]
+
+
+def test_lemma_tight():
+    g = GOLD["lemma_tight"]
+    A = agg.run_aggregator(range(len(g["sizes"])), g["sizes"], g["b_min"], g["b_max"])
+    assert A.peak_buffered == g["peak"] == g["b_min"] - 1 + max(g["sizes"])
+
+
+def test_memory_bound_formula():
+    g = GOLD["memory_bound"]
+    assert agg.memory_bound_bytes(g["S"], g["L"], g["d"]) == pytest.approx(g["bytes"])
+
+
+def _orders(rng, sizes):
+    yield sizes
+    yield np.sort(sizes)            # ascending: largest last
+    yield np.sort(sizes)[::-1]      # descending
+    s = np.sort(sizes)
+    alt = np.empty_like(s)
+    alt[0::2] = s[: (len(s) + 1) // 2]
+    alt[1::2] = s[(len(s) + 1) // 2:][::-1]
+    yield alt                       # small/large alternating
+    yield np.full_like(sizes, int(np.median(sizes)))
+    for _ in range(200):
+        yield rng.permutation(sizes)
+
+
+def test_lemma_adversarial_orders():
+    """O8: >= 10^3 random and crafted orders; max buffered <= B_min - 1 + max n_k (prefix form)."""
+    rng = np.random.default_rng(7)
+    n_checked = 0
+    for trial in range(5):
+        sizes = np.maximum(1, rng.lognormal(9.03, 1.72, size=300).astype(np.int64))
+        for b_min in (10_000, 100_000):
+            for order in _orders(rng, sizes):
+                A = agg.run_aggregator(range(len(order)), order, b_min, 5 * b_min)
+                assert A.peak_buffered <= b_min - 1 + int(np.max(order))
+                # overshoot: every efficiency flush lies in [B_min, B_min + n_max)
+                for sb in A.flushes:
+                    if sb.reason == agg.EFFICIENCY:
+                        assert b_min <= sb.total < b_min + int(np.max(order))
+                    if sb.reason == agg.SAFETY:
+                        assert sb.total >= 5 * b_min
+                n_checked += 1
+    assert n_checked >= 1000
+
+
+def test_theorem_bound_and_completeness():
+    """O7 + O11: F <= min(P, ceil(N/B_min)); every key in exactly one SuperBatch; sum S = N."""
+    rng = np.random.default_rng(3)
+    for trial in range(50):
+        P = int(rng.integers(1, 400))
+        sizes = np.maximum(1, rng.lognormal(6, 1.5, size=P).astype(np.int64))
+        sizes[rng.random(P) < 0.05] = 0
+        b_min = int(rng.integers(1, 5000))
+        A = agg.run_aggregator(range(P), sizes, b_min, b_min * int(rng.integers(2, 6)))
+        N = int(sizes.sum())
+        F = len(A.flushes)
+        assert F <= agg.theorem_flush_bound(N, P, b_min)
+        keys = [k for sb in A.flushes for k in sb.keys] + A.empty_keys
+        assert sorted(keys) == list(range(P))
+        assert sum(sb.total for sb in A.flushes) == N
+        # (F-1)*B_min + 1 <= N  (every non-final flush holds >= B_min texts)
+        if F:
+            assert (F - 1) * b_min + 1 <= N
+
+
+def test_flush_count_paper_workload():
+    """tab:threshold P:878: 89 flushes and 44.9 partitions per SuperBatch at 10M / B_min=100K.
+
+    Our rescaled generator (DESIGN.md input recipe) is not the paper's data, so this is a
+    soft band around the printed values; the hard check is the Theorem's upper bound F <= 100.
+    """
+    g = GOLD["flush_count_10M"]
+    Fs, pps = [], []
+    for seed in range(3):
+        w = WORKLOADS["minilm"]
+        sizes = partition_sizes(w, np.random.Generator(np.random.PCG64(seed)))
+        assert sizes.sum() == g["n_texts"]
+        A = agg.run_aggregator(range(len(sizes)), sizes, g["b_min"], g["b_max"])
+        assert len(A.flushes) <= g["theorem_F"]
+        Fs.append(len(A.flushes))
+        pps.append(len(sizes) / len(A.flushes))
+    assert abs(np.mean(Fs) - g["flushes"]) <= 8
+    assert abs(np.mean(pps) - g["parts_per_superbatch"]) <= 5
+
+
+def test_fill_ratio_monte_carlo():
+    """O10: E[S/B_min] -> 1 + sigma^2/(2 mu B_min) (eq:fill-ratio) within +-0.02."""
+    g = GOLD["fill_ratio"]
+    mu, sd, b_min = g["mu"], g["sigma"], g["b_min"]
+    assert agg.fill_ratio_prediction(mu, sd, b_min) == pytest.approx(g["formula"], abs=1e-4)
+    assert round(agg.fill_ratio_prediction(mu, sd, b_min), 2) == g["printed"]
+    s2 = math.log(1 + (sd / mu) ** 2)
+    rng = np.random.default_rng(11)
+    sizes = np.maximum(1, np.rint(rng.lognormal(math.log(mu) - s2 / 2, math.sqrt(s2), size=200_000))).astype(np.int64)
+    A = agg.run_aggregator(range(len(sizes)), sizes, b_min, 10**12)
+    ratios = [sb.total / b_min for sb in A.flushes if sb.reason == agg.EFFICIENCY]
+    assert len(ratios) >= 10_000
+    assert abs(np.mean(ratios) - g["formula"]) <= g["mc_tolerance"]
+
+
+def test_errors():
+    with pytest.raises(ValueError):
+        agg.Aggregator(10, 10)
+    A = agg.Aggregator(10, 20)
+    A.add_partition("a", 3)
+    with pytest.raises(agg.DuplicateKey):
+        A.add_partition("a", 1)
+    A.finish()
+    with pytest.raises(RuntimeError):
+        A.add_partition("b", 1)
+
+
+def test_zero_text_partitions_do_not_enter_buffer():
+    A = agg.run_aggregator(["a", "b", "c"], [0, 5, 0], 3, 10)
+    assert A.empty_keys == ["a", "c"]
+    assert [sb.keys for sb in A.flushes] == [["b"]]
+
+
+def test_pack_brute_force():
+    """O12 packing: cu monotone, cu[0]=0, cu[S]=T, offsets equal brute-force sums."""
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        sizes = list(rng.integers(1, 30, size=int(rng.integers(1, 12))))
+        lengths = rng.integers(1, 513, size=sum(sizes))
+        p = agg.pack(lengths, sizes)
+        assert p.cu_seqlens[0] == 0 and p.cu_seqlens[-1] == lengths.sum()
+        assert np.all(np.diff(p.cu_seqlens) == lengths)
+        for j in range(len(sizes) + 1):
+            r = sum(sizes[:j])
+            assert p.part_row_off[j] == r
+            assert p.part_tok_off[j] == sum(int(x) for x in lengths[:r])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_lpt_brute_force(world):
+    """O12 LPT: rule re-checked step by step; cover-once; piece <= U unless one text; makespan bound."""
+    rng = np.random.default_rng(world)
+    for _ in range(10):
+        sizes = list(rng.integers(1, 400, size=int(rng.integers(1, 40))))
+        lengths = rng.integers(1, 200, size=sum(sizes))
+        pieces, per_rank = agg.lpt_plan(lengths, sizes, world)
+        T = int(lengths.sum())
+        # cover every row exactly once, in order, pieces inside one member
+        cover = np.zeros(sum(sizes), dtype=int)
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        for p in pieces:
+            cover[p.first_row:p.first_row + p.n_rows] += 1
+            assert off[p.member] <= p.first_row and p.first_row + p.n_rows <= off[p.member + 1]
+            assert p.tokens == lengths[p.first_row:p.first_row + p.n_rows].sum()
+        assert np.all(cover == 1)
+        if world == 1:
+            assert len(pieces) == len(sizes)
+            continue
+        U = math.ceil(T / (8 * world))
+        for p in pieces:
+            assert p.tokens <= U or p.n_rows == 1
+        # replay greedy: each piece (in (tokens desc, first_row asc) order) went to an argmin-load rank
+        load = [0] * world
+        for p in sorted(pieces, key=lambda p: (-p.tokens, p.first_row)):
+            best = min(load)
+            assert load[p.rank] == best and p.rank == load.index(best)
+            load[p.rank] += p.tokens
+        assert max(load) <= T / world + max(p.tokens for p in pieces)
+        for r in range(world):
+            rows = [p.first_row for p in per_rank[r]]
+            assert rows == sorted(rows)
+
+
+def test_determinism():
+    """O14: same recipe and seed -> byte-identical inputs and identical SuperBatches."""
+    w = WORKLOADS["toy"]
+    e = ENCODERS["toy"]
+    a = make_workload(w, e.vocab_size, e.max_position, seed=2)
+    b = make_workload(w, e.vocab_size, e.max_position, seed=2)
+    assert a.ids.tobytes() == b.ids.tobytes() and a.lengths.tobytes() == b.lengths.tobytes()
+    A = agg.run_aggregator(a.keys, a.sizes, w.b_min, w.b_max)
+    B = agg.run_aggregator(b.keys, b.sizes, w.b_min, w.b_max)
+    assert [(s.reason, s.keys) for s in A.flushes] == [(s.reason, s.keys) for s in B.flushes]
+
+
+def test_toy_safety_variant_hits_safety():
+    """C1-safety variant (largest-last, B_max=96) exercises the Safety branch."""
+    w = WORKLOADS["toy_safety"]
+    e = ENCODERS["toy"]
+    hits = 0
+    for seed in range(5):
+        wl = make_workload(w, e.vocab_size, e.max_position, seed=seed)
+        A = agg.run_aggregator(wl.keys, wl.sizes, w.b_min, w.b_max)
+        hits += any(sb.reason == agg.SAFETY for sb in A.flushes)
+    assert hits >= 3

@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""bench.py -- SURGE hot path on B200: texts/s for 10M texts, P=4,000 log-normal(sigma=1.72)
+partitions, MiniLM-L6-class encoder (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One STEP = the whole hot path over the whole 10M-text workload: Alg.1 aggregation (surge_aggregate)
+-> per SuperBatch surge_encode_superbatch (LPT shard, K1 pack, encoder chain, K9 pool, rows into the
+output).  `value`: inputs resident in HBM, CUDA events on the launching stream, max over ranks.
+`e2e`: the streaming C ABI (surge_submit_partition / poll / release) from host buffers, H2D of the
+ids and D2H of the embeddings inside the timed region.  N > 1: one process per GPU (torchrun);
+every SuperBatch is LPT-split across ranks (strong scaling; no per-batch collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.configs import ENCODERS, WORKLOADS, scaled  # noqa: E402
+from synth.weights import make_weights, pack_blob  # noqa: E402
+from synth.workload import make_workload  # noqa: E402
+
+METRIC = "texts/sec (10M texts, P=4000, MiniLM-L6) at 1/2/4/8 B200; TTFO; % TC peak"
+UNIT = "texts/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="minilm")
+    ap.add_argument("--n-texts", type=int, default=0, help="override N (default: the config's 10M)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--chunk-tokens", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile-run", action="store_true",
+                    help="for ncu: one SuperBatch, no e2e/baseline/JSON timing")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks line of B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(ecfg, w, wl, seconds: float, one_step: bool = False):
+    """The oracle (fp64 numpy, as it stands) on host cores over a bounded sample of the workload."""
+    from threadpoolctl import threadpool_limits
+    from oracle import aggregator as oagg
+    from oracle import encoder as oenc
+    E = oenc.Encoder(ecfg, w)
+    t0 = time.perf_counter()
+    oagg.run_aggregator(range(len(wl.sizes)), wl.sizes, wl.cfg.b_min, wl.cfg.b_max)   # full-stream Alg.1
+    t_agg = time.perf_counter() - t0
+    n = 0
+    tok = 0
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        off = 0
+        while True:
+            l = int(wl.lengths[n])
+            E.encode_text(wl.ids[off:off + l])
+            off += l
+            tok += l
+            n += 1
+            if time.perf_counter() - t0 >= seconds or n >= wl.n_texts:
+                break
+        dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {n} texts ({tok} tokens) of the stream, fp64 per-text encode, 1 thread; "
+                      f"plus Alg.1 over all {len(wl.sizes)} partitions in {t_agg:.3f}s",
+            "texts": n, "seconds": dt}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle timed on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    ecfg = ENCODERS["minilm"]
+    wcfg = WORKLOADS[args.workload]
+    if args.n_texts:
+        wcfg = scaled(wcfg, n_texts=args.n_texts)
+    w = make_weights(ecfg, seed=1234)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
+    from threadpoolctl import threadpool_limits
+    from oracle import aggregator as oagg
+    from oracle import encoder as oenc
+    E = oenc.Encoder(ecfg, w)
+    per_step = 256
+    times = []
+    with threadpool_limits(limits=1):
+        off_t = 0
+        pos = 0
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oagg.run_aggregator(range(len(wl.sizes)), wl.sizes, wcfg.b_min, wcfg.b_max)
+            for _ in range(per_step):
+                l = int(wl.lengths[pos])
+                E.encode_text(wl.ids[off_t:off_t + l])
+                off_t += l
+                pos += 1
+            if step >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    v = per_step * len(times) / sum(times)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.workload}: N={wcfg.n_texts}, P={wcfg.n_partitions}, sigma={wcfg.sigma}, "
+                                   f"MiniLM-L6 class (d=384, 6 layers), B_min={wcfg.b_min}, B_max={wcfg.b_max}",
+                       "step": f"Alg.1 over all partitions + oracle encode of {per_step} texts"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} texts per step, consecutive in stream order"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "ours":
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import torch
+    from paper_2605_01060_b200 import native as N
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ecfg = ENCODERS["minilm"]
+    wcfg = WORKLOADS[args.workload]
+    if args.n_texts:
+        wcfg = scaled(wcfg, n_texts=args.n_texts)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
+    # weights: rank 0 draws them; one NCCL broadcast over NVLink replicates them (K11)
+    w = make_weights(ecfg, seed=1234) if rank == 0 or world == 1 else None
+    n_w = sum(int(np.prod(s)) for s in [v.shape for v in (w or make_weights_shapes(ecfg)).values()])
+    if rank == 0 or world == 1:
+        blob_dev = torch.from_numpy(pack_blob(ecfg, w).view(np.int16)).to(dev)
+    else:
+        blob_dev = torch.empty(n_w, dtype=torch.int16, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast(blob_dev, src=0)
+    cfg = N.make_config(ecfg, wcfg.b_min, wcfg.b_max, rank=rank, world_size=world, device=local,
+                        chunk_tokens=args.chunk_tokens, weights_on_device=1)
+    h = N.surge_create(cfg, blob_dev, n_weights=blob_dev.numel())
+    stream = torch.cuda.Stream(device=dev)
+
+    sizes = wl.sizes.astype(np.int64)
+    d_ids = torch.from_numpy(wl.ids).to(dev)
+    d_len = torch.from_numpy(wl.lengths).to(dev)
+    d_out = torch.empty(wl.n_texts, ecfg.hidden, dtype=torch.float32, device=dev)
+    text_off, tok_off = wl.text_off, wl.tok_off
+
+    def step(limit_sb=None):
+        sbs, _ = N.surge_aggregate(sizes, wcfg.b_min, wcfg.b_max)         # a1 (host, Alg.1)
+        for j, (a, b, _r) in enumerate(sbs):
+            if limit_sb is not None and j >= limit_sb:
+                break
+            t0, t1 = int(text_off[a]), int(text_off[b])
+            k0 = int(tok_off[a])
+            N.surge_encode_superbatch(h, d_ids.data_ptr() + 4 * k0, d_len.data_ptr() + 4 * t0,
+                                      wl.lengths[t0:t1], sizes[a:b], d_out.data_ptr() + 4 * t0 * ecfg.hidden,
+                                      stream)
+        return len(sbs)
+
+    if args.profile_run:
+        step(limit_sb=1)
+        torch.cuda.synchronize()
+        step(limit_sb=2)
+        torch.cuda.synchronize()
+        print("profile run done", flush=True)
+        return
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st0 = N.surge_get_stats(h)
+    N.surge_profile_enable(h, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        F = 0
+        for _ in range(args.steps):
+            F = step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = N.surge_profile_read(h)
+    N.surge_profile_enable(h, False)
+    st1 = N.surge_get_stats(h)
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = wl.n_texts * args.steps / (ms_max / 1e3)
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+
+    # roofline of the dominant kernel class (largest device-time share)
+    peaks = measured_peaks()
+    tc_peak = peaks.get("bf16_tflops_sustained") or 1399.5
+    hbm_peak = peaks.get("hbm_gbs") or 6553.6
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    P = prof[dom]
+    total_kernel_ms = sum(v["ms"] for v in prof.values())
+    if P["flops"] > 0 and dom.startswith("gemm"):
+        achieved = P["flops"] / (P["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": achieved / tc_peak}
+    else:
+        achieved = P["bytes"] / (P["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak}
+    roof.update({"kernel": dom, "traffic": ncu_traffic(dom), "share_of_kernel_time": P["ms"] / total_kernel_ms,
+                 "launches": P["launches"], "avg_launch_us": 1e3 * P["ms"] / max(P["launches"], 1),
+                 "peak_source": "MEASURED_PEAKS.json " + ("bf16_tflops_sustained" if roof["bound"] == "tensor"
+                                                          else "hbm_gbs")})
+    gemm_flops = sum(v["flops"] for k, v in prof.items() if k.startswith("gemm"))
+    gemm_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("gemm"))
+    all_flops = sum(v["flops"] for v in prof.values())
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: N={wl.n_texts} texts ({wl.n_tokens} tokens), "
+                                   f"P={wcfg.n_partitions} log-normal sigma={wcfg.sigma}, MiniLM-L6 class "
+                                   f"(d=384, 6 layers, 12 heads, ffn 1536, random-init bf16), "
+                                   f"B_min={wcfg.b_min}, B_max={wcfg.b_max}",
+                       "superbatches_per_step": F, "parallelism": f"lpt{world}",
+                       "l2": "inputs (ids 565 MB) and outputs (15.4 GB) larger than L2; no explicit flush",
+                       "chunk_tokens": cfg.chunk_tokens or 131072},
+            "tokens_per_s": wl.n_tokens * args.steps / (ms_max / 1e3),
+            "tc_fraction_of_sustained": all_flops / (ms_max / 1e3) / 1e12 / tc_peak,   # this rank's share
+            "gemm_tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,
+            "kernel_profile": {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"] // args.steps,
+                                   "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12 if v["flops"] else None,
+                                   "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9}
+                               for k, v in prof.items() if v["launches"]},
+            "roofline": roof, "gpu_launches": launches}
+
+    # ---------------------------------------------------------------- e2e through the streaming ABI
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(N, h, wl, args, world, rank, dev)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(ecfg, w, wl, args.cpu_seconds)
+    line["clocks"] = clk.summary()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    N.surge_destroy(h)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def make_weights_shapes(ecfg):
+    from synth.weights import blob_layout
+    return {n: np.zeros(s, dtype=np.uint8) for n, s in blob_layout(ecfg)}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if present."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_e2e(N, h, wl, args, world, rank, dev):
+    """Streaming C ABI from host memory: submit every partition, poll + release, finish, drain."""
+    import torch
+    parts = [wl.partition(k) for k in range(len(wl.sizes))]
+
+    def one():
+        n_rows = 0
+        for key, ids, lens in parts:
+            N.surge_submit_partition(h, key, ids, lens)
+            for r in N.surge_poll_flushed(h, 4096, 0):
+                n_rows += r.n_rows
+                N.surge_release(h, r)
+        N.surge_finish(h)
+        while N.surge_pending(h) > 0:
+            for r in N.surge_poll_flushed(h, 4096, 20):
+                n_rows += r.n_rows
+                N.surge_release(h, r)
+        for r in N.surge_poll_flushed(h, 4096, 0):
+            n_rows += r.n_rows
+            N.surge_release(h, r)
+        st = N.surge_get_stats(h)
+        N.surge_reset(h)
+        return n_rows, st
+
+    one()   # warm-up (pinned pools)
+    times, stats, rows = [], None, 0
+    for _ in range(max(1, args.e2e_steps)):
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        t0 = time.perf_counter()
+        rows, stats = one()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": wl.n_texts / t, "unit": UNIT,
+            "h2d_bytes_per_step": int(4 * (stats["local_tokens"] + stats["local_texts"])),
+            "d2h_bytes_per_step": int(stats["local_texts"]) * 384 * 4,
+            "steps": len(times), "ttfo_s": stats["ttfo_s"], "peak_buffered_texts": stats["peak_buffered_texts"],
+            "lemma_bound_texts": int(wl.cfg.b_min - 1 + int(wl.sizes.max())),
+            "peak_inflight_texts": stats["peak_inflight_texts"], "superbatches": stats["superbatches"],
+            "safety_flushes": stats["safety_flushes"], "rows_delivered": rows,
+            "encode_ms_total": stats["encode_ms_total"],
+            "host_peak_rss_gb": peak_rss_gb()}
+
+
+def peak_rss_gb():
+    try:
+        for line in open("/proc/self/status"):
+            if line.startswith("VmHWM:"):
+                return int(line.split()[1]) / 1e6
+    except Exception:
+        pass
+    return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,309 @@
+// gemm_tc.cu -- K4/K6/K7/K8: bf16 GEMM on 5th-gen tensor cores (tcgen05.mma, accumulators in
+// TMEM, operands staged by TMA with 128-byte swizzle) with fused epilogues:
+//   EPI_BIAS      C = A B^T + b                          (QKV projection, K4)
+//   EPI_BIAS_GELU C = GELU_erf(A B^T + b)                (FFN1, K7)
+//   EPI_BIAS_LN   C = LN(A B^T + b + R) * gamma + beta   (attention out-proj K6, FFN2 K8)
+// A: [M x K] activations (row-major, K contiguous), B: [N x K] weights (HF nn.Linear [out,in]).
+//
+// Design: one CTA per 128 x BN output tile, warp-specialised:
+//   warp 0 (one lane)  TMA producer: A box 64x128, B box 64x(BN or BN/2) per K-block, STAGES ring
+//   warp 1             TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256 per MMA)
+//   warps 2..5         epilogue: tcgen05.ld 32x32b -> registers -> bias/GELU/residual+LN -> bf16
+// Rows >= M of the last tile are zero-filled by TMA and never stored.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace surge {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                       // 64 bf16 = 128 B = one swizzle row
+constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
+constexpr int GEMM_THREADS = 192;            // 6 warps
+
+template <int BN>
+struct TileCfg {
+  static constexpr int B_BOX = (BN <= 256) ? BN : BN / 2;       // TMA box rows for B
+  static constexpr int N_LOADS = BN / B_BOX;
+  static constexpr int MMA_N = B_BOX;                            // <= 256, multiple of 16
+  static constexpr int N_MMA = BN / MMA_N;
+  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+  static constexpr int STAGES = (BN >= 384) ? 3 : 4;
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
+  static_assert(B_BOX * N_LOADS == BN, "B box split");
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
+                   const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
+                   float eps) {
+  using T = TileCfg<BN>;
+  constexpr int STAGES = T::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                   // STAGES x 16 KB
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;          // STAGES x B_STAGE_BYTES
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * T::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int num_kb = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, T::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      const uint64_t pol_w = l2_policy_evict_last();   // weights: re-read by every M tile
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], T::STAGE_BYTES);
+        tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
+#pragma unroll
+        for (int j = 0; j < T::N_LOADS; ++j)
+          tma_load_2d_hint(sB + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
+                           n0 + j * T::B_BOX, pol_w);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
+        const uint32_t b0 = smem_u32(sB + s * T::B_STAGE_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+#pragma unroll
+          for (int j = 0; j < T::N_MMA; ++j) {
+            tc_mma_bf16(tmem_base + j * T::MMA_N, umma_desc_sw128(a0 + k * 32),
+                        umma_desc_sw128(b0 + j * T::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+          }
+        }
+        tc_commit(&empty[s]);                 // frees this smem stage when the MMAs retire
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+      tc_commit(tmem_full);                   // accumulator complete
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;                   // TMEM lane quadrant this warp may access
+    const int row = m0 + q * 32 + lane;
+    const bool ok = row < M;
+    const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
+      uint16_t* crow = C + size_t(row) * N + n0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c, r);
+        tmem_ld_wait();
+        uint32_t p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float v0 = __uint_as_float(r[2 * i]) + __ldg(bias + n0 + c + 2 * i);
+          float v1 = __uint_as_float(r[2 * i + 1]) + __ldg(bias + n0 + c + 2 * i + 1);
+          if constexpr (EPI == EPI_BIAS_GELU) {
+            v0 = gelu_erf(v0);
+            v1 = gelu_erf(v1);
+          }
+          p[i] = pack_bf16x2(v0, v1);
+        }
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(crow + c);
+          dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+          dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        }
+      }
+    } else {
+      // LayerNorm over the full row (BN == N): pass 1 statistics, pass 2 normalise + store.
+      const uint16_t* rrow = res + size_t(ok ? row : 0) * N;
+      uint16_t* crow = C + size_t(row) * N;
+      float shift = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c, r);
+        tmem_ld_wait();
+        const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
+        const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
+        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float v = __uint_as_float(r[i]) + __ldg(bias + c + i) + ((i & 1) ? bf16hi(rr[i >> 1]) : bf16lo(rr[i >> 1]));
+          if (c == 0 && i == 0) shift = v;    // shifted sums: var is shift-invariant, less cancellation
+          const float t = v - shift;
+          s1 += t;
+          s2 += t * t;
+        }
+      }
+      const float inv_n = 1.0f / float(BN);
+      const float mt = s1 * inv_n;
+      const float var = fmaxf(s2 * inv_n - mt * mt, 0.f);
+      const float mean = shift + mt;
+      const float rstd = rsqrtf(var + eps);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c, r);
+        tmem_ld_wait();
+        const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
+        const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
+        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+        uint32_t p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j0 = 2 * i, j1 = 2 * i + 1;
+          float v0 = __uint_as_float(r[j0]) + __ldg(bias + c + j0) + bf16lo(rr[i]);
+          float v1 = __uint_as_float(r[j1]) + __ldg(bias + c + j1) + bf16hi(rr[i]);
+          v0 = (v0 - mean) * rstd * __ldg(gamma + c + j0) + __ldg(beta + c + j0);
+          v1 = (v1 - mean) * rstd * __ldg(gamma + c + j1) + __ldg(beta + c + j1);
+          p[i] = pack_bf16x2(v0, v1);
+        }
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(crow + c);
+          dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+          dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, T::TMEM_COLS);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+
+template <int BN, int EPI>
+cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
+  using T = TileCfg<BN>;
+  static bool attr_set = false;
+  auto kern = gemm_tc_kernel<BN, EPI>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((g.M + BM - 1) / BM, g.N / BN);
+  kern<<<grid, GEMM_THREADS, T::SMEM_BYTES, st>>>(*g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
+                                                  g.beta, g.C, g.eps);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t init_tma_encoder() {
+  if (g_encode_tiled) return cudaSuccess;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess) return e;
+  if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorSymbolNotFound;
+  g_encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return cudaSuccess;
+}
+
+// Row-major bf16 matrix [rows x cols] (cols contiguous), box = 64 cols x box_rows, 128 B swizzle.
+cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  if (!g_encode_tiled) {
+    cudaError_t e = init_tma_encoder();
+    if (e != cudaSuccess) return e;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int gemm_bn_for(int N, int epi) {
+  if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
+  if (N % 384 == 0 && N >= 1152) return 384;
+  if (N % 256 == 0) return 256;
+  if (N % 192 == 0) return 192;
+  if (N % 128 == 0) return 128;
+  if (N % 64 == 0) return 64;
+  return 0;
+}
+
+uint32_t gemm_b_box_rows(int BN) { return BN <= 256 ? BN : BN / 2; }
+
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
+  const int BN = gemm_bn_for(g.N, g.epi);
+  if (BN == 0 || g.K % BK != 0 || g.K <= 0 || g.M <= 0) return cudaErrorInvalidValue;
+  switch (g.epi) {
+    case EPI_BIAS:
+      switch (BN) {
+        case 64: return launch_gemm_t<64, EPI_BIAS>(g, st);
+        case 128: return launch_gemm_t<128, EPI_BIAS>(g, st);
+        case 192: return launch_gemm_t<192, EPI_BIAS>(g, st);
+        case 256: return launch_gemm_t<256, EPI_BIAS>(g, st);
+        case 384: return launch_gemm_t<384, EPI_BIAS>(g, st);
+      }
+      break;
+    case EPI_BIAS_GELU:
+      switch (BN) {
+        case 64: return launch_gemm_t<64, EPI_BIAS_GELU>(g, st);
+        case 128: return launch_gemm_t<128, EPI_BIAS_GELU>(g, st);
+        case 192: return launch_gemm_t<192, EPI_BIAS_GELU>(g, st);
+        case 256: return launch_gemm_t<256, EPI_BIAS_GELU>(g, st);
+        case 384: return launch_gemm_t<384, EPI_BIAS_GELU>(g, st);
+      }
+      break;
+    case EPI_BIAS_LN:
+      switch (BN) {
+        case 64: return launch_gemm_t<64, EPI_BIAS_LN>(g, st);
+        case 384: return launch_gemm_t<384, EPI_BIAS_LN>(g, st);
+      }
+      break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace surge

@@ -1,0 +1,134 @@
+// internal.h -- declarations shared by libsurge's translation units (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace surge {
+
+enum Epilogue : int { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_BIAS_LN = 2 };
+
+struct GemmArgs {
+  const CUtensorMap* tmA;   // A [M x K]
+  const CUtensorMap* tmB;   // B [N x K]
+  int64_t M;
+  int N, K, epi;
+  const float* bias;
+  const uint16_t* res;      // [M x N] (EPI_BIAS_LN)
+  const float* gamma;
+  const float* beta;
+  uint16_t* C;              // [M x N]
+  float eps;
+};
+
+cudaError_t init_tma_encoder();
+cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+int gemm_bn_for(int N, int epi);
+uint32_t gemm_b_box_rows(int BN);
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);
+
+// K1: cu[0..n], row_off[0..m], tok_off[0..m] (single CTA)
+cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes, int64_t m, int32_t* cu,
+                        int32_t* row_off, int32_t* tok_off, cudaStream_t st);
+// K3: tokens of texts [0, n_texts) described by cu (absolute offsets), activations indexed cu[i]-tok0
+cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_texts, int32_t tok0,
+                            const uint16_t* word, const uint16_t* pos, const uint16_t* type, const float* gamma,
+                            const float* beta, int d, float eps, uint16_t* x, cudaStream_t st);
+// K5
+cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0, int heads,
+                             int head_dim, uint16_t* out, cudaStream_t st);
+// K9
+cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
+                               float* out, cudaStream_t st);
+
+cudaError_t launch_bf16_to_f32(const uint16_t* in, float* out, int64_t n, cudaStream_t st);
+
+// --------------------------------------------------------------------- per-kernel-class timing
+enum KernelKind : int {
+  KK_EMBED = 0, KK_QKV = 1, KK_ATTN = 2, KK_OUT_LN = 3, KK_FFN1 = 4, KK_FFN2 = 5, KK_POOL = 6, KK_PACK = 7,
+  KK_COUNT = 8
+};
+
+// Records a CUDA event pair around launches of each kind (only when enabled).  Not thread-safe:
+// one Profiler per launching thread/stream.
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+    double fl, by;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  int64_t launches[KK_COUNT] = {};
+  double ms[KK_COUNT] = {}, flops[KK_COUNT] = {}, bytes[KK_COUNT] = {};
+  cudaEvent_t take();
+  void begin(cudaStream_t st, cudaEvent_t* a);
+  void end(int kind, cudaStream_t st, cudaEvent_t a, double fl, double by);
+  cudaError_t resolve();   // sync-free if the events completed; call after stream sync
+  void clear();
+  ~Profiler();
+};
+
+// ------------------------------------------------------------------------------ device model
+struct ModelShape {
+  int vocab, max_pos, type_vocab, d, layers, heads, ffn;
+  float eps;
+};
+
+struct LayerW {
+  uint16_t *wqkv, *wo, *w1, *w2;      // bf16 [3d x d], [d x d], [ff x d], [d x ff]
+  float *bqkv, *bo, *ln1_g, *ln1_b, *b1, *b2, *ln2_g, *ln2_b;
+  CUtensorMap tm_wqkv, tm_wo, tm_w1, tm_w2;
+};
+
+// Activation workspace for one chunk of <= cap tokens (bf16): X, QKV, O, X1, H.
+struct Workspace {
+  int64_t cap = 0;
+  uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
+  cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
+  void release();
+  ~Workspace() { release(); }
+};
+
+// Owns the encoder weights on one device and runs the encoder chain (K3, K4-K8, K5, K9).
+class DeviceModel {
+ public:
+  DeviceModel() = default;
+  ~DeviceModel();
+  // blob: HF-order bf16 weights (host or device pointer), layout of include/surge.h.
+  cudaError_t init(const ModelShape& s, const uint16_t* blob, bool blob_on_device, cudaStream_t st);
+  // Texts [s0, s1) of a packed stream: d_ids/d_cu absolute (cu[i] = first token of text i),
+  // activations chunk-local (token t at row t - tok0); writes d_out rows [s0, s1) (fp32 [n x d]).
+  // host_cu (optional, absolute, indexed like d_cu) is only read when prof is enabled.
+  cudaError_t encode_chunk(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, int64_t s0, int64_t s1,
+                           int32_t tok0, int32_t ntok, float* d_out, cudaStream_t st, int64_t* launches,
+                           Profiler* prof = nullptr, const int32_t* host_cu = nullptr) const;
+  // All texts [0, n): cuts chunks of <= ws.cap tokens at text boundaries using host_cu.
+  cudaError_t encode(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, const int32_t* host_cu,
+                     int64_t n_texts, float* d_out, cudaStream_t st, int64_t* launches,
+                     Profiler* prof = nullptr) const;
+  const ModelShape& shape() const { return s_; }
+  const uint16_t* word() const { return word_; }
+  const uint16_t* pos() const { return pos_; }
+  const uint16_t* type() const { return type_; }
+  const float* emb_g() const { return emb_g_; }
+  const float* emb_b() const { return emb_b_; }
+
+ private:
+  ModelShape s_{};
+  std::vector<void*> allocs_;
+  uint16_t *word_ = nullptr, *pos_ = nullptr, *type_ = nullptr;
+  float *emb_g_ = nullptr, *emb_b_ = nullptr;
+  std::vector<LayerW> layers_;
+  cudaError_t dalloc(void** p, size_t bytes);
+};
+
+// Elements in the HF-order weight blob for shape s.
+size_t blob_elems(const ModelShape& s);
+
+}  // namespace surge

@@ -1,0 +1,264 @@
+// model.cu -- device-resident BERT-class encoder (weights + chunked encoder chain).
+//
+// Per chunk of whole texts (<= Workspace::cap tokens), the chain is:
+//   K3 embed+LN -> L x [ K4 QKV GEMM(+bias) -> K5 varlen attention -> K6 out-proj GEMM(+bias+res+LN)
+//                        -> K7 FFN1 GEMM(+bias+GELU) -> K8 FFN2 GEMM(+bias+res+LN) ] -> K9 meanpool+L2
+// Activations are bf16 in HBM between kernels; all math is fp32 inside the kernels.
+#include <cstring>
+
+#include "internal.h"
+
+namespace surge {
+
+size_t blob_elems(const ModelShape& s) {
+  const size_t d = s.d, f = s.ffn;
+  size_t n = size_t(s.vocab + s.max_pos + s.type_vocab) * d + 2 * d;
+  n += size_t(s.layers) * (4 * (d * d + d) + 2 * d + (f * d + f) + (d * f + d) + 2 * d);
+  return n;
+}
+
+cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
+  release();
+  const size_t t = size_t(cap_tokens);
+  cudaError_t e;
+  if ((e = cudaMalloc(&X, t * s.d * 2)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&QKV, t * 3 * s.d * 2)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&O, t * s.d * 2)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&X1, t * s.d * 2)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&H, t * s.ffn * 2)) != cudaSuccess) return e;
+  cap = cap_tokens;
+  return cudaSuccess;
+}
+
+void Workspace::release() {
+  for (uint16_t** p : {&X, &QKV, &O, &X1, &H}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  cap = 0;
+}
+
+DeviceModel::~DeviceModel() {
+  for (void* p : allocs_) cudaFree(p);
+}
+
+cudaError_t DeviceModel::dalloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess) allocs_.push_back(*p);
+  return e;
+}
+
+#define SURGE_TRY(x)                   \
+  do {                                 \
+    cudaError_t _e = (x);              \
+    if (_e != cudaSuccess) return _e;  \
+  } while (0)
+
+cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool blob_on_device, cudaStream_t st) {
+  s_ = s;
+  const size_t n = blob_elems(s);
+  uint16_t* dblob = nullptr;
+  SURGE_TRY(cudaMalloc(&dblob, n * 2));
+  cudaError_t e = cudaMemcpyAsync(dblob, blob, n * 2, blob_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) { cudaFree(dblob); return e; }
+
+  size_t off = 0;
+  // copy a bf16 tensor of `cnt` elements out of the blob into its own allocation
+  auto take_bf16 = [&](uint16_t** dst, size_t cnt) -> cudaError_t {
+    SURGE_TRY(dalloc(reinterpret_cast<void**>(dst), cnt * 2));
+    SURGE_TRY(cudaMemcpyAsync(*dst, dblob + off, cnt * 2, cudaMemcpyDeviceToDevice, st));
+    off += cnt;
+    return cudaSuccess;
+  };
+  auto take_f32 = [&](float** dst, size_t cnt) -> cudaError_t {
+    SURGE_TRY(dalloc(reinterpret_cast<void**>(dst), cnt * 4));
+    SURGE_TRY(launch_bf16_to_f32(dblob + off, *dst, int64_t(cnt), st));
+    off += cnt;
+    return cudaSuccess;
+  };
+  const size_t d = s.d, f = s.ffn;
+  e = [&]() -> cudaError_t {
+    SURGE_TRY(take_bf16(&word_, size_t(s.vocab) * d));
+    SURGE_TRY(take_bf16(&pos_, size_t(s.max_pos) * d));
+    SURGE_TRY(take_bf16(&type_, size_t(s.type_vocab) * d));
+    SURGE_TRY(take_f32(&emb_g_, d));
+    SURGE_TRY(take_f32(&emb_b_, d));
+    layers_.resize(s.layers);
+    for (int l = 0; l < s.layers; ++l) {
+      LayerW& L = layers_[l];
+      // Q, K, V weights are separated by their biases in the blob -> gather into [3d x d] / [3d]
+      SURGE_TRY(dalloc(reinterpret_cast<void**>(&L.wqkv), 3 * d * d * 2));
+      SURGE_TRY(dalloc(reinterpret_cast<void**>(&L.bqkv), 3 * d * 4));
+      for (int j = 0; j < 3; ++j) {
+        SURGE_TRY(cudaMemcpyAsync(L.wqkv + j * d * d, dblob + off, d * d * 2, cudaMemcpyDeviceToDevice, st));
+        off += d * d;
+        SURGE_TRY(launch_bf16_to_f32(dblob + off, L.bqkv + j * d, int64_t(d), st));
+        off += d;
+      }
+      SURGE_TRY(take_bf16(&L.wo, d * d));
+      SURGE_TRY(take_f32(&L.bo, d));
+      SURGE_TRY(take_f32(&L.ln1_g, d));
+      SURGE_TRY(take_f32(&L.ln1_b, d));
+      SURGE_TRY(take_bf16(&L.w1, f * d));
+      SURGE_TRY(take_f32(&L.b1, f));
+      SURGE_TRY(take_bf16(&L.w2, d * f));
+      SURGE_TRY(take_f32(&L.b2, d));
+      SURGE_TRY(take_f32(&L.ln2_g, d));
+      SURGE_TRY(take_f32(&L.ln2_b, d));
+      SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(gemm_bn_for(int(3 * d), EPI_BIAS))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(gemm_bn_for(int(d), EPI_BIAS_LN))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(gemm_bn_for(int(f), EPI_BIAS_GELU))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(gemm_bn_for(int(d), EPI_BIAS_LN))));
+    }
+    return cudaSuccess;
+  }();
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaFree(dblob);
+  if (e != cudaSuccess) return e;
+  if (off != n) return cudaErrorInvalidValue;
+  return e2;
+}
+
+// ------------------------------------------------------------------------------ profiler
+cudaEvent_t Profiler::take() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void Profiler::begin(cudaStream_t st, cudaEvent_t* a) {
+  *a = nullptr;
+  if (!on) return;
+  *a = take();
+  cudaEventRecord(*a, st);
+}
+void Profiler::end(int kind, cudaStream_t st, cudaEvent_t a, double fl, double by) {
+  if (!on || !a) return;
+  cudaEvent_t b = take();
+  cudaEventRecord(b, st);
+  recs.push_back({kind, a, b, fl, by});
+}
+cudaError_t Profiler::resolve() {
+  for (const Rec& r : recs) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return e;
+    e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) return e;
+    launches[r.kind] += 1;
+    ms[r.kind] += t;
+    flops[r.kind] += r.fl;
+    bytes[r.kind] += r.by;
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  recs.clear();
+  return cudaSuccess;
+}
+void Profiler::clear() {
+  for (const Rec& r : recs) {
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  recs.clear();
+  for (int k = 0; k < KK_COUNT; ++k) {
+    launches[k] = 0;
+    ms[k] = flops[k] = bytes[k] = 0;
+  }
+}
+Profiler::~Profiler() {
+  for (const Rec& r : recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
+cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, int64_t s0,
+                                      int64_t s1, int32_t tok0, int32_t ntok, float* d_out, cudaStream_t st,
+                                      int64_t* launches, Profiler* prof, const int32_t* host_cu) const {
+  const int64_t n = s1 - s0;
+  if (n <= 0) return cudaSuccess;
+  if (ntok > ws.cap) return cudaErrorInvalidValue;
+  const int d = s_.d, f = s_.ffn;
+  const int32_t* cu = d_cu + s0;
+  CUtensorMap tmX, tmO, tmX1, tmH;
+  SURGE_TRY(make_tmap_bf16(&tmX, ws.X, ntok, d, 128));
+  SURGE_TRY(make_tmap_bf16(&tmO, ws.O, ntok, d, 128));
+  SURGE_TRY(make_tmap_bf16(&tmX1, ws.X1, ntok, d, 128));
+  SURGE_TRY(make_tmap_bf16(&tmH, ws.H, ntok, f, 128));
+  const bool P = prof && prof->on;
+  double sum_l2 = 0;
+  if (P && host_cu)
+    for (int64_t i = s0; i < s1; ++i) {
+      const double l = double(host_cu[i + 1] - host_cu[i]);
+      sum_l2 += l * l;
+    }
+  const double M = ntok, D = d, F = f;
+  cudaEvent_t ev = nullptr;
+  int64_t k = 0;
+  if (P) prof->begin(st, &ev);
+  SURGE_TRY(launch_embed_ln(d_ids, cu, n, tok0, word_, pos_, type_, emb_g_, emb_b_, d, s_.eps, ws.X, st));
+  if (P) prof->end(KK_EMBED, st, ev, 0.0, M * (4 + 2 * D + 2 * D + 2 * D));
+  ++k;
+  for (const LayerW& L : layers_) {
+    GemmArgs g{};
+    g.M = ntok;
+    g.eps = s_.eps;
+    // K4: QKV = X Wqkv^T + b
+    g.tmA = &tmX; g.tmB = &L.tm_wqkv; g.N = 3 * d; g.K = d; g.epi = EPI_BIAS; g.bias = L.bqkv; g.C = ws.QKV;
+    if (P) prof->begin(st, &ev);
+    SURGE_TRY(launch_gemm(g, st));
+    if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
+    // K5: O = attention(QKV) per text
+    if (P) prof->begin(st, &ev);
+    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, s_.heads, d / s_.heads, ws.O, st));
+    if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
+    // K6: X1 = LN(O Wo^T + bo + X)
+    g.tmA = &tmO; g.tmB = &L.tm_wo; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
+    g.gamma = L.ln1_g; g.beta = L.ln1_b; g.C = ws.X1;
+    if (P) prof->begin(st, &ev);
+    SURGE_TRY(launch_gemm(g, st));
+    if (P) prof->end(KK_OUT_LN, st, ev, 2 * M * D * D, 2 * (M * D + D * D + 2 * M * D));
+    // K7: H = GELU(X1 W1^T + b1)
+    g.tmA = &tmX1; g.tmB = &L.tm_w1; g.N = f; g.K = d; g.epi = EPI_BIAS_GELU; g.bias = L.b1; g.res = nullptr;
+    g.gamma = g.beta = nullptr; g.C = ws.H;
+    if (P) prof->begin(st, &ev);
+    SURGE_TRY(launch_gemm(g, st));
+    if (P) prof->end(KK_FFN1, st, ev, 2 * M * F * D, 2 * (M * D + F * D + M * F));
+    // K8: X = LN(H W2^T + b2 + X1)
+    g.tmA = &tmH; g.tmB = &L.tm_w2; g.N = d; g.K = f; g.epi = EPI_BIAS_LN; g.bias = L.b2; g.res = ws.X1;
+    g.gamma = L.ln2_g; g.beta = L.ln2_b; g.C = ws.X;
+    if (P) prof->begin(st, &ev);
+    SURGE_TRY(launch_gemm(g, st));
+    if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
+    k += 5;
+  }
+  if (P) prof->begin(st, &ev);
+  SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));
+  if (P) prof->end(KK_POOL, st, ev, 0.0, M * 2 * D + double(n) * 4 * D);
+  ++k;
+  if (launches) *launches += k;
+  return cudaSuccess;
+}
+
+cudaError_t DeviceModel::encode(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, const int32_t* host_cu,
+                                int64_t n_texts, float* d_out, cudaStream_t st, int64_t* launches,
+                                Profiler* prof) const {
+  int64_t s0 = 0;
+  while (s0 < n_texts) {
+    int64_t s1 = s0 + 1;
+    while (s1 < n_texts && int64_t(host_cu[s1 + 1]) - host_cu[s0] <= ws.cap) ++s1;
+    const int32_t tok0 = host_cu[s0];
+    const int32_t ntok = host_cu[s1] - tok0;
+    SURGE_TRY(encode_chunk(ws, d_ids, d_cu, s0, s1, tok0, ntok, d_out, st, launches, prof, host_cu));
+    s0 = s1;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace surge

@@ -1,0 +1,201 @@
+"""End-to-end GPU parity: libsurge (C ABI, sm_100a) vs the oracle on the same seeded inputs.
+
+Gates (BASELINE.json north star):
+  bit-exact  SuperBatch membership/reasons/order, F, safety flushes, peak buffered texts,
+             per-partition row counts and row order, piece coverage;
+  embeddings per-row cos >= 0.999 and max|delta| <= 1e-2 on the unit vectors; |norm-1| <= 1e-5;
+  self-invariance: identical embeddings across SuperBatch compositions, PBP mode, the
+             device-level path, and rank splits (world_size 2 on one GPU).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import aggregator as oagg
+from oracle import encoder as oenc
+from synth.configs import ENCODERS, WORKLOADS, scaled
+from synth.weights import make_weights, pack_blob
+from synth.workload import make_workload
+
+pytestmark = pytest.mark.gpu
+
+COS_MIN, ABS_MAX, NORM_TOL = 0.999, 1e-2, 1e-5
+
+
+@pytest.fixture(scope="module")
+def N():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2605_01060_b200 import native
+    return native
+
+
+def texts_of(ids, lens):
+    off = np.concatenate([[0], np.cumsum(lens)])
+    return [ids[off[i]:off[i + 1]] for i in range(len(lens))]
+
+
+def compare(got: np.ndarray, ref: np.ndarray):
+    g = got.astype(np.float64)
+    cos = (g * ref).sum(1) / np.maximum(np.linalg.norm(g, axis=1) * np.linalg.norm(ref, axis=1), 1e-30)
+    assert g.shape == ref.shape
+    assert cos.min() >= COS_MIN, cos.min()
+    assert np.max(np.abs(g - ref)) <= ABS_MAX, np.max(np.abs(g - ref))
+    assert np.max(np.abs(np.linalg.norm(g, axis=1) - 1)) <= NORM_TOL
+    return float(cos.min()), float(np.max(np.abs(g - ref)))
+
+
+def run_lib(N, ecfg, w, wl, b_min, b_max, **kw):
+    from paper_2605_01060_b200 import SurgeEncoder
+    with SurgeEncoder(ecfg, pack_blob(ecfg, w), b_min, b_max, **kw) as enc:
+        out = enc.run(wl)
+        return out, enc.superbatches(), enc.stats(), enc.pieces
+
+
+def check_integer_parity(wl, sbs, stats, b_min, b_max):
+    A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, b_min, b_max)
+    assert [(s["reason"], s["members"]) for s in sbs] == [(s.reason, [int(k) for k in s.keys]) for s in A.flushes]
+    assert [s["n_texts"] for s in sbs] == [s.total for s in A.flushes]
+    assert stats["superbatches"] == len(A.flushes) <= oagg.theorem_flush_bound(int(wl.sizes.sum()), len(wl.sizes), b_min)
+    assert stats["safety_flushes"] == sum(s.reason == oagg.SAFETY for s in A.flushes)
+    assert stats["peak_buffered_texts"] == A.peak_buffered <= b_min - 1 + A.nmax_seen
+    return A
+
+
+@pytest.mark.parametrize("wname,init", [("toy", "surge"), ("toy", "pin"), ("toy_safety", "pin")])
+def test_toy_all_rows(N, wname, init):
+    ecfg, wcfg = ENCODERS["toy"], WORKLOADS[wname]
+    w = make_weights(ecfg, seed=1234, init=init)
+    E = oenc.Encoder(ecfg, w)
+    for seed in range(3):
+        wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=seed)
+        got, sbs, stats, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+        check_integer_parity(wl, sbs, stats, wcfg.b_min, wcfg.b_max)
+        assert set(got) == {int(k) for k in wl.keys}
+        for key, ids, lens in wl:
+            assert got[key].shape == (len(lens), ecfg.hidden)           # row count and order
+            compare(got[key], E.encode_texts(texts_of(ids, lens)))
+
+
+def test_minilm_multi_superbatch_sample(N):
+    """C2 shapes (d=384, 6 layers) on a scaled C2 recipe spanning several SuperBatches and chunks."""
+    ecfg = ENCODERS["minilm"]
+    wcfg = scaled(WORKLOADS["minilm"], n_texts=60_000, n_partitions=60, b_min=10_000, b_max=50_000)
+    w = make_weights(ecfg, seed=1234)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=0)
+    got, sbs, stats, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max, chunk_tokens=65536)
+    check_integer_parity(wl, sbs, stats, wcfg.b_min, wcfg.b_max)
+    E = oenc.Encoder(ecfg, w)
+    rng = np.random.default_rng(0)
+    for k, (key, ids, lens) in enumerate(wl):
+        n = len(lens)
+        rows = sorted({0, n - 1, *rng.integers(0, n, size=min(n, 6)).tolist()})
+        T = texts_of(ids, lens)
+        compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def test_edge_cases_and_errors(N):
+    from paper_2605_01060_b200 import SurgeEncoder
+    ecfg = ENCODERS["toy"]
+    w = make_weights(ecfg, seed=7, init="pin")
+    E = oenc.Encoder(ecfg, w)
+    enc = SurgeEncoder(ecfg, pack_blob(ecfg, w), 5, 8)
+    h = enc.h
+    try:
+        one = np.array([3], np.int32)
+        maxl = np.arange(4, 4 + ecfg.max_position, dtype=np.int32) % ecfg.vocab_size
+        parts = [(11, np.zeros(0, np.int32), np.zeros(0, np.int32)),          # empty partition
+                 (12, one, np.array([1], np.int32)),                          # one text of length 1
+                 (13, maxl, np.array([ecfg.max_position], np.int32)),         # length = max_position
+                 (14, np.concatenate([one, maxl, one]), np.array([1, ecfg.max_position, 1], np.int32)),
+                 (15, np.tile(one, 9), np.ones(9, np.int32))]                 # oversized: >= b_max alone
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_submit_partition(h, 99, np.array([1, 2], np.int32), np.array([ecfg.max_position + 1], np.int32))
+        assert ei.value.status == N.SURGE_E_TOO_LONG
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_submit_partition(h, 98, np.array([ecfg.vocab_size], np.int32), np.array([1], np.int32))
+        assert ei.value.status == N.SURGE_E_TOKEN_ID
+        got = enc.run(parts)
+        assert got[11].shape == (0, ecfg.hidden)
+        for key, ids, lens in parts[1:]:
+            compare(got[key], E.encode_texts(texts_of(ids, lens)))
+        sbs = enc.superbatches()
+        assert [s["reason"] for s in sbs] == ["efficiency", "safety"]   # 1+64+... crosses b_min; 9 >= b_max
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_submit_partition(h, 12, one, np.array([1], np.int32))
+        assert ei.value.status in (N.SURGE_E_DUPLICATE_ID, N.SURGE_E_STATE)
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_finish(h)
+        assert ei.value.status == N.SURGE_E_STATE
+        # reset -> a new stream on the same handle, duplicate id now allowed again
+        N.surge_reset(h)
+        got2 = enc.run(parts[1:3])
+        for key, ids, lens in parts[1:3]:
+            assert np.array_equal(got2[key], got[key])
+    finally:
+        enc.close()
+
+
+def test_duplicate_id_rejected(N):
+    ecfg = ENCODERS["toy"]
+    w = make_weights(ecfg)
+    h = N.surge_create(N.make_config(ecfg, 64, 320), pack_blob(ecfg, w))
+    try:
+        N.surge_submit_partition(h, 5, np.array([1, 2], np.int32), np.array([2], np.int32))
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_submit_partition(h, 5, np.array([1, 2], np.int32), np.array([2], np.int32))
+        assert ei.value.status == N.SURGE_E_DUPLICATE_ID
+    finally:
+        N.surge_destroy(h)
+
+
+def test_self_invariance_bit_exact(N):
+    """Each text's embedding must not depend on its SuperBatch: vary B_min, PBP mode (B_min=1),
+    chunk size, and the device-level entry point; all must be bit-identical."""
+    ecfg, wcfg = ENCODERS["minilm"], scaled(WORKLOADS["minilm"], n_texts=3000, n_partitions=12)
+    w = make_weights(ecfg, seed=1234)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=1)
+    base, _, _, _ = run_lib(N, ecfg, w, wl, 1000, 5000)
+    for b_min, b_max, chunk in ((1, 2, 0), (2500, 3000, 1024), (10**6, 10**7, 8192)):
+        other, sbs, _, _ = run_lib(N, ecfg, w, wl, b_min, b_max, chunk_tokens=chunk)
+        if b_min == 1:
+            assert len(sbs) == len(wl.sizes)                                # PBP: one SuperBatch per partition
+        for k in base:
+            assert np.array_equal(base[k], other[k]), (b_min, k)
+    # device-level path on the whole stream as one packed batch
+    h = N.surge_create(N.make_config(ecfg, 1000, 5000), pack_blob(ecfg, w))
+    try:
+        out = torch.zeros(wl.n_texts, ecfg.hidden, device="cuda")
+        N.surge_encode_packed(h, torch.from_numpy(wl.ids).cuda(), torch.from_numpy(wl.lengths).cuda(),
+                              wl.lengths, wl.n_texts, out)
+        torch.cuda.synchronize()
+        flat = out.cpu().numpy()
+        for k, (key, ids, lens) in enumerate(wl):
+            assert np.array_equal(flat[wl.text_off[k]:wl.text_off[k + 1]], base[key])
+    finally:
+        N.surge_destroy(h)
+
+
+def test_two_ranks_on_one_gpu_cover_exactly(N):
+    """world_size=2: two handles (rank 0, rank 1) fed the same stream encode disjoint LPT pieces whose
+    union equals the world_size=1 result bit-exactly, with the oracle's LPT assignment."""
+    ecfg, wcfg = ENCODERS["toy"], scaled(WORKLOADS["toy"], n_texts=2000, n_partitions=20, b_min=300, b_max=1500)
+    w = make_weights(ecfg, seed=1234, init="pin")
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=3)
+    full, sbs1, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+    rows = {}
+    for rank in (0, 1):
+        _, sbs, stats, pieces = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max, rank=rank, world_size=2)
+        assert [s["members"] for s in sbs] == [s["members"] for s in sbs1]
+        for key, (n, parts) in pieces.items():
+            for rb, arr in parts.items():
+                for i in range(arr.shape[0]):
+                    assert (key, rb + i) not in rows
+                    rows[(key, rb + i)] = arr[i]
+    assert len(rows) == wl.n_texts
+    for key, M in full.items():
+        for i in range(M.shape[0]):
+            assert np.array_equal(rows[(key, i)], M[i])
+    # oracle LPT: per SuperBatch, the rank-owned rows match
+    A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, wcfg.b_min, wcfg.b_max)
+    assert len(A.flushes) == len(sbs1)

@@ -5,10 +5,9 @@
 //   EPI_BIAS_LN   C = LN(A B^T + b + R) * gamma + beta   (attention out-proj K6, FFN2 K8)
 // A: [M x K] activations (row-major, K contiguous), B: [N x K] weights (HF nn.Linear [out,in]).
 //
-// Design: one CTA per 128 x BN output tile, warp-specialised:
-//   warp 0 (one lane)  TMA producer: A box 64x128, B box 64x(BN or BN/2) per K-block, STAGES ring
-//   warp 1             TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256 per MMA)
-//   warps 2..5         epilogue: tcgen05.ld 32x32b -> registers -> bias/GELU/residual+LN -> bf16
+// Design: persistent grid (<= #SMs), 128 x BN output tiles, warp-specialised
+// (TMA producer, single-thread MMA issuer, TMEM allocator, 8 epilogue warps); accumulators double-
+// buffered in TMEM when 2*BN <= 512 so the epilogue of one tile overlaps the next tile's mainloop.
 // Rows >= M of the last tile are zero-filled by TMA and never stored.
 #include <cudaTypedefs.h>
 
@@ -24,7 +23,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;                       // 64 bf16 = 128 B = one swizzle row
 constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
-constexpr int GEMM_THREADS = 192;            // 6 warps
+constexpr int NUM_EPI_WARPS = 8;             // 2 per TMEM lane quadrant, splitting the columns
+constexpr int GEMM_THREADS = 128 + NUM_EPI_WARPS * 32;
 
 template <int BN>
 struct TileCfg {
@@ -34,13 +34,34 @@ struct TileCfg {
   static constexpr int N_MMA = BN / MMA_N;
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES = (BN >= 384) ? 3 : 4;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int ACC = (2 * BN <= 512) ? 2 : 1;            // TMEM accumulator buffers
+  static constexpr int ACC_COLS = ACC * BN;
+  static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
+                                   : ACC_COLS <= 256 ? 256 : 512;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * ACC) + 16;
+  static constexpr int STATS_BYTES = 2 * 2 * BM * 4 * 4;          // [buf][half][row] x float4
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + BAR_BYTES + STATS_BYTES;
+  static constexpr int HALF = BN / 2;                             // columns per epilogue warp
   static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
   static_assert(B_BOX * N_LOADS == BN, "B box split");
+  static_assert(HALF % 16 == 0, "epilogue column split");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
 };
 
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Persistent, warp-specialised tcgen05 GEMM.  Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...
+// (n fastest, so concurrently running CTAs share the A rows of one M block in L2).
+//   warp 0        TMA producer (one lane), STAGES-deep smem ring
+//   warp 1        MMA issuer (one lane): UMMA 128 x MMA_N x 16, accumulator buffer it % ACC
+//   warp 2        TMEM allocator
+//   warps 4..11   epilogue: warp w reads TMEM lane quadrant w % 4, column half (w - 4) / 4;
+//                 the accumulator buffer is released as soon as it is drained, so with ACC = 2 the
+//                 epilogue of tile i overlaps the mainloop of tile i + 1.
 template <int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
@@ -48,19 +69,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
                    float eps) {
   using T = TileCfg<BN>;
-  constexpr int STAGES = T::STAGES;
+  constexpr int STAGES = T::STAGES, ACC = T::ACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                   // STAGES x 16 KB
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;          // STAGES x B_STAGE_BYTES
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * T::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
+  float4* stats = reinterpret_cast<float4*>(smem + STAGES * T::STAGE_BYTES + T::BAR_BYTES);  // [2][2][BM]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int num_kb = K / BK;
+  const int n_tiles = N / BN;
+  const int num_tiles = ((M + BM - 1) / BM) * n_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -69,10 +93,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], NUM_EPI_WARPS);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) {
+  if (warp == 2) {
     tmem_alloc(tmem_slot, T::TMEM_COLS);
     tmem_relinquish();
   }
@@ -87,15 +114,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_w = l2_policy_evict_last();   // weights: re-read by every M tile
       int s = 0;
       uint32_t ph = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], T::STAGE_BYTES);
-        tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], T::STAGE_BYTES);
+          tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
 #pragma unroll
-        for (int j = 0; j < T::N_LOADS; ++j)
-          tma_load_2d_hint(sB + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
-                           n0 + j * T::B_BOX, pol_w);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+          for (int j = 0; j < T::N_LOADS; ++j)
+            tma_load_2d_hint(sB + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
+                             n0 + j * T::B_BOX, pol_w);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -104,115 +134,176 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
       int s = 0;
       uint32_t ph = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full[s], ph);
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it % ACC;
+        const uint32_t aph = (it / ACC) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);     // epilogue drained this accumulator buffer
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
-        const uint32_t b0 = smem_u32(sB + s * T::B_STAGE_BYTES);
+        const uint32_t d0 = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * T::B_STAGE_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
+          for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
-          for (int j = 0; j < T::N_MMA; ++j) {
-            tc_mma_bf16(tmem_base + j * T::MMA_N, umma_desc_sw128(a0 + k * 32),
-                        umma_desc_sw128(b0 + j * T::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+            for (int j = 0; j < T::N_MMA; ++j) {
+              tc_mma_bf16(d0 + j * T::MMA_N, umma_desc_sw128(a0 + k * 32),
+                          umma_desc_sw128(b0 + j * T::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+            }
           }
+          tc_commit(&empty[s]);               // frees this smem stage when the MMAs retire
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        tc_commit(&empty[s]);                 // frees this smem stage when the MMAs retire
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        tc_commit(&tfull[acc]);               // accumulator complete
       }
-      tc_commit(tmem_full);                   // accumulator complete
     }
-  } else {
-    // ------------------------------------------------------------------ epilogue (warps 2..5)
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue (warps 4..11)
     const int q = warp & 3;                   // TMEM lane quadrant this warp may access
-    const int row = m0 + q * 32 + lane;
-    const bool ok = row < M;
-    const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
-      uint16_t* crow = C + size_t(row) * N + n0;
+    const int hh = (warp - 4) >> 2;           // column half
+    const int c_lo = hh * T::HALF;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
+      const int acc = it % ACC;
+      const uint32_t aph = (it / ACC) & 1;
+      const int row = m0 + q * 32 + lane;
+      const bool ok = row < M;
+      const uint32_t taddr = tmem_base + acc * BN + (uint32_t(q * 32) << 16);
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
+        uint16_t* crow = C + size_t(row) * N + n0;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(taddr + c, r);
-        tmem_ld_wait();
-        uint32_t p[8];
+        for (int c = c_lo; c < c_lo + T::HALF; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c, r);
+          float bv[16];
+          const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float v0 = __uint_as_float(r[2 * i]) + __ldg(bias + n0 + c + 2 * i);
-          float v1 = __uint_as_float(r[2 * i + 1]) + __ldg(bias + n0 + c + 2 * i + 1);
-          if constexpr (EPI == EPI_BIAS_GELU) {
-            v0 = gelu_erf(v0);
-            v1 = gelu_erf(v1);
+          for (int i = 0; i < 4; ++i) {
+            const float4 b4 = __ldg(bp + i);
+            bv[4 * i] = b4.x; bv[4 * i + 1] = b4.y; bv[4 * i + 2] = b4.z; bv[4 * i + 3] = b4.w;
           }
-          p[i] = pack_bf16x2(v0, v1);
-        }
-        if (ok) {
-          uint4* dst = reinterpret_cast<uint4*>(crow + c);
-          dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-          dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
-        }
-      }
-    } else {
-      // LayerNorm over the full row (BN == N): pass 1 statistics, pass 2 normalise + store.
-      const uint16_t* rrow = res + size_t(ok ? row : 0) * N;
-      uint16_t* crow = C + size_t(row) * N;
-      float shift = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(taddr + c, r);
-        tmem_ld_wait();
-        const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
-        const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
-        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          tmem_ld_wait();
+          uint32_t p[8];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float v = __uint_as_float(r[i]) + __ldg(bias + c + i) + ((i & 1) ? bf16hi(rr[i >> 1]) : bf16lo(rr[i >> 1]));
-          if (c == 0 && i == 0) shift = v;    // shifted sums: var is shift-invariant, less cancellation
-          const float t = v - shift;
-          s1 += t;
-          s2 += t * t;
+          for (int i = 0; i < 8; ++i) {
+            float v0 = __uint_as_float(r[2 * i]) + bv[2 * i];
+            float v1 = __uint_as_float(r[2 * i + 1]) + bv[2 * i + 1];
+            if constexpr (EPI == EPI_BIAS_GELU) {
+              v0 = gelu_erf(v0);
+              v1 = gelu_erf(v1);
+            }
+            p[i] = pack_bf16x2(v0, v1);
+          }
+          if (ok) {
+            uint4* dst = reinterpret_cast<uint4*>(crow + c);
+            dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+            dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+          }
         }
-      }
-      const float inv_n = 1.0f / float(BN);
-      const float mt = s1 * inv_n;
-      const float var = fmaxf(s2 * inv_n - mt * mt, 0.f);
-      const float mean = shift + mt;
-      const float rstd = rsqrtf(var + eps);
+      } else {
+        // LayerNorm over the full row (BN == N), two warps per row (column halves):
+        // pass 1: shifted partial sums per half -> combine via smem (Chan's formula); pass 2: write.
+        const uint16_t* rrow = res + size_t(ok ? row : 0) * N;
+        uint16_t* crow = C + size_t(row) * N;
+        float shift = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(taddr + c, r);
-        tmem_ld_wait();
-        const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
-        const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
-        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-        uint32_t p[8];
+        for (int c = c_lo; c < c_lo + T::HALF; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c, r);
+          const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
+          const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
+          float bv[16];
+          const float4* bp = reinterpret_cast<const float4*>(bias + c);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int j0 = 2 * i, j1 = 2 * i + 1;
-          float v0 = __uint_as_float(r[j0]) + __ldg(bias + c + j0) + bf16lo(rr[i]);
-          float v1 = __uint_as_float(r[j1]) + __ldg(bias + c + j1) + bf16hi(rr[i]);
-          v0 = (v0 - mean) * rstd * __ldg(gamma + c + j0) + __ldg(beta + c + j0);
-          v1 = (v1 - mean) * rstd * __ldg(gamma + c + j1) + __ldg(beta + c + j1);
-          p[i] = pack_bf16x2(v0, v1);
+          for (int i = 0; i < 4; ++i) {
+            const float4 b4 = __ldg(bp + i);
+            bv[4 * i] = b4.x; bv[4 * i + 1] = b4.y; bv[4 * i + 2] = b4.z; bv[4 * i + 3] = b4.w;
+          }
+          tmem_ld_wait();
+          const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float v = __uint_as_float(r[i]) + bv[i] + ((i & 1) ? bf16hi(rr[i >> 1]) : bf16lo(rr[i >> 1]));
+            if (c == c_lo && i == 0) shift = v;
+            const float d = v - shift;
+            s1 += d;
+            s2 += d * d;
+          }
         }
-        if (ok) {
-          uint4* dst = reinterpret_cast<uint4*>(crow + c);
-          dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-          dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        const int sbuf = it & 1;
+        stats[(sbuf * 2 + hh) * BM + q * 32 + lane] = make_float4(shift, s1, s2, 0.f);
+        named_bar_sync(1 + q, 64);            // the two warps of this quadrant
+        const float4 o = stats[(sbuf * 2 + (hh ^ 1)) * BM + q * 32 + lane];
+        const float nh = float(T::HALF);
+        const float mean_a = shift + s1 / nh, m2_a = s2 - s1 * s1 / nh;
+        const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
+        const float dm = mean_a - mean_b;
+        const float mean = 0.5f * (mean_a + mean_b);
+        const float var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
+        const float rstd = rsqrtf(var + eps);
+#pragma unroll 1
+        for (int c = c_lo; c < c_lo + T::HALF; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c, r);
+          const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
+          const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
+          float bv[16], gv[16], be[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c) + i);
+            const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + c) + i);
+            const float4 e4 = __ldg(reinterpret_cast<const float4*>(beta + c) + i);
+            bv[4 * i] = b4.x; bv[4 * i + 1] = b4.y; bv[4 * i + 2] = b4.z; bv[4 * i + 3] = b4.w;
+            gv[4 * i] = g4.x; gv[4 * i + 1] = g4.y; gv[4 * i + 2] = g4.z; gv[4 * i + 3] = g4.w;
+            be[4 * i] = e4.x; be[4 * i + 1] = e4.y; be[4 * i + 2] = e4.z; be[4 * i + 3] = e4.w;
+          }
+          tmem_ld_wait();
+          const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          uint32_t p[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j0 = 2 * i, j1 = 2 * i + 1;
+            float v0 = __uint_as_float(r[j0]) + bv[j0] + bf16lo(rr[i]);
+            float v1 = __uint_as_float(r[j1]) + bv[j1] + bf16hi(rr[i]);
+            v0 = (v0 - mean) * rstd * gv[j0] + be[j0];
+            v1 = (v1 - mean) * rstd * gv[j1] + be[j1];
+            p[i] = pack_bf16x2(v0, v1);
+          }
+          if (ok) {
+            uint4* dst = reinterpret_cast<uint4*>(crow + c);
+            dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+            dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+          }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 2) {
     __syncwarp();
     tmem_dealloc(tmem_base, T::TMEM_COLS);
   }
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
@@ -227,7 +318,8 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((g.M + BM - 1) / BM, g.N / BN);
+  const int64_t tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
+  const int grid = int(tiles < num_sms() ? tiles : num_sms());
   kern<<<grid, GEMM_THREADS, T::SMEM_BYTES, st>>>(*g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
                                                   g.beta, g.C, g.eps);
   return cudaGetLastError();
@@ -264,7 +356,6 @@ cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uin
 
 int gemm_bn_for(int N, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
-  if (N % 384 == 0 && N >= 1152) return 384;
   if (N % 256 == 0) return 256;
   if (N % 192 == 0) return 192;
   if (N % 128 == 0) return 128;

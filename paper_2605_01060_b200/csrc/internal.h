@@ -38,9 +38,13 @@ cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes,
 cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_texts, int32_t tok0,
                             const uint16_t* word, const uint16_t* pos, const uint16_t* type, const float* gamma,
                             const float* beta, int d, float eps, uint16_t* x, cudaStream_t st);
-// K5
-cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0, int heads,
-                             int head_dim, uint16_t* out, cudaStream_t st);
+// K5: window kernel for texts of <= 32 tokens (+ per-(text, head) kernel when max_len > 32).
+// win: int32[ceil(ntok/32)+1] scratch; win_ready = already filled by launch_window_index for this chunk.
+cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t ntok, int32_t* win,
+                                cudaStream_t st);
+cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
+                             int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
+                             uint16_t* out, cudaStream_t st);
 // K9
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
                                float* out, cudaStream_t st);
@@ -90,6 +94,7 @@ struct LayerW {
 struct Workspace {
   int64_t cap = 0;
   uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
+  int32_t* win = nullptr;   // attention window index, cap/32 + 2 entries
   cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
   void release();
   ~Workspace() { release(); }

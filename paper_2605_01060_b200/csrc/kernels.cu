@@ -168,7 +168,8 @@ template <int DH, int ATT_WARPS = AttCfg<DH>::WARPS>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(const uint16_t* __restrict__ qkv,
                                                                    const int32_t* __restrict__ cu, int64_t n_texts,
                                                                    int32_t tok0, int heads,
-                                                                   uint16_t* __restrict__ out, float qscale) {
+                                                                   uint16_t* __restrict__ out, float qscale,
+                                                                   int32_t min_len) {
   __shared__ __align__(16) float sK[ATT_WARPS][32][DH];
   __shared__ __align__(16) float sV[ATT_WARPS][32][DH];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(const uint16_
   const int d = heads * DH, ld = 3 * d;
   const int32_t start = cu[text] - tok0;
   const int32_t len = cu[text + 1] - cu[text];
+  if (len < min_len) return;   // short texts are handled by attention_window_kernel
   constexpr int V8 = DH / 8;   // 16-byte vectors per head row
 
   for (int qb = 0; qb < len; qb += 32) {
@@ -282,6 +284,148 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(const uint16_
   }
 }
 
+// ------------------------------------------------------- K5 (short texts): window attention
+// win[w] = min{s : a_s >= 32 w} for w in [0, nwin], a_s = cu[s] - tok0 (a_n = T): the first
+// text starting in 32-token window w.  One thread per text boundary s in [0, n].
+__global__ void window_index_kernel(const int32_t* __restrict__ cu, int64_t n, int32_t tok0, int32_t ntok,
+                                    int32_t* __restrict__ win) {
+  const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > n) return;
+  const int32_t nwin = (ntok + 31) >> 5;
+  const int32_t prev = (s == 0) ? -1 : cu[s - 1] - tok0;
+  const int32_t a = (s == n) ? ntok : cu[s] - tok0;
+  const int32_t w_lo = (prev < 0) ? 0 : (prev >> 5) + 1;
+  const int32_t w_hi = (s == n) ? nwin : (a >> 5);
+  for (int32_t w = w_lo; w <= w_hi; ++w) win[w] = int32_t(s);
+}
+
+// One warp per (32-token window, head) over the texts that START in the window and have
+// length <= 32 (their rows lie in [R0, R0 + 64)).  Each lane stages the K/V head slices of its
+// rows once into padded fp32 shared memory; lane = query row; online softmax over the text's own
+// keys with a lazy rescale (only when the running max grows).  Longer texts: attention_kernel.
+template <int DH>
+struct WinCfg {
+  static constexpr int WARPS = 4;
+  static constexpr int LD = DH + 4;   // padded row stride (floats): distinct rows hit distinct banks
+  static constexpr int SMEM = 2 * WARPS * 64 * LD * 4;
+};
+
+template <int DH, int WARPS = WinCfg<DH>::WARPS>
+__global__ void __launch_bounds__(WARPS * 32) attention_window_kernel(
+    const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu, int32_t tok0, int32_t ntok,
+    const int32_t* __restrict__ win, int heads, uint16_t* __restrict__ out, float qscale) {
+  constexpr int LD = WinCfg<DH>::LD;
+  constexpr int V8 = DH / 8;
+  extern __shared__ __align__(16) float att_smem[];
+  float(*sK)[64][LD] = reinterpret_cast<float(*)[64][LD]>(att_smem);
+  float(*sV)[64][LD] = reinterpret_cast<float(*)[64][LD]>(att_smem + WARPS * 64 * LD);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = int64_t(blockIdx.x) * WARPS + w;
+  const int32_t nwin = (ntok + 31) >> 5;
+  if (gw >= int64_t(nwin) * heads) return;
+  const int32_t window = int32_t(gw / heads);
+  const int h = int(gw % heads);
+  const int32_t s_a = win[window], s_b = win[window + 1];
+  const int32_t nb = s_b - s_a;                     // texts starting in this window (<= 32)
+  if (nb <= 0) return;
+  const int d = heads * DH, ld = 3 * d;
+  const int32_t bnd = (lane < nb) ? cu[s_a + lane] - tok0 : 0x7fffffff;   // start of text s_a + lane
+  const int32_t R1 = cu[s_b] - tok0;
+  const int32_t R0 = __shfl_sync(0xffffffffu, bnd, 0);
+
+  int32_t ts[2], te[2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int32_t r = R0 + lane + 32 * p;
+    int t = -1;
+    for (int i = 0; i < nb; ++i) t += (__shfl_sync(0xffffffffu, bnd, i) <= r);
+    const int32_t st = __shfl_sync(0xffffffffu, bnd, t < 0 ? 0 : t);
+    const int32_t en_n = __shfl_sync(0xffffffffu, bnd, (t + 1) < 32 ? t + 1 : 31);
+    const int32_t en = (t + 1 < nb) ? en_n : R1;
+    const bool ok = (r < R1) && (en - st <= 32);
+    ts[p] = ok ? st - R0 : 0;
+    te[p] = ok ? en - R0 : 0;                       // empty range => row not handled here
+    if (ok) {
+      const size_t base = size_t(r) * ld + h * DH;
+      const uint4* kp = reinterpret_cast<const uint4*>(qkv + base + d);
+      const uint4* vp = reinterpret_cast<const uint4*>(qkv + base + 2 * d);
+      float* kr = &sK[w][lane + 32 * p][0];
+      float* vr = &sV[w][lane + 32 * p][0];
+#pragma unroll
+      for (int v = 0; v < V8; ++v) {
+        const uint4 ku = kp[v], vu = vp[v];
+        reinterpret_cast<float4*>(kr)[2 * v] = make_float4(bf16lo(ku.x), bf16hi(ku.x), bf16lo(ku.y), bf16hi(ku.y));
+        reinterpret_cast<float4*>(kr)[2 * v + 1] = make_float4(bf16lo(ku.z), bf16hi(ku.z), bf16lo(ku.w), bf16hi(ku.w));
+        reinterpret_cast<float4*>(vr)[2 * v] = make_float4(bf16lo(vu.x), bf16hi(vu.x), bf16lo(vu.y), bf16hi(vu.y));
+        reinterpret_cast<float4*>(vr)[2 * v + 1] = make_float4(bf16lo(vu.z), bf16hi(vu.z), bf16lo(vu.w), bf16hi(vu.w));
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    if (te[p] <= ts[p]) continue;
+    const int32_t r = R0 + lane + 32 * p;
+    float q[DH];
+    {
+      const uint4* qp = reinterpret_cast<const uint4*>(qkv + size_t(r) * ld + h * DH);
+#pragma unroll
+      for (int v = 0; v < V8; ++v) {
+        const uint4 u = qp[v];
+        const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          q[v * 8 + 2 * k] = bf16lo(uu[k]) * qscale;
+          q[v * 8 + 2 * k + 1] = bf16hi(uu[k]) * qscale;
+        }
+      }
+    }
+    float o[DH];
+#pragma unroll
+    for (int c = 0; c < DH; ++c) o[c] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int32_t j = ts[p]; j < te[p]; ++j) {
+      const float4* kr = reinterpret_cast<const float4*>(&sK[w][j][0]);
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < DH / 4; ++c) {
+        const float4 k4 = kr[c];
+        acc = fmaf(q[4 * c], k4.x, acc);
+        acc = fmaf(q[4 * c + 1], k4.y, acc);
+        acc = fmaf(q[4 * c + 2], k4.z, acc);
+        acc = fmaf(q[4 * c + 3], k4.w, acc);
+      }
+      if (acc > m) {                                 // lazy rescale
+        const float corr = exp2f(m - acc);
+        l *= corr;
+#pragma unroll
+        for (int c = 0; c < DH; ++c) o[c] *= corr;
+        m = acc;
+      }
+      const float pj = exp2f(acc - m);
+      l += pj;
+      const float4* vr = reinterpret_cast<const float4*>(&sV[w][j][0]);
+#pragma unroll
+      for (int c = 0; c < DH / 4; ++c) {
+        const float4 v4 = vr[c];
+        o[4 * c] = fmaf(pj, v4.x, o[4 * c]);
+        o[4 * c + 1] = fmaf(pj, v4.y, o[4 * c + 1]);
+        o[4 * c + 2] = fmaf(pj, v4.z, o[4 * c + 2]);
+        o[4 * c + 3] = fmaf(pj, v4.w, o[4 * c + 3]);
+      }
+    }
+    const float inv = 1.0f / l;
+    uint4* op = reinterpret_cast<uint4*>(out + size_t(r) * d + h * DH);
+#pragma unroll
+    for (int v = 0; v < V8; ++v) {
+      op[v] = make_uint4(pack_bf16x2(o[v * 8 + 0] * inv, o[v * 8 + 1] * inv),
+                         pack_bf16x2(o[v * 8 + 2] * inv, o[v * 8 + 3] * inv),
+                         pack_bf16x2(o[v * 8 + 4] * inv, o[v * 8 + 5] * inv),
+                         pack_bf16x2(o[v * 8 + 6] * inv, o[v * 8 + 7] * inv));
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- K9 meanpool + L2
 template <int D>
 __global__ void __launch_bounds__(256) meanpool_l2_kernel(const uint16_t* __restrict__ x,
@@ -372,15 +516,31 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_tex
   return cudaGetLastError();
 }
 
-cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0, int heads,
-                             int head_dim, uint16_t* out, cudaStream_t st) {
+cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
+                             int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
+                             uint16_t* out, cudaStream_t st) {
   if (n_texts <= 0) return cudaSuccess;
   const float qscale = 1.4426950408889634f / sqrtf(float(head_dim));
-#define SURGE_ATT(DH)                                                                                  \
-  case DH: {                                                                                           \
-    constexpr int W = AttCfg<DH>::WARPS;                                                               \
-    attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W), W * 32, 0, st>>>(qkv, cu, n_texts, tok0, \
-                                                                                   heads, out, qscale); \
+  const int32_t nwin = (ntok + 31) >> 5;
+  if (!win_ready) {
+    window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
+  }
+#define SURGE_ATT(DH)                                                                                        \
+  case DH: {                                                                                                 \
+    constexpr int W = WinCfg<DH>::WARPS;                                                                     \
+    static bool attr_##DH = false;                                                                           \
+    if (!attr_##DH) {                                                                                        \
+      cudaFuncSetAttribute(attention_window_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                           WinCfg<DH>::SMEM);                                                                \
+      attr_##DH = true;                                                                                      \
+    }                                                                                                        \
+    attention_window_kernel<DH><<<blocks_for_warps(int64_t(nwin) * heads, W), W * 32, WinCfg<DH>::SMEM, st>>>( \
+        qkv, cu, tok0, ntok, win, heads, out, qscale);                                                       \
+    if (max_len > 32) {                                                                                      \
+      constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \
+      attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W1), W1 * 32, 0, st>>>(qkv, cu, n_texts, tok0, \
+                                                                                      heads, out, qscale, 33); \
+    }                                                                                                        \
   } break;
   switch (head_dim) {
     SURGE_ATT(16)
@@ -389,6 +549,13 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
     default: return cudaErrorInvalidValue;
   }
 #undef SURGE_ATT
+  return cudaGetLastError();
+}
+
+cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t ntok, int32_t* win,
+                                cudaStream_t st) {
+  if (n_texts <= 0) return cudaSuccess;
+  window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
   return cudaGetLastError();
 }
 

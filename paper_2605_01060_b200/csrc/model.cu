@@ -26,6 +26,7 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   if ((e = cudaMalloc(&O, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&X1, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&H, t * s.ffn * 2)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&win, (t / 32 + 2) * sizeof(int32_t))) != cudaSuccess) return e;
   cap = cap_tokens;
   return cudaSuccess;
 }
@@ -35,6 +36,8 @@ void Workspace::release() {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
+  if (win) cudaFree(win);
+  win = nullptr;
   cap = 0;
 }
 
@@ -193,18 +196,23 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   SURGE_TRY(make_tmap_bf16(&tmH, ws.H, ntok, f, 128));
   const bool P = prof && prof->on;
   double sum_l2 = 0;
-  if (P && host_cu)
+  int32_t max_len = s_.max_pos;     // unknown -> assume long texts may be present
+  if (host_cu) {
+    max_len = 0;
     for (int64_t i = s0; i < s1; ++i) {
-      const double l = double(host_cu[i + 1] - host_cu[i]);
-      sum_l2 += l * l;
+      const int32_t li = host_cu[i + 1] - host_cu[i];
+      max_len = li > max_len ? li : max_len;
+      sum_l2 += double(li) * double(li);
     }
+  }
   const double M = ntok, D = d, F = f;
   cudaEvent_t ev = nullptr;
   int64_t k = 0;
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_embed_ln(d_ids, cu, n, tok0, word_, pos_, type_, emb_g_, emb_b_, d, s_.eps, ws.X, st));
+  SURGE_TRY(launch_window_index(cu, n, tok0, ntok, ws.win, st));
   if (P) prof->end(KK_EMBED, st, ev, 0.0, M * (4 + 2 * D + 2 * D + 2 * D));
-  ++k;
+  k += 2;
   for (const LayerW& L : layers_) {
     GemmArgs g{};
     g.M = ntok;
@@ -216,7 +224,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
     // K5: O = attention(QKV) per text
     if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, s_.heads, d / s_.heads, ws.O, st));
+    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st));
     if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
     // K6: X1 = LN(O Wo^T + bo + X)
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
@@ -236,7 +244,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (P) prof->begin(st, &ev);
     SURGE_TRY(launch_gemm(g, st));
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += 5;
+    k += 5 + (max_len > 32 ? 1 : 0);
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));

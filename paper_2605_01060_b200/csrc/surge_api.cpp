@@ -1134,9 +1134,23 @@ surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float
 surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int64_t n_texts, int32_t heads,
                                 int32_t head_dim, uint16_t* d_out, void* stream) {
   if (!d_qkv || !d_cu || !d_out || n_texts < 0 || heads <= 0) return SURGE_E_INVALID_ARG;
-  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, 0, heads, head_dim, d_out,
-                                          static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? SURGE_OK : SURGE_E_CUDA;
+  if (n_texts == 0) return SURGE_OK;
+  // test entry point: read cu back to find the token count and the longest text (synchronous)
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<int32_t> hcu(static_cast<size_t>(n_texts + 1));
+  if (cudaMemcpyAsync(hcu.data(), d_cu, hcu.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return SURGE_E_CUDA;
+  int32_t max_len = 0;
+  for (int64_t i = 0; i < n_texts; ++i) max_len = std::max(max_len, hcu[i + 1] - hcu[i]);
+  const int32_t ntok = hcu[n_texts] - hcu[0];
+  int32_t* win = nullptr;
+  if (cudaMalloc(&win, (size_t(ntok) / 32 + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
+  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, win, false, heads,
+                                          head_dim, d_out, st);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaFree(win);
+  return (e == cudaSuccess && e2 == cudaSuccess) ? SURGE_OK : SURGE_E_CUDA;
 }
 
 surge_status surge_op_meanpool_l2(const uint16_t* d_x, const int32_t* d_cu, int64_t n_texts, int32_t d, float* d_out,

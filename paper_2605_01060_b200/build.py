@@ -1,6 +1,6 @@
 """Build libsurge.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery).
 
-    python -m paper_2605_01060_b200.build          # or __graft_entry__.build()
+    python paper_2605_01060_b200/build.py          # or __graft_entry__.build()
 
 Objects go to paper_2605_01060_b200/_build/, the library to paper_2605_01060_b200/libsurge.so.
 cudart is linked statically; the TMA encoder is resolved at run time through

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsurge.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libsurge.so not built at {LIB_PATH}: run __graft_entry__.build() "
-                      "(python -m paper_2605_01060_b200.build)")
+                      "(python paper_2605_01060_b200/build.py)")
 lib = C.CDLL(LIB_PATH)
 
 SURGE_OK, SURGE_E_INVALID_ARG, SURGE_E_DUPLICATE_ID, SURGE_E_STATE = 0, -1, -2, -3

@@ -36,6 +36,72 @@ __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
 }
 
+// ---------------------------------------------------------------- packed fp32x2 (FFMA2/FADD2/FMUL2)
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f2lo(f32x2 v) {
+  float a;
+  asm("{.reg .f32 t;\n\tmov.b64 {%0, t}, %1;}" : "=f"(a) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float f2hi(f32x2 v) {
+  float b;
+  asm("{.reg .f32 t;\n\tmov.b64 {t, %0}, %1;}" : "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Exact-erf GELU, x * Phi(x), on a pair: with t = min(|x|, 5.5),
+// E = Phi(-t) = exp(-t^2/2) * m(t), where m (the scaled Mills ratio) is a degree-9 minimax
+// polynomial (relative error 5.5e-5 on [0, 5.5]); then x * Phi(x) = x/2 + |x| (1/2 - E) for either
+// sign of x (branch-free).  |gelu error| <= 5.5e-5 |gelu(x)| wherever |gelu(x)| > 1e-6 and <= 9e-6
+// absolute everywhere: 36x below the bf16 rounding of the stored result.  One MUFU.EX2 and ~10
+// issue slots per value.
+__device__ __forceinline__ void gelu2(float& x0, float& x1) {
+  const float t0 = fminf(fabsf(x0), 5.5f), t1 = fminf(fabsf(x1), 5.5f);
+  const f32x2 t = f2(t0, t1);
+  const f32x2 a = fmul2(fmul2(t, t), f2(-0.72134752044448170368f, -0.72134752044448170368f));  // -t^2/2 log2 e
+  const f32x2 e = f2(ex2_approx(f2lo(a)), ex2_approx(f2hi(a)));
+  f32x2 m = f2(-8.42938611e-07f, -8.42938611e-07f);
+  m = ffma2(m, t, f2(2.55162200e-05f, 2.55162200e-05f));
+  m = ffma2(m, t, f2(-3.38936006e-04f, -3.38936006e-04f));
+  m = ffma2(m, t, f2(2.61646596e-03f, 2.61646596e-03f));
+  m = ffma2(m, t, f2(-1.31696069e-02f, -1.31696069e-02f));
+  m = ffma2(m, t, f2(4.63381338e-02f, 4.63381338e-02f));
+  m = ffma2(m, t, f2(-1.20678578e-01f, -1.20678578e-01f));
+  m = ffma2(m, t, f2(2.44876648e-01f, 2.44876648e-01f));
+  m = ffma2(m, t, f2(-3.98055506e-01f, -3.98055506e-01f));
+  m = ffma2(m, t, f2(4.99972499e-01f, 4.99972499e-01f));
+  const f32x2 E = fmul2(m, e);                                   // Phi(-|x|)
+  const f32x2 R = ffma2(E, f2(-1.f, -1.f), f2(0.5f, 0.5f));      // 1/2 - Phi(-|x|)
+  const f32x2 g = ffma2(f2(fabsf(x0), fabsf(x1)), R, fmul2(f2(x0, x1), f2(0.5f, 0.5f)));
+  x0 = f2lo(g);
+  x1 = f2hi(g);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -140,6 +206,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// 32 lanes x 32-bit, 32 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -11,6 +11,7 @@
 // Rows >= M of the last tile are zero-filled by TMA and never stored.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -26,70 +27,101 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
 constexpr int NUM_EPI_WARPS = 8;             // 2 per TMEM lane quadrant, splitting the columns
 constexpr int GEMM_THREADS = 128 + NUM_EPI_WARPS * 32;
 
-template <int BN>
+template <int BN, int EPI>
 struct TileCfg {
   static constexpr int B_BOX = (BN <= 256) ? BN : BN / 2;       // TMA box rows for B
   static constexpr int N_LOADS = BN / B_BOX;
   static constexpr int MMA_N = B_BOX;                            // <= 256, multiple of 16
   static constexpr int N_MMA = BN / MMA_N;
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
   static constexpr int ACC = (2 * BN <= 512) ? 2 : 1;            // TMEM accumulator buffers
   static constexpr int ACC_COLS = ACC * BN;
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
                                    : ACC_COLS <= 256 ? 256 : 512;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 2 * ACC) + 16;
-  static constexpr int STATS_BYTES = 2 * 2 * BM * 4 * 4;          // [buf][half][row] x float4
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + BAR_BYTES + STATS_BYTES;
+  static constexpr int HEAD_BYTES = 1024;                         // mbarriers + TMEM slot
+  static constexpr int STATS_BYTES = EPI == EPI_BIAS_LN ? 2 * 2 * BM * 4 * 4 : 0;   // [buf][half][row] x float4
+  static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES;
+  static constexpr int MAX_SMEM = 227 * 1024;
+  static constexpr int MAX_STAGES = 8;
   static constexpr int HALF = BN / 2;                             // columns per epilogue warp
   static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
   static_assert(B_BOX * N_LOADS == BN, "B box split");
-  static_assert(HALF % 16 == 0, "epilogue column split");
-  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
+  static_assert(HALF % 32 == 0, "epilogue column split");
+  // Weight-stationary (ws): the CTA's whole B slice [BN x K] stays resident; only A streams.
+  __host__ __device__ static int b_res_bytes(int K, bool ws) { return ws ? BN * K * 2 : 0; }
+  __host__ __device__ static int stage_bytes(bool ws) { return A_STAGE_BYTES + (ws ? 0 : B_STAGE_BYTES); }
+  __host__ __device__ static int stages(int K, bool ws) {
+    const int n = (MAX_SMEM - FIXED_BYTES - b_res_bytes(K, ws)) / stage_bytes(ws);
+    return n > MAX_STAGES ? MAX_STAGES : n;
+  }
+  __host__ __device__ static int smem_bytes(int K, bool ws) { return FIXED_BYTES + b_res_bytes(K, ws) + stages(K, ws) * stage_bytes(ws); }
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Persistent, warp-specialised tcgen05 GEMM.  Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...
-// (n fastest, so concurrently running CTAs share the A rows of one M block in L2).
-//   warp 0        TMA producer (one lane), STAGES-deep smem ring
+// Tile schedule of one CTA.  Streaming (WS = false): tiles t = blockIdx.x, +gridDim.x, ... over
+// (m, n) with n fastest, so concurrently running CTAs share the A rows of one M block in L2.
+// Weight-stationary (WS = true): CTA c owns the N slice c % n_tiles for the whole launch (its B
+// slice is loaded once and stays in shared memory) and walks M tiles c / n_tiles, + gridDim.x /
+// n_tiles, ...; the grid is a multiple of n_tiles.
+template <bool WS>
+struct Sched {
+  int t0, dt, tend, n_tiles, slice;
+  __device__ Sched(int m_tiles, int n_tiles_) : n_tiles(n_tiles_) {
+    if (WS) {
+      slice = blockIdx.x % n_tiles;
+      t0 = blockIdx.x / n_tiles;
+      dt = gridDim.x / n_tiles;
+      tend = m_tiles;
+    } else {
+      slice = 0;
+      t0 = blockIdx.x;
+      dt = gridDim.x;
+      tend = m_tiles * n_tiles;
+    }
+  }
+  __device__ int m0(int t) const { return (WS ? t : t / n_tiles) * BM; }
+  __device__ int n0(int t) const { return (WS ? slice : t % n_tiles); }
+};
+
+// Persistent, warp-specialised tcgen05 GEMM.
+//   warp 0        TMA producer (one lane): `stages`-deep smem ring (A, plus B when streaming)
 //   warp 1        MMA issuer (one lane): UMMA 128 x MMA_N x 16, accumulator buffer it % ACC
 //   warp 2        TMEM allocator
 //   warps 4..11   epilogue: warp w reads TMEM lane quadrant w % 4, column half (w - 4) / 4;
 //                 the accumulator buffer is released as soon as it is drained, so with ACC = 2 the
 //                 epilogue of tile i overlaps the mainloop of tile i + 1.
-template <int BN, int EPI>
+template <int BN, int EPI, bool WS>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
-                   float eps) {
-  using T = TileCfg<BN>;
-  constexpr int STAGES = T::STAGES, ACC = T::ACC;
+                   float eps, int stages) {
+  using T = TileCfg<BN, EPI>;
+  constexpr int ACC = T::ACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                   // STAGES x 16 KB
-  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;          // STAGES x B_STAGE_BYTES
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * T::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + ACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
-  float4* stats = reinterpret_cast<float4*>(smem + STAGES * T::STAGE_BYTES + T::BAR_BYTES);  // [2][2][BM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [stages]
+  uint64_t* empty = full + T::MAX_STAGES;               // [stages]
+  uint64_t* tfull = empty + T::MAX_STAGES;              // [ACC]
+  uint64_t* tempty = tfull + 2;                         // [ACC]
+  uint64_t* bfull = tempty + 2;                         // resident B slice landed (WS)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  float4* stats = reinterpret_cast<float4*>(smem + T::HEAD_BYTES);                  // [2][2][BM]
+  uint8_t* sB = smem + T::HEAD_BYTES + T::STATS_BYTES;  // WS: resident [K/64][BN x 128 B]; else ring
+  uint8_t* sA = sB + T::b_res_bytes(K, WS);             // [stages] x 16 KB
+  uint8_t* sBs = sA + stages * A_STAGE_BYTES;           // streaming B ring [stages] x B_STAGE_BYTES
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_kb = K / BK;
-  const int n_tiles = N / BN;
-  const int num_tiles = ((M + BM - 1) / BM) * n_tiles;
+  const Sched<WS> sc((M + BM - 1) / BM, N / BN);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -97,6 +129,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], NUM_EPI_WARPS);
     }
+    mbar_init(bfull, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -112,19 +145,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       // ------------------------------------------------------------------ TMA producer
       const uint64_t pol_w = l2_policy_evict_last();   // weights: re-read by every M tile
+      if constexpr (WS) {
+        if (sc.t0 < sc.tend) {
+          const int n0 = sc.slice * BN;
+          mbar_arrive_expect_tx(bfull, uint32_t(BN) * K * 2);
+          for (int kb = 0; kb < num_kb; ++kb)
+#pragma unroll
+            for (int j = 0; j < T::N_LOADS; ++j)
+              tma_load_2d_hint(sB + kb * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, bfull, kb * BK,
+                               n0 + j * T::B_BOX, pol_w);
+        }
+      }
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
+      for (int t = sc.t0; t < sc.tend; t += sc.dt) {
+        const int m0 = sc.m0(t), n0 = sc.n0(t) * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], T::STAGE_BYTES);
+          mbar_arrive_expect_tx(&full[s], T::stage_bytes(WS));
           tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
+          if constexpr (!WS) {
 #pragma unroll
-          for (int j = 0; j < T::N_LOADS; ++j)
-            tma_load_2d_hint(sB + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
-                             n0 + j * T::B_BOX, pol_w);
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+            for (int j = 0; j < T::N_LOADS; ++j)
+              tma_load_2d_hint(sBs + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
+                               n0 + j * T::B_BOX, pol_w);
+          }
+          if (++s == stages) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -132,10 +178,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       // ------------------------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
+      if constexpr (WS) mbar_wait(bfull, 0);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int t = sc.t0; t < sc.tend; t += sc.dt, ++it) {
         const int acc = it % ACC;
         const uint32_t aph = (it / ACC) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);     // epilogue drained this accumulator buffer
@@ -145,7 +192,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
-          const uint32_t b0 = smem_u32(sB + s * T::B_STAGE_BYTES);
+          const uint32_t b0 = smem_u32(WS ? sB + kb * T::B_STAGE_BYTES : sBs + s * T::B_STAGE_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
@@ -155,7 +202,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
           tc_commit(&empty[s]);               // frees this smem stage when the MMAs retire
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++s == stages) { s = 0; ph ^= 1; }
         }
         tc_commit(&tfull[acc]);               // accumulator complete
       }
@@ -166,8 +213,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int hh = (warp - 4) >> 2;           // column half
     const int c_lo = hh * T::HALF;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int m0 = (t / n_tiles) * BM, n0 = (t % n_tiles) * BN;
+    for (int t = sc.t0; t < sc.tend; t += sc.dt, ++it) {
+      const int m0 = sc.m0(t), n0 = sc.n0(t) * BN;
       const int acc = it % ACC;
       const uint32_t aph = (it / ACC) & 1;
       const int row = m0 + q * 32 + lane;
@@ -176,34 +223,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
+        // 32 columns per step: one TMEM load (x32) + the bias slice, then fp32x2 math, 4 x 16-B stores
         uint16_t* crow = C + size_t(row) * N + n0;
 #pragma unroll 1
-        for (int c = c_lo; c < c_lo + T::HALF; c += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c, r);
-          float bv[16];
+        for (int c = c_lo; c < c_lo + T::HALF; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c, r);
+          float4 b4[8];
           const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 b4 = __ldg(bp + i);
-            bv[4 * i] = b4.x; bv[4 * i + 1] = b4.y; bv[4 * i + 2] = b4.z; bv[4 * i + 3] = b4.w;
-          }
+          for (int i = 0; i < 8; ++i) b4[i] = __ldg(bp + i);
           tmem_ld_wait();
-          uint32_t p[8];
+          uint32_t p[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            float v0 = __uint_as_float(r[2 * i]) + bv[2 * i];
-            float v1 = __uint_as_float(r[2 * i + 1]) + bv[2 * i + 1];
+            const f32x2 v01 = fadd2(f2(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1])), f2(b4[i].x, b4[i].y));
+            const f32x2 v23 = fadd2(f2(__uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])), f2(b4[i].z, b4[i].w));
+            float v0 = f2lo(v01), v1 = f2hi(v01), v2 = f2lo(v23), v3 = f2hi(v23);
             if constexpr (EPI == EPI_BIAS_GELU) {
-              v0 = gelu_erf(v0);
-              v1 = gelu_erf(v1);
+              gelu2(v0, v1);
+              gelu2(v2, v3);
             }
-            p[i] = pack_bf16x2(v0, v1);
+            p[2 * i] = pack_bf16x2(v0, v1);
+            p[2 * i + 1] = pack_bf16x2(v2, v3);
           }
           if (ok) {
             uint4* dst = reinterpret_cast<uint4*>(crow + c);
-            dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-            dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
           }
         }
       } else {
@@ -308,21 +355,46 @@ int num_sms() {
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool WS>
 cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
-  using T = TileCfg<BN>;
-  static bool attr_set = false;
-  auto kern = gemm_tc_kernel<BN, EPI>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
+  using T = TileCfg<BN, EPI>;
+  auto kern = gemm_tc_kernel<BN, EPI, WS>;
+  const int smem = T::smem_bytes(g.K, WS);
+  const int stages = T::stages(g.K, WS);
+  if (stages < 2 || smem > T::MAX_SMEM) return cudaErrorInvalidValue;
+  static int attr = 0;
+  if (attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::MAX_SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr = T::MAX_SMEM;
   }
-  const int64_t tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
-  const int grid = int(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, GEMM_THREADS, T::SMEM_BYTES, st>>>(*g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
-                                                  g.beta, g.C, g.eps);
+  const int64_t m_tiles = (g.M + BM - 1) / BM, n_tiles = g.N / BN;
+  int grid;
+  if (WS) {
+    const int64_t per = std::min<int64_t>(std::max<int64_t>(num_sms() / n_tiles, 1), m_tiles);
+    grid = int(per * n_tiles);
+  } else {
+    grid = int(std::min<int64_t>(m_tiles * n_tiles, num_sms()));
+  }
+  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
+                                         g.eps, stages);
   return cudaGetLastError();
+}
+
+// Weight-stationary when the B slice fits next to >= 4 A stages and there are enough M tiles to
+// give every slice's CTAs work.
+template <int BN, int EPI>
+bool use_ws(const GemmArgs& g) {
+  using T = TileCfg<BN, EPI>;
+  return g.epi != EPI_BIAS_LN && T::stages(g.K, true) >= 4 && (g.M + BM - 1) / BM >= num_sms() / (g.N / BN);
+}
+
+template <int BN, int EPI>
+cudaError_t launch_gemm_bn(const GemmArgs& g, cudaStream_t st) {
+  if constexpr (EPI != EPI_BIAS_LN) {
+    if (use_ws<BN, EPI>(g)) return launch_gemm_t<BN, EPI, true>(g, st);
+  }
+  return launch_gemm_t<BN, EPI, false>(g, st);
 }
 
 }  // namespace
@@ -354,8 +426,11 @@ cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uin
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-int gemm_bn_for(int N, int epi) {
+int gemm_bn_for(int N, int K, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
+  // 192-column slices whose [192 x K] weight block can stay resident (weight-stationary) win over
+  // streaming 256-column tiles: A is re-read N/192 times from L2 but B is read once per CTA.
+  if (N % 192 == 0 && TileCfg<192, EPI_BIAS>::stages(K, true) >= 4) return 192;
   if (N % 256 == 0) return 256;
   if (N % 192 == 0) return 192;
   if (N % 128 == 0) return 128;
@@ -366,31 +441,31 @@ int gemm_bn_for(int N, int epi) {
 uint32_t gemm_b_box_rows(int BN) { return BN <= 256 ? BN : BN / 2; }
 
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
-  const int BN = gemm_bn_for(g.N, g.epi);
+  const int BN = gemm_bn_for(g.N, g.K, g.epi);
   if (BN == 0 || g.K % BK != 0 || g.K <= 0 || g.M <= 0) return cudaErrorInvalidValue;
   switch (g.epi) {
     case EPI_BIAS:
       switch (BN) {
-        case 64: return launch_gemm_t<64, EPI_BIAS>(g, st);
-        case 128: return launch_gemm_t<128, EPI_BIAS>(g, st);
-        case 192: return launch_gemm_t<192, EPI_BIAS>(g, st);
-        case 256: return launch_gemm_t<256, EPI_BIAS>(g, st);
-        case 384: return launch_gemm_t<384, EPI_BIAS>(g, st);
+        case 64: return launch_gemm_bn<64, EPI_BIAS>(g, st);
+        case 128: return launch_gemm_bn<128, EPI_BIAS>(g, st);
+        case 192: return launch_gemm_bn<192, EPI_BIAS>(g, st);
+        case 256: return launch_gemm_bn<256, EPI_BIAS>(g, st);
+        case 384: return launch_gemm_bn<384, EPI_BIAS>(g, st);
       }
       break;
     case EPI_BIAS_GELU:
       switch (BN) {
-        case 64: return launch_gemm_t<64, EPI_BIAS_GELU>(g, st);
-        case 128: return launch_gemm_t<128, EPI_BIAS_GELU>(g, st);
-        case 192: return launch_gemm_t<192, EPI_BIAS_GELU>(g, st);
-        case 256: return launch_gemm_t<256, EPI_BIAS_GELU>(g, st);
-        case 384: return launch_gemm_t<384, EPI_BIAS_GELU>(g, st);
+        case 64: return launch_gemm_bn<64, EPI_BIAS_GELU>(g, st);
+        case 128: return launch_gemm_bn<128, EPI_BIAS_GELU>(g, st);
+        case 192: return launch_gemm_bn<192, EPI_BIAS_GELU>(g, st);
+        case 256: return launch_gemm_bn<256, EPI_BIAS_GELU>(g, st);
+        case 384: return launch_gemm_bn<384, EPI_BIAS_GELU>(g, st);
       }
       break;
     case EPI_BIAS_LN:
       switch (BN) {
-        case 64: return launch_gemm_t<64, EPI_BIAS_LN>(g, st);
-        case 384: return launch_gemm_t<384, EPI_BIAS_LN>(g, st);
+        case 64: return launch_gemm_bn<64, EPI_BIAS_LN>(g, st);
+        case 384: return launch_gemm_bn<384, EPI_BIAS_LN>(g, st);
       }
       break;
   }

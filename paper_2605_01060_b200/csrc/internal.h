@@ -27,7 +27,7 @@ struct GemmArgs {
 
 cudaError_t init_tma_encoder();
 cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
-int gemm_bn_for(int N, int epi);
+int gemm_bn_for(int N, int K, int epi);
 uint32_t gemm_b_box_rows(int BN);
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);
 
@@ -38,12 +38,12 @@ cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes,
 cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_texts, int32_t tok0,
                             const uint16_t* word, const uint16_t* pos, const uint16_t* type, const float* gamma,
                             const float* beta, int d, float eps, uint16_t* x, cudaStream_t st);
-// K5: window kernel for texts of <= 32 tokens (+ per-(text, head) kernel when max_len > 32).
-// win: int32[ceil(ntok/32)+1] scratch; win_ready = already filled by launch_window_index for this chunk.
-cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t ntok, int32_t* win,
-                                cudaStream_t st);
+// K5: tensor-core tile kernel for texts of <= 64 tokens (+ per-(text, head) kernel when max_len > 64).
+// seg: int32[2 * ntok] scratch = per-token (first, end) of its text; seg_ready = already filled by
+// launch_seg for this chunk.  max_len bounds the longest text (sizes the K/V staging).
+cudaError_t launch_seg(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t* seg, cudaStream_t st);
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
-                             int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
+                             int32_t ntok, int32_t max_len, int32_t* seg, bool seg_ready, int heads, int head_dim,
                              uint16_t* out, cudaStream_t st);
 // K9
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
@@ -94,7 +94,7 @@ struct LayerW {
 struct Workspace {
   int64_t cap = 0;
   uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
-  int32_t* win = nullptr;   // attention window index, cap/32 + 2 entries
+  int32_t* seg = nullptr;   // attention: per-token (first, end) of its text, 2 * cap entries
   cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
   void release();
   ~Workspace() { release(); }

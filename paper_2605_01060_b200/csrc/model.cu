@@ -26,7 +26,7 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   if ((e = cudaMalloc(&O, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&X1, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&H, t * s.ffn * 2)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&win, (t / 32 + 2) * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&seg, (2 * t + 2) * sizeof(int32_t))) != cudaSuccess) return e;
   cap = cap_tokens;
   return cudaSuccess;
 }
@@ -36,8 +36,8 @@ void Workspace::release() {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
-  if (win) cudaFree(win);
-  win = nullptr;
+  if (seg) cudaFree(seg);
+  seg = nullptr;
   cap = 0;
 }
 
@@ -108,10 +108,10 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(take_f32(&L.b2, d));
       SURGE_TRY(take_f32(&L.ln2_g, d));
       SURGE_TRY(take_f32(&L.ln2_b, d));
-      SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(gemm_bn_for(int(3 * d), EPI_BIAS))));
-      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(gemm_bn_for(int(d), EPI_BIAS_LN))));
-      SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(gemm_bn_for(int(f), EPI_BIAS_GELU))));
-      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(gemm_bn_for(int(d), EPI_BIAS_LN))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(gemm_bn_for(int(3 * d), int(d), EPI_BIAS))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(gemm_bn_for(int(d), int(d), EPI_BIAS_LN))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(gemm_bn_for(int(f), int(d), EPI_BIAS_GELU))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(gemm_bn_for(int(d), int(f), EPI_BIAS_LN))));
     }
     return cudaSuccess;
   }();
@@ -210,7 +210,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   int64_t k = 0;
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_embed_ln(d_ids, cu, n, tok0, word_, pos_, type_, emb_g_, emb_b_, d, s_.eps, ws.X, st));
-  SURGE_TRY(launch_window_index(cu, n, tok0, ntok, ws.win, st));
+  SURGE_TRY(launch_seg(cu, n, tok0, ws.seg, st));
   if (P) prof->end(KK_EMBED, st, ev, 0.0, M * (4 + 2 * D + 2 * D + 2 * D));
   k += 2;
   for (const LayerW& L : layers_) {
@@ -224,7 +224,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
     // K5: O = attention(QKV) per text
     if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st));
+    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.seg, true, s_.heads, d / s_.heads, ws.O, st));
     if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
     // K6: X1 = LN(O Wo^T + bo + X)
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
@@ -244,7 +244,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (P) prof->begin(st, &ev);
     SURGE_TRY(launch_gemm(g, st));
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += 5 + (max_len > 32 ? 1 : 0);
+    k += 5 + (max_len > 64 ? 1 : 0);
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));

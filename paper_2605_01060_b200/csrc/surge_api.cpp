@@ -1120,7 +1120,7 @@ surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float
   using namespace surge;
   if (!d_a || !d_b || !d_bias || !d_c || M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 2) return SURGE_E_INVALID_ARG;
   if (epi == EPI_BIAS_LN && (!d_res || !d_gamma || !d_beta)) return SURGE_E_INVALID_ARG;
-  const int BN = gemm_bn_for(N, epi);
+  const int BN = gemm_bn_for(N, K, epi);
   if (BN == 0 || K % 64 != 0) return SURGE_E_INVALID_ARG;
   if (init_tma_encoder() != cudaSuccess) return SURGE_E_CUDA;
   CUtensorMap ta, tb;
@@ -1144,12 +1144,12 @@ surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int6
   int32_t max_len = 0;
   for (int64_t i = 0; i < n_texts; ++i) max_len = std::max(max_len, hcu[i + 1] - hcu[i]);
   const int32_t ntok = hcu[n_texts] - hcu[0];
-  int32_t* win = nullptr;
-  if (cudaMalloc(&win, (size_t(ntok) / 32 + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
-  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, win, false, heads,
+  int32_t* seg = nullptr;
+  if (cudaMalloc(&seg, (2 * size_t(ntok) + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
+  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, seg, false, heads,
                                           head_dim, d_out, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
-  cudaFree(win);
+  cudaFree(seg);
   return (e == cudaSuccess && e2 == cudaSuccess) ? SURGE_OK : SURGE_E_CUDA;
 }
 

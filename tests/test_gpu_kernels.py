@@ -106,11 +106,11 @@ def ref_attention(qkv, cu, heads, dh):
     return out
 
 
-@pytest.mark.parametrize("heads,dh,maxlen", [(12, 32, 128), (4, 16, 64), (12, 32, 20), (16, 64, 300)])
+@pytest.mark.parametrize("heads,dh,maxlen", [(12, 32, 128), (4, 16, 64), (12, 32, 20), (16, 64, 300), (12, 32, 65)])
 def test_attention_vs_torch(N, heads, dh, maxlen):
     rng = np.random.default_rng(heads * dh + maxlen)
     lens = rng.integers(1, maxlen + 1, size=97).astype(np.int32)
-    lens[:4] = [1, 2, 31, min(33, maxlen)]
+    lens[:6] = [1, 2, 31, min(33, maxlen), min(64, maxlen), min(65, maxlen)]   # tile/long kernel boundary
     lens[-1] = maxlen
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     T = int(cu[-1])

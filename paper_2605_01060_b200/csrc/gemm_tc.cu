@@ -39,8 +39,11 @@ struct TileCfg {
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
                                    : ACC_COLS <= 256 ? 256 : 512;
   static constexpr int HEAD_BYTES = 1024;                         // mbarriers + TMEM slot
-  static constexpr int STATS_BYTES = EPI == EPI_BIAS_LN ? 2 * 2 * BM * 4 * 4 : 0;   // [buf][half][row] x float4
-  static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES;
+  static constexpr int STATS_BYTES =                              // LN: stats + bias/gamma/beta, 1 KB aligned
+      EPI == EPI_BIAS_LN ? ((2 * 2 * BM * 4 * 4 + 3 * BN * 4 + 1023) / 1024) * 1024 : 0;
+  static constexpr int STG_BUFS = EPI == EPI_BIAS_LN ? 1 : 2;    // per-warp output staging buffers
+  static constexpr int STG_BYTES = NUM_EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
+  static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES + STG_BYTES;
   static constexpr int MAX_SMEM = 227 * 1024;
   static constexpr int MAX_STAGES = 8;
   static constexpr int HALF = BN / 2;                             // columns per epilogue warp
@@ -95,7 +98,8 @@ struct Sched {
 //                 epilogue of tile i overlaps the mainloop of tile i + 1.
 template <int BN, int EPI, bool WS>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
                    float eps, int stages) {
@@ -110,7 +114,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* bfull = tempty + 2;                         // resident B slice landed (WS)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
   float4* stats = reinterpret_cast<float4*>(smem + T::HEAD_BYTES);                  // [2][2][BM]
-  uint8_t* sB = smem + T::HEAD_BYTES + T::STATS_BYTES;  // WS: resident [K/64][BN x 128 B]; else ring
+  float* s_bias = reinterpret_cast<float*>(stats + 2 * 2 * BM);                      // LN: [BN] each
+  float* s_gamma = s_bias + BN;
+  float* s_beta = s_gamma + BN;
+  uint8_t* sStg = smem + T::HEAD_BYTES + T::STATS_BYTES;  // [epi warp][STG_BUFS][2 KB] (1 KB aligned)
+  uint8_t* sB = sStg + T::STG_BYTES;                    // WS: resident [K/64][BN x 128 B]; else ring
   uint8_t* sA = sB + T::b_res_bytes(K, WS);             // [stages] x 16 KB
   uint8_t* sBs = sA + stages * A_STAGE_BYTES;           // streaming B ring [stages] x B_STAGE_BYTES
 
@@ -209,6 +217,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue (warps 4..11)
+    if constexpr (EPI == EPI_BIAS_LN) {       // LN tiles span all N columns: constants once
+      for (int i = threadIdx.x - 128; i < BN; i += NUM_EPI_WARPS * 32) {
+        s_bias[i] = bias[i];
+        s_gamma[i] = gamma[i];
+        s_beta[i] = beta[i];
+      }
+      named_bar_sync(5, NUM_EPI_WARPS * 32);
+    }
+    int stg = 0;                              // staged output boxes issued by this warp
     const int q = warp & 3;                   // TMEM lane quadrant this warp may access
     const int hh = (warp - 4) >> 2;           // column half
     const int c_lo = hh * T::HALF;
@@ -220,25 +237,51 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = m0 + q * 32 + lane;
       const bool ok = row < M;
       const uint32_t taddr = tmem_base + acc * BN + (uint32_t(q * 32) << 16);
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
-        // 32 columns per step: one TMEM load (x32) + the bias slice, then fp32x2 math, 4 x 16-B stores
-        uint16_t* crow = C + size_t(row) * N + n0;
-#pragma unroll 1
-        for (int c = c_lo; c < c_lo + T::HALF; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c, r);
-          float4 b4[8];
-          const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c);
+      // Output: each warp stages its 32 rows x 32 columns (bf16) in a private, 64-byte-swizzled
+      // smem buffer and one lane TMA-stores the box (coalesced; rows >= M clipped by TMA).
+      auto stage_store = [&](const uint32_t (&p)[16], int col) {
+        uint8_t* buf = sStg + ((warp - 4) * T::STG_BUFS + (stg % T::STG_BUFS)) * 2048;
+        if (lane == 0 && stg >= T::STG_BUFS) bulk_wait_read<T::STG_BUFS - 1>();   // buffer drained
+        __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 8; ++i) b4[i] = __ldg(bp + i);
-          tmem_ld_wait();
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, buf, col, m0 + q * 32);
+          bulk_commit();
+        }
+        ++stg;
+      };
+      constexpr int NSTEP = T::HALF / 32;     // 32-column steps per warp
+      if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
+        // Software-pipelined over 32-column steps: the TMEM load and bias slice of step k+1 are in
+        // flight while step k is computed and stored (tcgen05.wait::ld then covers only step k+1).
+        const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c_lo);
+        uint32_t r[2][32];
+        float4 b4[2][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) b4[0][i] = __ldg(bp + i);
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        tmem_ld32(taddr + c_lo, r[0]);
+#pragma unroll
+        for (int k = 0; k < NSTEP; ++k) {
+          const int cur = k & 1;
+          tmem_ld_wait_regs(r[cur]);
+          if (k + 1 < NSTEP) {
+            tmem_ld32(taddr + c_lo + 32 * (k + 1), r[cur ^ 1]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) b4[cur ^ 1][i] = __ldg(bp + 8 * (k + 1) + i);
+          }
           uint32_t p[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const f32x2 v01 = fadd2(f2(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1])), f2(b4[i].x, b4[i].y));
-            const f32x2 v23 = fadd2(f2(__uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])), f2(b4[i].z, b4[i].w));
+            const float4 bb = b4[cur][i];
+            const f32x2 v01 = fadd2(f2(__uint_as_float(r[cur][4 * i]), __uint_as_float(r[cur][4 * i + 1])), f2(bb.x, bb.y));
+            const f32x2 v23 = fadd2(f2(__uint_as_float(r[cur][4 * i + 2]), __uint_as_float(r[cur][4 * i + 3])), f2(bb.z, bb.w));
             float v0 = f2lo(v01), v1 = f2hi(v01), v2 = f2lo(v23), v3 = f2hi(v23);
             if constexpr (EPI == EPI_BIAS_GELU) {
               gelu2(v0, v1);
@@ -247,92 +290,93 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             p[2 * i] = pack_bf16x2(v0, v1);
             p[2 * i + 1] = pack_bf16x2(v2, v3);
           }
-          if (ok) {
-            uint4* dst = reinterpret_cast<uint4*>(crow + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
-          }
+          stage_store(p, n0 + c_lo + 32 * k);
         }
       } else {
-        // LayerNorm over the full row (BN == N), two warps per row (column halves):
-        // pass 1: shifted partial sums per half -> combine via smem (Chan's formula); pass 2: write.
-        const uint16_t* rrow = res + size_t(ok ? row : 0) * N;
-        uint16_t* crow = C + size_t(row) * N;
-        float shift = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll 1
-        for (int c = c_lo; c < c_lo + T::HALF; c += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c, r);
-          const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
-          const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
-          float bv[16];
-          const float4* bp = reinterpret_cast<const float4*>(bias + c);
+        // LayerNorm over the full row (BN == N), two warps per row (column halves).
+        // pass 1: v = acc + bias + residual, written back to TMEM in place, shifted partial sums;
+        //         the residual slice and TMEM load of step k+1 are in flight while step k is
+        //         computed (the first residual slice is fetched before the accumulator is ready);
+        // combine the halves (Chan) through smem; pass 2: y = (v - mean) rstd gamma + beta,
+        //         TMEM loads pipelined the same way.
+        const uint16_t* rrow = res + size_t(ok ? row : 0) * N + c_lo;
+        uint32_t r[2][32];
+        uint4 rs[2][4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 b4 = __ldg(bp + i);
-            bv[4 * i] = b4.x; bv[4 * i + 1] = b4.y; bv[4 * i + 2] = b4.z; bv[4 * i + 3] = b4.w;
+        for (int i = 0; i < 4; ++i) rs[0][i] = reinterpret_cast<const uint4*>(rrow)[i];
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        tmem_ld32(taddr + c_lo, r[0]);
+        float shift = 0.f;
+        f32x2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < NSTEP; ++k) {
+          const int cur = k & 1;
+          const int c = c_lo + 32 * k;
+          tmem_ld_wait_regs(r[cur]);
+          if (k + 1 < NSTEP) {
+            tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rs[cur ^ 1][i] = reinterpret_cast<const uint4*>(rrow + 32 * (k + 1))[i];
           }
-          tmem_ld_wait();
-          const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+          const uint32_t rr[16] = {rs[cur][0].x, rs[cur][0].y, rs[cur][0].z, rs[cur][0].w,
+                                   rs[cur][1].x, rs[cur][1].y, rs[cur][1].z, rs[cur][1].w,
+                                   rs[cur][2].x, rs[cur][2].y, rs[cur][2].z, rs[cur][2].w,
+                                   rs[cur][3].x, rs[cur][3].y, rs[cur][3].z, rs[cur][3].w};
+          if (k == 0) shift = __uint_as_float(r[cur][0]) + s_bias[c] + bf16lo(rr[0]);
+          uint32_t w[32];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float v = __uint_as_float(r[i]) + bv[i] + ((i & 1) ? bf16hi(rr[i >> 1]) : bf16lo(rr[i >> 1]));
-            if (c == c_lo && i == 0) shift = v;
-            const float d = v - shift;
-            s1 += d;
-            s2 += d * d;
+            const float2 bb = *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
+            const f32x2 v = fadd2(fadd2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])),
+                                        f2(bb.x, bb.y)),
+                                  f2(bf16lo(rr[i]), bf16hi(rr[i])));
+            const f32x2 dv = fadd2(v, f2(-shift, -shift));
+            s1 = fadd2(s1, dv);
+            s2 = ffma2(dv, dv, s2);
+            w[2 * i] = __float_as_uint(f2lo(v));
+            w[2 * i + 1] = __float_as_uint(f2hi(v));
           }
+          tmem_st32(taddr + c, w);
         }
+        tmem_st_wait();
+        const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
         const int sbuf = it & 1;
-        stats[(sbuf * 2 + hh) * BM + q * 32 + lane] = make_float4(shift, s1, s2, 0.f);
+        stats[(sbuf * 2 + hh) * BM + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);
         named_bar_sync(1 + q, 64);            // the two warps of this quadrant
         const float4 o = stats[(sbuf * 2 + (hh ^ 1)) * BM + q * 32 + lane];
         const float nh = float(T::HALF);
-        const float mean_a = shift + s1 / nh, m2_a = s2 - s1 * s1 / nh;
+        const float mean_a = shift + S1 / nh, m2_a = S2 - S1 * S1 / nh;
         const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
         const float dm = mean_a - mean_b;
         const float mean = 0.5f * (mean_a + mean_b);
         const float var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
         const float rstd = rsqrtf(var + eps);
-#pragma unroll 1
-        for (int c = c_lo; c < c_lo + T::HALF; c += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c, r);
-          const uint4 ra = reinterpret_cast<const uint4*>(rrow + c)[0];
-          const uint4 rb = reinterpret_cast<const uint4*>(rrow + c)[1];
-          float bv[16], gv[16], be[16];
+        const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);
+        tmem_ld32(taddr + c_lo, r[0]);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + c) + i);
-            const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + c) + i);
-            const float4 e4 = __ldg(reinterpret_cast<const float4*>(beta + c) + i);
-            bv[4 * i] = b4.x; bv[4 * i + 1] = b4.y; bv[4 * i + 2] = b4.z; bv[4 * i + 3] = b4.w;
-            gv[4 * i] = g4.x; gv[4 * i + 1] = g4.y; gv[4 * i + 2] = g4.z; gv[4 * i + 3] = g4.w;
-            be[4 * i] = e4.x; be[4 * i + 1] = e4.y; be[4 * i + 2] = e4.z; be[4 * i + 3] = e4.w;
-          }
-          tmem_ld_wait();
-          const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-          uint32_t p[8];
+        for (int k = 0; k < NSTEP; ++k) {
+          const int cur = k & 1;
+          const int c = c_lo + 32 * k;
+          tmem_ld_wait_regs(r[cur]);
+          if (k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+          uint32_t p[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j0 = 2 * i, j1 = 2 * i + 1;
-            float v0 = __uint_as_float(r[j0]) + bv[j0] + bf16lo(rr[i]);
-            float v1 = __uint_as_float(r[j1]) + bv[j1] + bf16hi(rr[i]);
-            v0 = (v0 - mean) * rstd * gv[j0] + be[j0];
-            v1 = (v1 - mean) * rstd * gv[j1] + be[j1];
-            p[i] = pack_bf16x2(v0, v1);
+          for (int i = 0; i < 16; ++i) {
+            const float2 gg = *reinterpret_cast<const float2*>(s_gamma + c + 2 * i);
+            const float2 be = *reinterpret_cast<const float2*>(s_beta + c + 2 * i);
+            const f32x2 z = ffma2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])), k_rstd, k_off);
+            const f32x2 y = ffma2(z, f2(gg.x, gg.y), f2(be.x, be.y));
+            p[i] = pack_bf16x2(f2lo(y), f2hi(y));
           }
-          if (ok) {
-            uint4* dst = reinterpret_cast<uint4*>(crow + c);
-            dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-            dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
-          }
+          stage_store(p, c);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait_all();           // output stores complete before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
@@ -376,7 +420,7 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   } else {
     grid = int(std::min<int64_t>(m_tiles * n_tiles, num_sms()));
   }
-  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
+  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
                                          g.eps, stages);
   return cudaGetLastError();
 }
@@ -386,7 +430,7 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
 template <int BN, int EPI>
 bool use_ws(const GemmArgs& g) {
   using T = TileCfg<BN, EPI>;
-  return g.epi != EPI_BIAS_LN && T::stages(g.K, true) >= 4 && (g.M + BM - 1) / BM >= num_sms() / (g.N / BN);
+  return g.epi != EPI_BIAS_LN && T::stages(g.K, true) >= 3 && (g.M + BM - 1) / BM >= num_sms() / (g.N / BN);
 }
 
 template <int BN, int EPI>
@@ -426,11 +470,26 @@ cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uin
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols) {
+  if (!g_encode_tiled) {
+    cudaError_t e = init_tma_encoder();
+    if (e != cudaSuccess) return e;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 int gemm_bn_for(int N, int K, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
   // 192-column slices whose [192 x K] weight block can stay resident (weight-stationary) win over
   // streaming 256-column tiles: A is re-read N/192 times from L2 but B is read once per CTA.
-  if (N % 192 == 0 && TileCfg<192, EPI_BIAS>::stages(K, true) >= 4) return 192;
+  if (N % 192 == 0 && TileCfg<192, EPI_BIAS>::stages(K, true) >= 3) return 192;
   if (N % 256 == 0) return 256;
   if (N % 192 == 0) return 192;
   if (N % 128 == 0) return 128;

@@ -15,6 +15,7 @@ enum Epilogue : int { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_BIAS_LN = 2 };
 struct GemmArgs {
   const CUtensorMap* tmA;   // A [M x K]
   const CUtensorMap* tmB;   // B [N x K]
+  const CUtensorMap* tmC;   // C [M x N], store map (make_tmap_store_bf16)
   int64_t M;
   int N, K, epi;
   const float* bias;
@@ -27,6 +28,8 @@ struct GemmArgs {
 
 cudaError_t init_tma_encoder();
 cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// Output map for the GEMM epilogue's TMA stores: box 32 rows x 32 columns, 64-byte swizzle.
+cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols);
 int gemm_bn_for(int N, int K, int epi);
 uint32_t gemm_b_box_rows(int BN);
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);

@@ -67,6 +67,8 @@ GEMM_CASES = [
     (129, 384, 384, 2), (4133, 384, 384, 2), (1000, 384, 1536, 2),
     (77, 192, 64, 0), (300, 256, 64, 1), (300, 64, 64, 2), (333, 64, 256, 2),
     (256, 128, 128, 0), (200, 64, 192, 0),
+    # many tiles per CTA (weight-stationary slices, TMEM double buffering) + ragged tails
+    (50001, 1152, 384, 0), (50001, 1536, 384, 1), (50001, 384, 384, 2), (20001, 384, 1536, 2),
 ]
 
 

@@ -183,37 +183,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
-      if constexpr (WS) mbar_wait(bfull, 0);
-      int s = 0;
-      uint32_t ph = 0;
-      int it = 0;
-      for (int t = sc.t0; t < sc.tend; t += sc.dt, ++it) {
-        const int acc = it % ACC;
-        const uint32_t aph = (it / ACC) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);     // epilogue drained this accumulator buffer
+    // -------------------------------------------------------------------- MMA issuer
+    // The whole warp walks the loop (warp-uniform control flow and operands, so descriptors live
+    // in uniform registers); one elected lane issues the tcgen05.mma / commit instructions.
+    // Shared-memory descriptors are built once and advanced by adding (byte offset >> 4) to their
+    // start-address field.
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
+    const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
+    const uint64_t b_desc0 = umma_desc_sw128(smem_u32(WS ? sB : sBs));
+    if constexpr (WS) mbar_wait(bfull, 0);
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int t = sc.t0; t < sc.tend; t += sc.dt, ++it) {
+      const int acc = it % ACC;
+      const uint32_t aph = (it / ACC) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + s * A_STAGE_BYTES);
-          const uint32_t b0 = smem_u32(WS ? sB + kb * T::B_STAGE_BYTES : sBs + s * T::B_STAGE_BYTES);
+        if (elect_one()) {
+          const uint64_t a_desc = a_desc0 + uint64_t((s * A_STAGE_BYTES) >> 4);
+          const uint64_t b_desc = b_desc0 + uint64_t(((WS ? kb : s) * T::B_STAGE_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
-            for (int j = 0; j < T::N_MMA; ++j) {
-              tc_mma_bf16(d0 + j * T::MMA_N, umma_desc_sw128(a0 + k * 32),
-                          umma_desc_sw128(b0 + j * T::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
-            }
+            for (int j = 0; j < T::N_MMA; ++j)
+              tc_mma_bf16(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), b_desc + uint64_t((j * T::MMA_N * 128 + k * 32) >> 4),
+                          idesc, (kb | k) != 0);
           }
           tc_commit(&empty[s]);               // frees this smem stage when the MMAs retire
-          if (++s == stages) { s = 0; ph ^= 1; }
         }
-        tc_commit(&tfull[acc]);               // accumulator complete
+        __syncwarp();
+        if (++s == stages) { s = 0; ph ^= 1; }
       }
+      if (elect_one()) tc_commit(&tfull[acc]);   // accumulator complete
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue (warps 4..11)

@@ -41,7 +41,7 @@ struct TileCfg {
   static constexpr int HEAD_BYTES = 1024;                         // mbarriers + TMEM slot
   static constexpr int STATS_BYTES =                              // LN: stats + bias/gamma/beta, 1 KB aligned
       EPI == EPI_BIAS_LN ? ((2 * 2 * BM * 4 * 4 + 3 * BN * 4 + 1023) / 1024) * 1024 : 0;
-  static constexpr int STG_BUFS = EPI == EPI_BIAS_LN ? 1 : 2;    // per-warp output staging buffers
+  static constexpr int STG_BUFS = 1;                              // per-warp output staging buffers
   static constexpr int STG_BYTES = NUM_EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
   static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES + STG_BYTES;
   static constexpr int MAX_SMEM = 227 * 1024;
@@ -90,9 +90,9 @@ struct Sched {
 };
 
 // Persistent, warp-specialised tcgen05 GEMM.
-//   warp 0        TMA producer (one lane): `stages`-deep smem ring (A, plus B when streaming)
-//   warp 1        MMA issuer (one lane): UMMA 128 x MMA_N x 16, accumulator buffer it % ACC
-//   warp 2        TMEM allocator
+//   warps 0,2,3   TMA producers (one lane each): `stages`-deep smem ring (A, plus B when streaming)
+//   warp 1        MMA issuer (whole warp, one elected lane): UMMA 128 x MMA_N x 16, accumulator it % ACC
+//   warp 2        also the TMEM allocator
 //   warps 4..11   epilogue: warp w reads TMEM lane quadrant w % 4, column half (w - 4) / 4;
 //                 the accumulator buffer is released as soon as it is drained, so with ACC = 2 the
 //                 epilogue of tile i overlaps the mainloop of tile i + 1.
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], WS ? 1 : 1 + T::N_LOADS);   // one arrive (+tx) per box
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < ACC; ++a) {
@@ -149,12 +149,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2 || warp == 3) {
     if (lane == 0) {
-      // ------------------------------------------------------------------ TMA producer
+      // ------------------------------------------------------------------ TMA producers
+      // Three producer threads (warps 0, 2, 3) share the ring: box b of k-block counter c is issued
+      // by producer (c * NBOX + b) % 3.  One thread sustains only ~one TMA box per ~500 cycles
+      // (measured: scripts/microbench/tma_bw2.cu), so a single producer would cap A+B ingest far
+      // below what the tensor core consumes.
+      constexpr int NPROD = 3;
+      constexpr int NBOX = WS ? 1 : 1 + T::N_LOADS;
+      const int p = warp == 0 ? 0 : warp - 1;
       const uint64_t pol_w = l2_policy_evict_last();   // weights: re-read by every M tile
       if constexpr (WS) {
-        if (sc.t0 < sc.tend) {
+        if (p == 0 && sc.t0 < sc.tend) {
           const int n0 = sc.slice * BN;
           mbar_arrive_expect_tx(bfull, uint32_t(BN) * K * 2);
           for (int kb = 0; kb < num_kb; ++kb)
@@ -164,21 +171,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                n0 + j * T::B_BOX, pol_w);
         }
       }
-      int s = 0;
-      uint32_t ph = 0;
+      uint32_t c = 0;
       for (int t = sc.t0; t < sc.tend; t += sc.dt) {
         const int m0 = sc.m0(t), n0 = sc.n0(t) * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], T::stage_bytes(WS));
-          tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
-          if constexpr (!WS) {
+        for (int kb = 0; kb < num_kb; ++kb, ++c) {
+          const int s = int(c % uint32_t(stages));
+          const uint32_t ph = (c / uint32_t(stages)) & 1;
 #pragma unroll
-            for (int j = 0; j < T::N_LOADS; ++j)
+          for (int b = 0; b < NBOX; ++b) {
+            if (int((c * NBOX + b) % NPROD) != p) continue;
+            mbar_wait(&empty[s], ph ^ 1);
+            if (b == 0) {
+              mbar_arrive_expect_tx(&full[s], A_STAGE_BYTES);
+              tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
+            } else {
+              const int j = b - 1;
+              mbar_arrive_expect_tx(&full[s], T::B_BOX * 128);
               tma_load_2d_hint(sBs + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
                                n0 + j * T::B_BOX, pol_w);
+            }
           }
-          if (++s == stages) { s = 0; ph ^= 1; }
         }
       }
     }

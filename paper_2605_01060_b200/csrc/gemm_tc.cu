@@ -99,14 +99,16 @@ struct Sched {
 template <int BN, int EPI, bool WS>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, int M, int N,
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
                    float eps, int stages) {
   using T = TileCfg<BN, EPI>;
   constexpr int ACC = T::ACC;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the __shared__ array (an integer round trip would turn every
+  // shared access into a generic one)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [stages]
   uint64_t* empty = full + T::MAX_STAGES;               // [stages]
   uint64_t* tfull = empty + T::MAX_STAGES;              // [ACC]
@@ -182,6 +184,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (int((c * NBOX + b) % NPROD) != p) continue;
             mbar_wait(&empty[s], ph ^ 1);
             if (b == 0) {
+              if constexpr (EPI == EPI_BIAS_LN) {
+                // warm L2 with this tile's residual rows (read by the LN epilogue); the C map
+                // covers the residual's shape, the map of R itself is tmR
+                if (kb < N / 64) tma_prefetch_2d(&tmR, kb * 64, m0);
+              }
               mbar_arrive_expect_tx(&full[s], A_STAGE_BYTES);
               tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
             } else {
@@ -439,7 +446,7 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   } else {
     grid = int(std::min<int64_t>(m_tiles * n_tiles, num_sms()));
   }
-  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
+  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, g.tmR ? *g.tmR : *g.tmC, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
                                          g.eps, stages);
   return cudaGetLastError();
 }

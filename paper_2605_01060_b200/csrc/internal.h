@@ -16,6 +16,7 @@ struct GemmArgs {
   const CUtensorMap* tmA;   // A [M x K]
   const CUtensorMap* tmB;   // B [N x K]
   const CUtensorMap* tmC;   // C [M x N], store map (make_tmap_store_bf16)
+  const CUtensorMap* tmR;   // residual [M x N] load map (make_tmap_bf16, box 128 rows) for L2 prefetch (LN)
   int64_t M;
   int N, K, epi;
   const float* bias;

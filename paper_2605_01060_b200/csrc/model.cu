@@ -232,19 +232,19 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.seg, true, s_.heads, d / s_.heads, ws.O, st));
     if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
     // K6: X1 = LN(O Wo^T + bo + X)
-    g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
+    g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
     g.gamma = L.ln1_g; g.beta = L.ln1_b; g.C = ws.X1;
     if (P) prof->begin(st, &ev);
     SURGE_TRY(launch_gemm(g, st));
     if (P) prof->end(KK_OUT_LN, st, ev, 2 * M * D * D, 2 * (M * D + D * D + 2 * M * D));
     // K7: H = GELU(X1 W1^T + b1)
-    g.tmA = &tmX1; g.tmB = &L.tm_w1; g.tmC = &smH; g.N = f; g.K = d; g.epi = EPI_BIAS_GELU; g.bias = L.b1; g.res = nullptr;
+    g.tmA = &tmX1; g.tmB = &L.tm_w1; g.tmC = &smH; g.tmR = nullptr; g.N = f; g.K = d; g.epi = EPI_BIAS_GELU; g.bias = L.b1; g.res = nullptr;
     g.gamma = g.beta = nullptr; g.C = ws.H;
     if (P) prof->begin(st, &ev);
     SURGE_TRY(launch_gemm(g, st));
     if (P) prof->end(KK_FFN1, st, ev, 2 * M * F * D, 2 * (M * D + F * D + M * F));
     // K8: X = LN(H W2^T + b2 + X1)
-    g.tmA = &tmH; g.tmB = &L.tm_w2; g.tmC = &smX; g.N = d; g.K = f; g.epi = EPI_BIAS_LN; g.bias = L.b2; g.res = ws.X1;
+    g.tmA = &tmH; g.tmB = &L.tm_w2; g.tmC = &smX; g.tmR = &tmX1; g.N = d; g.K = f; g.epi = EPI_BIAS_LN; g.bias = L.b2; g.res = ws.X1;
     g.gamma = L.ln2_g; g.beta = L.ln2_b; g.C = ws.X;
     if (P) prof->begin(st, &ev);
     SURGE_TRY(launch_gemm(g, st));

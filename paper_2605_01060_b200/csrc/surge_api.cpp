@@ -1128,7 +1128,10 @@ surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float
   if (make_tmap_bf16(&tb, d_b, uint64_t(N), uint64_t(K), gemm_b_box_rows(BN)) != cudaSuccess) return SURGE_E_CUDA;
   CUtensorMap tc;
   if (make_tmap_store_bf16(&tc, d_c, uint64_t(M), uint64_t(N)) != cudaSuccess) return SURGE_E_CUDA;
-  GemmArgs g{&ta, &tb, &tc, M, N, K, epi, d_bias, d_res, d_gamma, d_beta, d_c, ln_eps};
+  CUtensorMap tr;
+  if (make_tmap_bf16(&tr, epi == EPI_BIAS_LN ? d_res : d_c, uint64_t(M), uint64_t(N), 128) != cudaSuccess)
+    return SURGE_E_CUDA;
+  GemmArgs g{&ta, &tb, &tc, &tr, M, N, K, epi, d_bias, d_res, d_gamma, d_beta, d_c, ln_eps};
   cudaError_t e = launch_gemm(g, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SURGE_OK : SURGE_E_CUDA;
 }

@@ -27,13 +27,17 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
 constexpr int NUM_EPI_WARPS = 8;             // 2 per TMEM lane quadrant, splitting the columns
 constexpr int GEMM_THREADS = 128 + NUM_EPI_WARPS * 32;
 
-template <int BN, int EPI>
+// PAIR: a cluster of two CTAs runs cta_group::2 MMAs on 256 x BN tiles; each CTA holds its 128
+// rows of A and of the accumulator, and half of every MMA's N rows of B (so B traffic per CTA
+// halves).
+template <int BN, int EPI, bool PAIR = false>
 struct TileCfg {
-  static constexpr int B_BOX = (BN <= 256) ? BN : BN / 2;       // TMA box rows for B
-  static constexpr int N_LOADS = BN / B_BOX;
-  static constexpr int MMA_N = B_BOX;                            // <= 256, multiple of 16
+  static constexpr int MMA_N = (BN <= 256) ? BN : BN / 2;       // <= 256, multiple of 16
   static constexpr int N_MMA = BN / MMA_N;
-  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+  static constexpr int B_BOX = PAIR ? MMA_N / 2 : MMA_N;         // TMA box rows for B (this CTA)
+  static constexpr int N_LOADS = N_MMA;                          // B boxes per k-block
+  static constexpr int B_STAGE_BYTES = N_LOADS * B_BOX * 128;    // this CTA's B bytes per k-block
+  static constexpr int UMMA_M = PAIR ? 2 * BM : BM;
   static constexpr int ACC = (2 * BN <= 512) ? 2 : 1;            // TMEM accumulator buffers
   static constexpr int ACC_COLS = ACC * BN;
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
@@ -48,7 +52,7 @@ struct TileCfg {
   static constexpr int MAX_STAGES = 8;
   static constexpr int HALF = BN / 2;                             // columns per epilogue warp
   static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
-  static_assert(B_BOX * N_LOADS == BN, "B box split");
+  static_assert(B_BOX * N_LOADS * (PAIR ? 2 : 1) == BN, "B box split");
   static_assert(HALF % 32 == 0, "epilogue column split");
   // Weight-stationary (ws): the CTA's whole B slice [BN x K] stays resident; only A streams.
   __host__ __device__ static int b_res_bytes(int K, bool ws) { return ws ? BN * K * 2 : 0; }
@@ -69,23 +73,29 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // Weight-stationary (WS = true): CTA c owns the N slice c % n_tiles for the whole launch (its B
 // slice is loaded once and stays in shared memory) and walks M tiles c / n_tiles, + gridDim.x /
 // n_tiles, ...; the grid is a multiple of n_tiles.
-template <bool WS>
+// PAIR (streaming only): the unit is the cluster (blockIdx.x / 2) and M tiles are 256 rows; CTA
+// rank r of the pair owns rows [256 t + 128 r, +128).
+template <bool WS, bool PAIR = false>
 struct Sched {
-  int t0, dt, tend, n_tiles, slice;
-  __device__ Sched(int m_tiles, int n_tiles_) : n_tiles(n_tiles_) {
+  int t0, dt, tend, n_tiles, slice, rank;
+  __device__ Sched(int M, int n_tiles_) : n_tiles(n_tiles_) {
+    rank = PAIR ? int(blockIdx.x & 1) : 0;
+    const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+    const int units = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+    const int m_tiles = (M + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
     if (WS) {
-      slice = blockIdx.x % n_tiles;
-      t0 = blockIdx.x / n_tiles;
-      dt = gridDim.x / n_tiles;
+      slice = unit % n_tiles;
+      t0 = unit / n_tiles;
+      dt = units / n_tiles;
       tend = m_tiles;
     } else {
       slice = 0;
-      t0 = blockIdx.x;
-      dt = gridDim.x;
+      t0 = unit;
+      dt = units;
       tend = m_tiles * n_tiles;
     }
   }
-  __device__ int m0(int t) const { return (WS ? t : t / n_tiles) * BM; }
+  __device__ int m0(int t) const { return (WS ? t : t / n_tiles) * (PAIR ? 2 * BM : BM) + rank * BM; }
   __device__ int n0(int t) const { return (WS ? slice : t % n_tiles); }
 };
 
@@ -96,15 +106,16 @@ struct Sched {
 //   warps 4..11   epilogue: warp w reads TMEM lane quadrant w % 4, column half (w - 4) / 4;
 //                 the accumulator buffer is released as soon as it is drained, so with ACC = 2 the
 //                 epilogue of tile i overlaps the mainloop of tile i + 1.
-template <int BN, int EPI, bool WS>
+template <int BN, int EPI, bool WS, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
                    float eps, int stages) {
-  using T = TileCfg<BN, EPI>;
+  using T = TileCfg<BN, EPI, PAIR>;
   constexpr int ACC = T::ACC;
+  static_assert(!(WS && PAIR), "pairs run streaming tiles only");
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the __shared__ array (an integer round trip would turn every
   // shared access into a generic one)
@@ -126,28 +137,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_kb = K / BK;
-  const Sched<WS> sc((M + BM - 1) / BM, N / BN);
+  const Sched<WS, PAIR> sc(M, N / BN);
+  const bool leader = sc.rank == 0;              // PAIR: the CTA that issues the MMAs
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], WS ? 1 : 1 + T::N_LOADS);   // one arrive (+tx) per box
+      mbar_init(&full[s], WS ? 1 : 1 + T::N_LOADS);   // one arrive (+tx) per box (leader's boxes in PAIR)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], NUM_EPI_WARPS);
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * NUM_EPI_WARPS);
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, T::TMEM_COLS);
-    tmem_relinquish();
+    if constexpr (PAIR) {
+      tmem_alloc_pair(tmem_slot, T::TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, T::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();            // peer barriers initialised before any remote use
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -185,29 +203,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_wait(&empty[s], ph ^ 1);
             if (b == 0) {
               if constexpr (EPI == EPI_BIAS_LN) {
-                // warm L2 with this tile's residual rows (read by the LN epilogue); the C map
-                // covers the residual's shape, the map of R itself is tmR
+                // warm L2 with this tile's residual rows (read by the LN epilogue)
                 if (kb < N / 64) tma_prefetch_2d(&tmR, kb * 64, m0);
               }
-              mbar_arrive_expect_tx(&full[s], A_STAGE_BYTES);
-              tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
+              if constexpr (PAIR) {               // both halves complete on the leader's barrier
+                if (leader) mbar_arrive_expect_tx(&full[s], 2 * A_STAGE_BYTES);
+                tma_load_2d_pair(sA + s * A_STAGE_BYTES, &tmA, mapa_shared(smem_u32(&full[s]), 0), kb * BK, m0,
+                                 l2_policy_evict_first());
+              } else {
+                mbar_arrive_expect_tx(&full[s], A_STAGE_BYTES);
+                tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &full[s], kb * BK, m0);
+              }
             } else {
               const int j = b - 1;
-              mbar_arrive_expect_tx(&full[s], T::B_BOX * 128);
-              tma_load_2d_hint(sBs + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
-                               n0 + j * T::B_BOX, pol_w);
+              if constexpr (PAIR) {               // rows [j MMA_N + r MMA_N/2, +MMA_N/2) of MMA j's B
+                if (leader) mbar_arrive_expect_tx(&full[s], 2 * T::B_BOX * 128);
+                tma_load_2d_pair(sBs + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB,
+                                 mapa_shared(smem_u32(&full[s]), 0), kb * BK,
+                                 n0 + j * T::MMA_N + sc.rank * T::B_BOX, pol_w);
+              } else {
+                mbar_arrive_expect_tx(&full[s], T::B_BOX * 128);
+                tma_load_2d_hint(sBs + s * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, &full[s], kb * BK,
+                                 n0 + j * T::B_BOX, pol_w);
+              }
             }
           }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // -------------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (warp-uniform control flow and operands, so descriptors live
     // in uniform registers); one elected lane issues the tcgen05.mma / commit instructions.
     // Shared-memory descriptors are built once and advanced by adding (byte offset >> 4) to their
     // start-address field.
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
+    constexpr uint32_t idesc = umma_idesc_bf16(T::UMMA_M, T::MMA_N);
     const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
     const uint64_t b_desc0 = umma_desc_sw128(smem_u32(WS ? sB : sBs));
     if constexpr (WS) mbar_wait(bfull, 0);
@@ -229,16 +259,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
-            for (int j = 0; j < T::N_MMA; ++j)
-              tc_mma_bf16(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), b_desc + uint64_t((j * T::MMA_N * 128 + k * 32) >> 4),
-                          idesc, (kb | k) != 0);
+            for (int j = 0; j < T::N_MMA; ++j) {
+              const uint64_t bd = b_desc + uint64_t((j * T::B_BOX * 128 + k * 32) >> 4);
+              if constexpr (PAIR) tc_mma_bf16_pair(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), bd, idesc, (kb | k) != 0);
+              else tc_mma_bf16(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), bd, idesc, (kb | k) != 0);
+            }
           }
-          tc_commit(&empty[s]);               // frees this smem stage when the MMAs retire
+          if constexpr (PAIR) tc_commit_pair_mc(&empty[s], 0x3);   // frees the stage in both CTAs
+          else tc_commit(&empty[s]);          // frees this smem stage when the MMAs retire
         }
         __syncwarp();
         if (++s == stages) { s = 0; ph ^= 1; }
       }
-      if (elect_one()) tc_commit(&tfull[acc]);   // accumulator complete
+      if (elect_one()) {                      // accumulator complete (both CTAs' halves in PAIR)
+        if constexpr (PAIR) tc_commit_pair_mc(&tfull[acc], 0x3);
+        else tc_commit(&tfull[acc]);
+      }
       __syncwarp();
     }
   } else if (warp >= 4) {
@@ -400,15 +436,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));   // leader's barrier
+        else mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) bulk_wait_all();           // output stores complete before the CTA retires
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();            // the peer may still read our smem / signal us
+  else __syncthreads();
   if (warp == 2) {
     __syncwarp();
-    tmem_dealloc(tmem_base, T::TMEM_COLS);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, T::TMEM_COLS);
+    else tmem_dealloc(tmem_base, T::TMEM_COLS);
   }
 }
 
@@ -425,10 +466,10 @@ int num_sms() {
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 
-template <int BN, int EPI, bool WS>
+template <int BN, int EPI, bool WS, bool PAIR = false>
 cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
-  using T = TileCfg<BN, EPI>;
-  auto kern = gemm_tc_kernel<BN, EPI, WS>;
+  using T = TileCfg<BN, EPI, PAIR>;
+  auto kern = gemm_tc_kernel<BN, EPI, WS, PAIR>;
   const int smem = T::smem_bytes(g.K, WS);
   const int stages = T::stages(g.K, WS);
   if (stages < 2 || smem > T::MAX_SMEM) return cudaErrorInvalidValue;
@@ -443,11 +484,31 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   if (WS) {
     const int64_t per = std::min<int64_t>(std::max<int64_t>(num_sms() / n_tiles, 1), m_tiles);
     grid = int(per * n_tiles);
+  } else if (PAIR) {
+    const int64_t m2 = (g.M + 2 * BM - 1) / (2 * BM);
+    grid = 2 * int(std::min<int64_t>(m2 * n_tiles, num_sms() / 2));
   } else {
     grid = int(std::min<int64_t>(m_tiles * n_tiles, num_sms()));
   }
-  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, g.tmR ? *g.tmR : *g.tmC, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
-                                         g.eps, stages);
+  const CUtensorMap tmR = g.tmR ? *g.tmR : *g.tmC;
+  if (PAIR) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = size_t(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
+                              g.beta, g.C, g.eps, stages);
+  }
+  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K,
+                                         g.bias, g.res, g.gamma, g.beta, g.C, g.eps, stages);
   return cudaGetLastError();
 }
 
@@ -463,6 +524,8 @@ template <int BN, int EPI>
 cudaError_t launch_gemm_bn(const GemmArgs& g, cudaStream_t st) {
   if constexpr (EPI != EPI_BIAS_LN) {
     if (use_ws<BN, EPI>(g)) return launch_gemm_t<BN, EPI, true>(g, st);
+  } else {
+    if (gemm_use_pair(g.N, g.K, g.epi)) return launch_gemm_t<BN, EPI, false, true>(g, st);
   }
   return launch_gemm_t<BN, EPI, false>(g, st);
 }
@@ -511,6 +574,9 @@ cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t row
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// LN GEMMs (full-row tiles, single TMEM accumulator) run as CTA pairs: half the B bytes per CTA.
+bool gemm_use_pair(int N, int K, int epi) { return epi == EPI_BIAS_LN && N == 384 && K % 64 == 0; }
+
 int gemm_bn_for(int N, int K, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
   // 192-column slices whose [192 x K] weight block can stay resident (weight-stationary) win over
@@ -523,7 +589,11 @@ int gemm_bn_for(int N, int K, int epi) {
   return 0;
 }
 
-uint32_t gemm_b_box_rows(int BN) { return BN <= 256 ? BN : BN / 2; }
+uint32_t gemm_b_box_rows(int N, int K, int epi) {
+  const int BN = gemm_bn_for(N, K, epi);
+  const int mma_n = BN <= 256 ? BN : BN / 2;
+  return uint32_t(gemm_use_pair(N, K, epi) ? mma_n / 2 : mma_n);
+}
 
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   const int BN = gemm_bn_for(g.N, g.K, g.epi);

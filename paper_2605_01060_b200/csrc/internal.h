@@ -32,7 +32,8 @@ cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uin
 // Output map for the GEMM epilogue's TMA stores: box 32 rows x 32 columns, 64-byte swizzle.
 cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols);
 int gemm_bn_for(int N, int K, int epi);
-uint32_t gemm_b_box_rows(int BN);
+bool gemm_use_pair(int N, int K, int epi);
+uint32_t gemm_b_box_rows(int N, int K, int epi);   // TMA box rows of the B (weight) tensor map
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);
 
 // K1: cu[0..n], row_off[0..m], tok_off[0..m] (single CTA)

@@ -108,10 +108,10 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(take_f32(&L.b2, d));
       SURGE_TRY(take_f32(&L.ln2_g, d));
       SURGE_TRY(take_f32(&L.ln2_b, d));
-      SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(gemm_bn_for(int(3 * d), int(d), EPI_BIAS))));
-      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(gemm_bn_for(int(d), int(d), EPI_BIAS_LN))));
-      SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(gemm_bn_for(int(f), int(d), EPI_BIAS_GELU))));
-      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(gemm_bn_for(int(d), int(f), EPI_BIAS_LN))));
+      SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(int(3 * d), int(d), EPI_BIAS)));
+      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(int(d), int(d), EPI_BIAS_LN)));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), EPI_BIAS_LN)));
     }
     return cudaSuccess;
   }();

@@ -1125,7 +1125,7 @@ surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float
   if (init_tma_encoder() != cudaSuccess) return SURGE_E_CUDA;
   CUtensorMap ta, tb;
   if (make_tmap_bf16(&ta, d_a, uint64_t(M), uint64_t(K), 128) != cudaSuccess) return SURGE_E_CUDA;
-  if (make_tmap_bf16(&tb, d_b, uint64_t(N), uint64_t(K), gemm_b_box_rows(BN)) != cudaSuccess) return SURGE_E_CUDA;
+  if (make_tmap_bf16(&tb, d_b, uint64_t(N), uint64_t(K), gemm_b_box_rows(N, K, epi)) != cudaSuccess) return SURGE_E_CUDA;
   CUtensorMap tc;
   if (make_tmap_store_bf16(&tc, d_c, uint64_t(M), uint64_t(N)) != cudaSuccess) return SURGE_E_CUDA;
   CUtensorMap tr;

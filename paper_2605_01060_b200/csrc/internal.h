@@ -43,12 +43,13 @@ cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes,
 cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_texts, int32_t tok0,
                             const uint16_t* word, const uint16_t* pos, const uint16_t* type, const float* gamma,
                             const float* beta, int d, float eps, uint16_t* x, cudaStream_t st);
-// K5: tensor-core tile kernel for texts of <= 64 tokens (+ per-(text, head) kernel when max_len > 64).
-// seg: int32[2 * ntok] scratch = per-token (first, end) of its text; seg_ready = already filled by
-// launch_seg for this chunk.  max_len bounds the longest text (sizes the K/V staging).
-cudaError_t launch_seg(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t* seg, cudaStream_t st);
+// K5: text-tiled tensor-core kernel for texts of <= 64 tokens (+ per-(text, head) kernel when
+// max_len > 64).  win: int32[ntok/64 + 2] scratch = first text starting in each 64-token window;
+// win_ready = already filled by launch_window_index for this chunk.
+cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t ntok, int32_t* win,
+                                cudaStream_t st);
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
-                             int32_t ntok, int32_t max_len, int32_t* seg, bool seg_ready, int heads, int head_dim,
+                             int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
                              uint16_t* out, cudaStream_t st);
 // K9
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
@@ -99,7 +100,7 @@ struct LayerW {
 struct Workspace {
   int64_t cap = 0;
   uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
-  int32_t* seg = nullptr;   // attention: per-token (first, end) of its text, 2 * cap entries
+  int32_t* win = nullptr;   // attention: first text of each 64-token window, cap/64 + 2 entries
   cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
   void release();
   ~Workspace() { release(); }

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(const uint16_
   const int d = heads * DH, ld = 3 * d;
   const int32_t start = cu[text] - tok0;
   const int32_t len = cu[text + 1] - cu[text];
-  if (len < min_len) return;   // short texts are handled by attention_tile_kernel
+  if (len < min_len) return;   // short texts are handled by attention_text_kernel
   constexpr int V8 = DH / 8;   // 16-byte vectors per head row
 
   for (int qb = 0; qb < len; qb += 32) {
@@ -287,14 +287,18 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(const uint16_
 }
 
 // ------------------------------------------------- K5 (texts <= 64 tokens): tensor-core tiles
-// seg[t] = (first, end) token of the text containing token t (chunk-local).  One warp per text.
-__global__ void seg_kernel(const int32_t* __restrict__ cu, int64_t n, int32_t tok0, int2* __restrict__ seg) {
-  const int64_t text = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (text >= n) return;
-  const int32_t a = cu[text] - tok0, b = cu[text + 1] - tok0;
-  const int2 v = make_int2(a, b);
-  for (int32_t t = a + lane; t < b; t += 32) seg[t] = v;
+// win[w] = min{ s : cu[s] - tok0 >= 64 w } for w in [0, nwin], nwin = ceil(ntok / 64) (win[nwin] = n):
+// the first text that starts in 64-token window w.  One thread per text boundary s in [0, n].
+__global__ void window_index_kernel(const int32_t* __restrict__ cu, int64_t n, int32_t tok0, int32_t ntok,
+                                    int32_t* __restrict__ win) {
+  const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s > n) return;
+  const int32_t nwin = (ntok + 63) >> 6;
+  const int32_t prev = (s == 0) ? -1 : cu[s - 1] - tok0;
+  const int32_t a = (s == n) ? ntok : cu[s] - tok0;
+  const int32_t w_lo = (prev < 0) ? 0 : (prev >> 6) + 1;
+  const int32_t w_hi = (s == n) ? nwin : (a >> 6);
+  for (int32_t w = w_lo; w <= w_hi; ++w) win[w] = int32_t(s);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -322,207 +326,182 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// Block-diagonal varlen attention for texts of <= ATT_SHORT tokens.  A CTA owns query rows
-// [r0, r0 + ROWS) and a group of HG heads; it stages those Q rows and the K/V rows of every text
-// that intersects them ([k0, k1), at most ROWS + 2 (L - 1) rows) in padded shared memory with
-// cp.async, then each warp computes 16 query rows: S = Q K^T and O = P V on mma.sync m16n8k16
-// (bf16 in, fp32 accumulate; P split hi+lo bf16), 16-key blocks aligned to text starts over the warp's texts only, with the text mask
-// (key j valid for query i iff j lies in i's text), flash-style online softmax in exp2 form.
-// O is staged back into the Q tile and written with 16-byte stores.  Rows of longer texts are
-// left to attention_kernel.
+// Block-diagonal varlen attention for texts of <= ATT_SHORT tokens, text-tiled.  A CTA owns the
+// texts that START in one 64-token window (their rows [R0, R1) span at most 64 + 63 tokens, so
+// no halo is loaded) and a group of HG heads; Q/K/V of those rows are staged in padded shared
+// memory with cp.async.  Each warp takes whole texts: per (text, head), query tiles of 16 rows
+// and key blocks of 16 keys, both aligned to the text's first token, on mma.sync m16n8k16 (bf16
+// in, fp32 accumulate; P split hi+lo bf16), keys masked to j < len, flash-style online softmax in
+// exp2 form.  Every text's arithmetic is therefore identical wherever it sits in the stream
+// (bit-exact SuperBatch invariance).  O is written over the text's own Q rows and stored with
+// 16-byte coalesced stores.  A text longer than ATT_SHORT is left to attention_kernel.
 constexpr int ATT_SHORT = 64;
 
 template <int DH, int HG>
-struct TileAtt {
-  static constexpr int ROWS = 64;                // query rows per CTA
-  static constexpr int WARPS = ROWS / 16;
+struct TextAtt {
+  static constexpr int WIN = 64;                 // window of text starts per CTA
+  static constexpr int WARPS = 4;
   static constexpr int COLS = HG * DH;           // columns of one Q / K / V slice
   static constexpr int LDS = COLS + 8;           // smem row stride (bf16): 16-byte skew per row
   static constexpr int CH = COLS / 8;            // 16-byte chunks per row
-  static int kcap(int max_len) {                 // K/V rows staged (+16 zero rows for the last step)
+  // rows staged: texts starting in the window end within WIN + L - 1 rows (L = longest short
+  // text), + 16 zero rows read by the last tile
+  static int rows(int max_len) {
     const int L = max_len < ATT_SHORT ? (max_len < 1 ? 1 : max_len) : ATT_SHORT;
-    return ((ROWS + 2 * (L - 1) + 16 + 7) / 8) * 8;
+    return WIN + L - 1 + 16;
   }
-  static size_t smem(int max_len) { return size_t(ROWS + 2 * kcap(max_len)) * LDS * 2; }
+  static size_t smem(int max_len) { return size_t(3) * rows(max_len) * LDS * 2; }
 };
 
 template <int DH, int HG>
-__global__ void __launch_bounds__(TileAtt<DH, HG>::WARPS * 32) attention_tile_kernel(
-    const uint16_t* __restrict__ qkv, const int2* __restrict__ seg, int32_t ntok, int heads,
-    uint16_t* __restrict__ out, float qscale, int kcap) {
-  using A = TileAtt<DH, HG>;
-  constexpr int ROWS = A::ROWS, LDS = A::LDS, CH = A::CH;
+__global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_kernel(
+    const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu, int32_t tok0, int32_t ntok,
+    const int32_t* __restrict__ win, int heads, uint16_t* __restrict__ out, float qscale, int ROWS) {
+  using A = TextAtt<DH, HG>;
+  constexpr int LDS = A::LDS, CH = A::CH;
   extern __shared__ __align__(16) uint16_t att_sm[];
   uint16_t* sQ = att_sm;                         // [ROWS][LDS]  (Q, then O)
-  uint16_t* sK = sQ + ROWS * LDS;                // [kcap][LDS]
-  uint16_t* sV = sK + kcap * LDS;                // [kcap][LDS]
+  uint16_t* sK = sQ + ROWS * LDS;
+  uint16_t* sV = sK + ROWS * LDS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int d = heads * DH, ld = 3 * d;
-  const int32_t r0 = blockIdx.x * ROWS;
   const int col0 = blockIdx.y * A::COLS;
-  const int32_t r_end = min(r0 + ROWS, ntok);    // query rows [r0, r_end)
-  const int2 sa = seg[r0], sb = seg[r_end - 1];
-  const int32_t k0 = (sa.y - sa.x <= ATT_SHORT) ? sa.x : r0;
-  const int32_t k1 = (sb.y - sb.x <= ATT_SHORT) ? sb.y : r_end;
-  const int nq = r_end - r0, nk = k1 - k0;
-
-  for (int i = tid; i < nq * CH; i += blockDim.x) {
+  const int32_t s_a = win[blockIdx.x];
+  int32_t s_b = win[blockIdx.x + 1];             // texts [s_a, s_b) start in this window
+  if (s_b <= s_a) return;
+  const int32_t R0 = cu[s_a] - tok0;
+  // a text longer than ATT_SHORT can only be the window's last text (it ends past the next window)
+  if (cu[s_b] - cu[s_b - 1] > ATT_SHORT) --s_b;
+  const int32_t R1 = cu[s_b] - tok0;
+  const int nr = R1 - R0;                        // <= WIN + ATT_SHORT - 1
+  for (int i = tid; i < nr * CH; i += blockDim.x) {
     const int r = i / CH, c = i - r * CH;
-    cp_async16(sQ + r * LDS + c * 8, qkv + size_t(r0 + r) * ld + col0 + c * 8);
-  }
-  for (int i = tid; i < nk * CH; i += blockDim.x) {
-    const int r = i / CH, c = i - r * CH;
-    const uint16_t* g = qkv + size_t(k0 + r) * ld + col0 + c * 8;
+    const uint16_t* g = qkv + size_t(R0 + r) * ld + col0 + c * 8;
+    cp_async16(sQ + r * LDS + c * 8, g);
     cp_async16(sK + r * LDS + c * 8, g + d);
     cp_async16(sV + r * LDS + c * 8, g + 2 * d);
   }
   const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 16 * CH; i += blockDim.x) {   // zero rows after the span (masked, must be finite)
-    const int r = nk + i / CH, c = i % CH;
+  for (int i = tid; i < 16 * CH; i += blockDim.x) {   // tiles may read 15 rows past the last text
+    const int r = nr + i / CH, c = i % CH;
+    *reinterpret_cast<uint4*>(sQ + r * LDS + c * 8) = z;
     *reinterpret_cast<uint4*>(sK + r * LDS + c * 8) = z;
     *reinterpret_cast<uint4*>(sV + r * LDS + c * 8) = z;
   }
-  for (int i = tid; i < (ROWS - nq) * CH; i += blockDim.x) {
-    const int r = nq + i / CH, c = i % CH;
-    *reinterpret_cast<uint4*>(sQ + r * LDS + c * 8) = z;
-  }
-  cp_async_wait_all();
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
   const int g = lane >> 2, c4 = lane & 3;
-  const int32_t qr = r0 + warp * 16;             // first query row of this warp
-  const int32_t ra = qr + g, rb = qr + g + 8;
-  int2 ta = make_int2(0, 0), tb = make_int2(0, 0);
-  if (ra < r_end) ta = seg[ra];
-  if (rb < r_end) tb = seg[rb];
-  const bool va = ra < r_end && ta.y - ta.x <= ATT_SHORT;
-  const bool vb = rb < r_end && tb.y - tb.x <= ATT_SHORT;
-  if (!va) ta = make_int2(-1, -1);   // never matches a text start: the row takes no keys
-  if (!vb) tb = make_int2(-1, -1);
-  int32_t kw0 = min(va ? ta.x : INT_MAX, vb ? tb.x : INT_MAX);
-  int32_t kw1 = max(va ? ta.y : INT_MIN, vb ? tb.y : INT_MIN);
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    kw0 = min(kw0, __shfl_xor_sync(0xffffffffu, kw0, o));
-    kw1 = max(kw1, __shfl_xor_sync(0xffffffffu, kw1, o));
-  }
-  if (kw0 < kw1) {
-    const uint32_t q_base = smem_u32(sQ + (warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
+  // work units (text, head), round-robin over the warps
 #pragma unroll 1
-    for (int h = 0; h < HG; ++h) {
-      uint32_t qa[DH / 16][4];
-#pragma unroll
-      for (int kk = 0; kk < DH / 16; ++kk)
-        ldsm_x4(q_base + (h * DH + kk * 16) * 2, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
-      float o[DH / 8][4];
-#pragma unroll
-      for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-      float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
-      // Key blocks are aligned to each text's first token and visited text by text, so every
-      // query row sees exactly the same 16-key blocks (other texts' blocks contribute exact zeros
-      // and unit rescales) wherever its text sits in the stream: bit-exact SuperBatch invariance.
-      int32_t t_beg = kw0, t_end = kw0, kb = kw0;
+  for (int32_t u = warp; u < (s_b - s_a) * HG; u += A::WARPS) {
+    const int32_t txt = s_a + u / HG;
+    const int h = u % HG;
+    const int32_t ta = cu[txt] - tok0 - R0;      // smem row of the text's first token
+    const int32_t len = cu[txt + 1] - cu[txt];
+    const int nt = (len + 15) >> 4;              // query tiles = key blocks
+    {
 #pragma unroll 1
-      for (;;) {
-        if (kb >= t_end) {                         // next text
-          if (t_end >= kw1) break;
-          const int2 tx = seg[t_end];
-          t_beg = tx.x;
-          t_end = tx.y;
-          kb = t_beg;
-          if (t_end - t_beg > ATT_SHORT) {         // long text: its rows belong to attention_kernel
-            kb = t_end;
-            continue;
+      for (int qt = 0; qt < nt; ++qt) {
+        const int q0 = ta + 16 * qt;
+        uint32_t qa[DH / 16][4];
+        const uint32_t q_addr =
+            smem_u32(sQ + (q0 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + h * DH + (lane >> 4) * 8);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) ldsm_x4(q_addr + kk * 32, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+        float o[DH / 8][4];
+#pragma unroll
+        for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+        float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
+#pragma unroll 1
+        for (int kb = 0; kb < nt; ++kb) {
+          const int k0 = ta + 16 * kb;
+          float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+          const uint32_t k_addr =
+              smem_u32(sK + (k0 + (lane & 7) + ((lane >> 4) & 1) * 8) * LDS + h * DH + ((lane >> 3) & 1) * 8);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            uint32_t b00, b01, b10, b11;
+            ldsm_x4(k_addr + kk * 32, b00, b01, b10, b11);
+            mma_bf16_16816(s0, qa[kk], b00, b01);
+            mma_bf16_16816(s1, qa[kk], b10, b11);
+          }
+          // key index within the text: 16 kb + 2 c4 + {0, 1} (s0), + 8 (s1); valid iff < len
+          const int j0 = 16 * kb + 2 * c4;
+          const bool v0 = j0 < len, v1 = j0 + 1 < len, v2 = j0 + 8 < len, v3 = j0 + 9 < len;
+          float pa[4], pb[4];
+          pa[0] = v0 ? s0[0] * qscale : -INFINITY;
+          pa[1] = v1 ? s0[1] * qscale : -INFINITY;
+          pa[2] = v2 ? s1[0] * qscale : -INFINITY;
+          pa[3] = v3 ? s1[1] * qscale : -INFINITY;
+          pb[0] = v0 ? s0[2] * qscale : -INFINITY;
+          pb[1] = v1 ? s0[3] * qscale : -INFINITY;
+          pb[2] = v2 ? s1[2] * qscale : -INFINITY;
+          pb[3] = v3 ? s1[3] * qscale : -INFINITY;
+          float xa = fmaxf(fmaxf(pa[0], pa[1]), fmaxf(pa[2], pa[3]));
+          float xb = fmaxf(fmaxf(pb[0], pb[1]), fmaxf(pb[2], pb[3]));
+          xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
+          xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
+          xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
+          xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
+          const float na = fmaxf(ma, xa), nb = fmaxf(mb, xb);   // finite: key 0 of block 0 is valid
+          const float ca = exp2f(ma - na), cb = exp2f(mb - nb);
+          ma = na;
+          mb = nb;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            pa[i] = exp2f(pa[i] - na);
+            pb[i] = exp2f(pb[i] - nb);
+          }
+          la = la * ca + (pa[0] + pa[1] + pa[2] + pa[3]);
+          lb = lb * cb + (pb[0] + pb[1] + pb[2] + pb[3]);
+          if (kb > 0) {
+#pragma unroll
+            for (int n = 0; n < DH / 8; ++n) {
+              o[n][0] *= ca; o[n][1] *= ca;
+              o[n][2] *= cb; o[n][3] *= cb;
+            }
+          }
+          // P = P_hi + P_lo, both bf16 (two MMAs): P V keeps ~16 mantissa bits of P
+          const uint32_t pf[4] = {pack_bf16x2(pa[0], pa[1]), pack_bf16x2(pb[0], pb[1]), pack_bf16x2(pa[2], pa[3]),
+                                  pack_bf16x2(pb[2], pb[3])};
+          const uint32_t pl[4] = {pack_bf16x2(pa[0] - bf16lo(pf[0]), pa[1] - bf16hi(pf[0])),
+                                  pack_bf16x2(pb[0] - bf16lo(pf[1]), pb[1] - bf16hi(pf[1])),
+                                  pack_bf16x2(pa[2] - bf16lo(pf[2]), pa[3] - bf16hi(pf[2])),
+                                  pack_bf16x2(pb[2] - bf16lo(pf[3]), pb[3] - bf16hi(pf[3]))};
+          const uint32_t v_addr =
+              smem_u32(sV + (k0 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + h * DH + (lane >> 4) * 8);
+#pragma unroll
+          for (int n = 0; n < DH / 16; ++n) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(v_addr + n * 32, b0, b1, b2, b3);
+            mma_bf16_16816(o[2 * n], pf, b0, b1);
+            mma_bf16_16816(o[2 * n + 1], pf, b2, b3);
+            mma_bf16_16816(o[2 * n], pl, b0, b1);
+            mma_bf16_16816(o[2 * n + 1], pl, b2, b3);
           }
         }
-        const int kr = kb - k0;                    // smem row of key kb
-        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t k_addr =
-            smem_u32(sK + (kr + (lane & 7) + ((lane >> 4) & 1) * 8) * LDS + h * DH + ((lane >> 3) & 1) * 8);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          uint32_t b00, b01, b10, b11;
-          ldsm_x4(k_addr + kk * 32, b00, b01, b10, b11);
-          mma_bf16_16816(s0, qa[kk], b00, b01);
-          mma_bf16_16816(s1, qa[kk], b10, b11);
-        }
-        // scale + text mask: only rows of the current text [t_beg, t_end) take keys from this block
-        // (keys kb + 2c4 + {0,1} in s0, kb + 8 + 2c4 + {0,1} in s1; all >= t_beg by construction)
-        const int32_t j0 = kb + 2 * c4, j1 = j0 + 1, j2 = j0 + 8, j3 = j0 + 9;
-        const int32_t ea = (ta.x == t_beg) ? t_end : INT_MIN, eb = (tb.x == t_beg) ? t_end : INT_MIN;
-        float pa[4], pb[4];
-        pa[0] = j0 < ea ? s0[0] * qscale : -INFINITY;
-        pa[1] = j1 < ea ? s0[1] * qscale : -INFINITY;
-        pa[2] = j2 < ea ? s1[0] * qscale : -INFINITY;
-        pa[3] = j3 < ea ? s1[1] * qscale : -INFINITY;
-        pb[0] = j0 < eb ? s0[2] * qscale : -INFINITY;
-        pb[1] = j1 < eb ? s0[3] * qscale : -INFINITY;
-        pb[2] = j2 < eb ? s1[2] * qscale : -INFINITY;
-        pb[3] = j3 < eb ? s1[3] * qscale : -INFINITY;
-        float xa = fmaxf(fmaxf(pa[0], pa[1]), fmaxf(pa[2], pa[3]));
-        float xb = fmaxf(fmaxf(pb[0], pb[1]), fmaxf(pb[2], pb[3]));
-        xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
-        xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
-        xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
-        xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
-        const float na = fmaxf(ma, xa), nb = fmaxf(mb, xb);
-        const float ua = (na == -INFINITY) ? 0.f : na, ub = (nb == -INFINITY) ? 0.f : nb;
-        const float ca = exp2f(ma - ua), cb = exp2f(mb - ub);
-        ma = na;
-        mb = nb;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          pa[i] = exp2f(pa[i] - ua);
-          pb[i] = exp2f(pb[i] - ub);
-        }
-        la = la * ca + (pa[0] + pa[1] + pa[2] + pa[3]);
-        lb = lb * cb + (pb[0] + pb[1] + pb[2] + pb[3]);
+        la += __shfl_xor_sync(0xffffffffu, la, 1);
+        la += __shfl_xor_sync(0xffffffffu, la, 2);
+        lb += __shfl_xor_sync(0xffffffffu, lb, 1);
+        lb += __shfl_xor_sync(0xffffffffu, lb, 2);
+        const float ia = 1.0f / la, ib = 1.0f / lb;
+        __syncwarp();   // every lane has read its Q fragments before O overwrites the tile
+        const int ra = 16 * qt + g, rb = ra + 8;  // rows within the text
+        uint16_t* oa = sQ + (q0 + g) * LDS + h * DH + 2 * c4;
 #pragma unroll
         for (int n = 0; n < DH / 8; ++n) {
-          o[n][0] *= ca; o[n][1] *= ca;
-          o[n][2] *= cb; o[n][3] *= cb;
+          if (ra < len) *reinterpret_cast<uint32_t*>(oa + n * 8) = pack_bf16x2(o[n][0] * ia, o[n][1] * ia);
+          if (rb < len) *reinterpret_cast<uint32_t*>(oa + 8 * LDS + n * 8) = pack_bf16x2(o[n][2] * ib, o[n][3] * ib);
         }
-        // P = P_hi + P_lo, both bf16 (two MMAs): P·V keeps ~16 mantissa bits of P
-        const uint32_t pf[4] = {pack_bf16x2(pa[0], pa[1]), pack_bf16x2(pb[0], pb[1]), pack_bf16x2(pa[2], pa[3]),
-                                pack_bf16x2(pb[2], pb[3])};
-        const uint32_t pl[4] = {pack_bf16x2(pa[0] - bf16lo(pf[0]), pa[1] - bf16hi(pf[0])),
-                                pack_bf16x2(pb[0] - bf16lo(pf[1]), pb[1] - bf16hi(pf[1])),
-                                pack_bf16x2(pa[2] - bf16lo(pf[2]), pa[3] - bf16hi(pf[2])),
-                                pack_bf16x2(pb[2] - bf16lo(pf[3]), pb[3] - bf16hi(pf[3]))};
-        const uint32_t v_addr =
-            smem_u32(sV + (kr + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + h * DH + (lane >> 4) * 8);
-#pragma unroll
-        for (int n = 0; n < DH / 16; ++n) {
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(v_addr + n * 32, b0, b1, b2, b3);
-          mma_bf16_16816(o[2 * n], pf, b0, b1);
-          mma_bf16_16816(o[2 * n + 1], pf, b2, b3);
-          mma_bf16_16816(o[2 * n], pl, b0, b1);
-          mma_bf16_16816(o[2 * n + 1], pl, b2, b3);
-        }
-        kb += 16;
-      }
-      la += __shfl_xor_sync(0xffffffffu, la, 1);
-      la += __shfl_xor_sync(0xffffffffu, la, 2);
-      lb += __shfl_xor_sync(0xffffffffu, lb, 1);
-      lb += __shfl_xor_sync(0xffffffffu, lb, 2);
-      const float ia = la > 0.f ? 1.0f / la : 0.f, ib = lb > 0.f ? 1.0f / lb : 0.f;
-      __syncwarp();   // every lane has read its Q fragments of head h before they are overwritten
-      uint16_t* oa = sQ + (warp * 16 + g) * LDS + h * DH + 2 * c4;
-#pragma unroll
-      for (int n = 0; n < DH / 8; ++n) {
-        *reinterpret_cast<uint32_t*>(oa + n * 8) = pack_bf16x2(o[n][0] * ia, o[n][1] * ia);
-        *reinterpret_cast<uint32_t*>(oa + 8 * LDS + n * 8) = pack_bf16x2(o[n][2] * ib, o[n][3] * ib);
       }
     }
   }
   __syncthreads();
-  for (int i = tid; i < nq * CH; i += blockDim.x) {
+  for (int i = tid; i < nr * CH; i += blockDim.x) {
     const int r = i / CH, c = i - r * CH;
-    const int2 t = seg[r0 + r];
-    if (t.y - t.x <= ATT_SHORT)
-      *reinterpret_cast<uint4*>(out + size_t(r0 + r) * d + col0 + c * 8) =
-          *reinterpret_cast<const uint4*>(sQ + r * LDS + c * 8);
+    *reinterpret_cast<uint4*>(out + size_t(R0 + r) * d + col0 + c * 8) =
+        *reinterpret_cast<const uint4*>(sQ + r * LDS + c * 8);
   }
 }
 
@@ -617,26 +596,26 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_tex
 }
 
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
-                             int32_t ntok, int32_t max_len, int32_t* seg, bool seg_ready, int heads, int head_dim,
+                             int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
                              uint16_t* out, cudaStream_t st) {
   if (n_texts <= 0 || ntok <= 0) return cudaSuccess;
   if (heads % 2) return cudaErrorInvalidValue;
   const float qscale = 1.4426950408889634f / sqrtf(float(head_dim));
-  int2* sg = reinterpret_cast<int2*>(seg);
-  if (!seg_ready) seg_kernel<<<blocks_for_warps(n_texts, 8), 256, 0, st>>>(cu, n_texts, tok0, sg);
+  const int32_t nwin = (ntok + 63) >> 6;
+  if (!win_ready)
+    window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
 #define SURGE_ATT(DH)                                                                                        \
   case DH: {                                                                                                 \
-    using TA = TileAtt<DH, 2>;                                                                               \
-    static int attr_##DH = 0;                                                                                \
-    const size_t sm = TA::smem(max_len);                                                                     \
-    if (attr_##DH < int(sm)) {                                                                               \
-      cudaFuncSetAttribute(attention_tile_kernel<DH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+    using TA = TextAtt<DH, 2>;                                                                               \
+    static bool attr_##DH = false;                                                                           \
+    if (!attr_##DH) {                                                                                        \
+      cudaFuncSetAttribute(attention_text_kernel<DH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                            int(TA::smem(ATT_SHORT)));                                                        \
-      attr_##DH = int(TA::smem(ATT_SHORT));                                                                  \
+      attr_##DH = true;                                                                                      \
     }                                                                                                        \
-    const dim3 grid(unsigned((ntok + TA::ROWS - 1) / TA::ROWS), unsigned(heads / 2));                        \
-    attention_tile_kernel<DH, 2><<<grid, TA::WARPS * 32, sm, st>>>(qkv, sg, ntok, heads, out, qscale,        \
-                                                                   TA::kcap(max_len));                       \
+    const dim3 grid(unsigned(nwin), unsigned(heads / 2));                                                    \
+    attention_text_kernel<DH, 2><<<grid, TA::WARPS * 32, TA::smem(max_len), st>>>(                           \
+        qkv, cu, tok0, ntok, win, heads, out, qscale, TA::rows(max_len));                                    \
     if (max_len > ATT_SHORT) {                                                                               \
       constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \
       attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W1), W1 * 32, 0, st>>>(                       \
@@ -653,9 +632,10 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_seg(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t* seg, cudaStream_t st) {
+cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0, int32_t ntok, int32_t* win,
+                                cudaStream_t st) {
   if (n_texts <= 0) return cudaSuccess;
-  seg_kernel<<<blocks_for_warps(n_texts, 8), 256, 0, st>>>(cu, n_texts, tok0, reinterpret_cast<int2*>(seg));
+  window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
   return cudaGetLastError();
 }
 

@@ -26,7 +26,7 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   if ((e = cudaMalloc(&O, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&X1, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&H, t * s.ffn * 2)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&seg, (2 * t + 2) * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&win, (t / 64 + 2) * sizeof(int32_t))) != cudaSuccess) return e;
   cap = cap_tokens;
   return cudaSuccess;
 }
@@ -36,8 +36,8 @@ void Workspace::release() {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
-  if (seg) cudaFree(seg);
-  seg = nullptr;
+  if (win) cudaFree(win);
+  win = nullptr;
   cap = 0;
 }
 
@@ -215,7 +215,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   int64_t k = 0;
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_embed_ln(d_ids, cu, n, tok0, word_, pos_, type_, emb_g_, emb_b_, d, s_.eps, ws.X, st));
-  SURGE_TRY(launch_seg(cu, n, tok0, ws.seg, st));
+  SURGE_TRY(launch_window_index(cu, n, tok0, ntok, ws.win, st));
   if (P) prof->end(KK_EMBED, st, ev, 0.0, M * (4 + 2 * D + 2 * D + 2 * D));
   k += 2;
   for (const LayerW& L : layers_) {
@@ -229,7 +229,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
     // K5: O = attention(QKV) per text
     if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.seg, true, s_.heads, d / s_.heads, ws.O, st));
+    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st));
     if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
     // K6: X1 = LN(O Wo^T + bo + X)
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;

@@ -1149,12 +1149,12 @@ surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int6
   int32_t max_len = 0;
   for (int64_t i = 0; i < n_texts; ++i) max_len = std::max(max_len, hcu[i + 1] - hcu[i]);
   const int32_t ntok = hcu[n_texts] - hcu[0];
-  int32_t* seg = nullptr;
-  if (cudaMalloc(&seg, (2 * size_t(ntok) + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
-  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, seg, false, heads,
+  int32_t* win = nullptr;
+  if (cudaMalloc(&win, (size_t(ntok) / 64 + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
+  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, win, false, heads,
                                           head_dim, d_out, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
-  cudaFree(seg);
+  cudaFree(win);
   return (e == cudaSuccess && e2 == cudaSuccess) ? SURGE_OK : SURGE_E_CUDA;
 }
 

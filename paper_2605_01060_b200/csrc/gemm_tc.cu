@@ -55,7 +55,7 @@ struct TileCfg {
   static_assert(B_BOX * N_LOADS * (PAIR ? 2 : 1) == BN, "B box split");
   static_assert(HALF % 32 == 0, "epilogue column split");
   // Weight-stationary (ws): the CTA's whole B slice [BN x K] stays resident; only A streams.
-  __host__ __device__ static int b_res_bytes(int K, bool ws) { return ws ? BN * K * 2 : 0; }
+  __host__ __device__ static int b_res_bytes(int K, bool ws) { return ws ? (PAIR ? BN / 2 : BN) * K * 2 : 0; }
   __host__ __device__ static int stage_bytes(bool ws) { return A_STAGE_BYTES + (ws ? 0 : B_STAGE_BYTES); }
   __host__ __device__ static int stages(int K, bool ws) {
     const int n = (MAX_SMEM - FIXED_BYTES - b_res_bytes(K, ws)) / stage_bytes(ws);
@@ -115,7 +115,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                    float eps, int stages) {
   using T = TileCfg<BN, EPI, PAIR>;
   constexpr int ACC = T::ACC;
-  static_assert(!(WS && PAIR), "pairs run streaming tiles only");
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the __shared__ array (an integer round trip would turn every
   // shared access into a generic one)
@@ -183,12 +182,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if constexpr (WS) {
         if (p == 0 && sc.t0 < sc.tend) {
           const int n0 = sc.slice * BN;
-          mbar_arrive_expect_tx(bfull, uint32_t(BN) * K * 2);
-          for (int kb = 0; kb < num_kb; ++kb)
+          if constexpr (PAIR) {                   // each CTA loads its half; bytes land on the leader
+            if (leader) mbar_arrive_expect_tx(bfull, uint32_t(BN) * K * 2);
+            const uint32_t bar = mapa_shared(smem_u32(bfull), 0);
+            for (int kb = 0; kb < num_kb; ++kb)
 #pragma unroll
-            for (int j = 0; j < T::N_LOADS; ++j)
-              tma_load_2d_hint(sB + kb * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, bfull, kb * BK,
-                               n0 + j * T::B_BOX, pol_w);
+              for (int j = 0; j < T::N_LOADS; ++j)
+                tma_load_2d_pair(sB + kb * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, bar, kb * BK,
+                                 n0 + j * T::MMA_N + sc.rank * T::B_BOX, pol_w);
+          } else {
+            mbar_arrive_expect_tx(bfull, uint32_t(BN) * K * 2);
+            for (int kb = 0; kb < num_kb; ++kb)
+#pragma unroll
+              for (int j = 0; j < T::N_LOADS; ++j)
+                tma_load_2d_hint(sB + kb * T::B_STAGE_BYTES + j * T::B_BOX * 128, &tmB, bfull, kb * BK,
+                                 n0 + j * T::B_BOX, pol_w);
+          }
         }
       }
       uint32_t c = 0;
@@ -481,7 +490,11 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   }
   const int64_t m_tiles = (g.M + BM - 1) / BM, n_tiles = g.N / BN;
   int grid;
-  if (WS) {
+  if (WS && PAIR) {
+    const int64_t m2 = (g.M + 2 * BM - 1) / (2 * BM);
+    const int64_t per = std::min<int64_t>(std::max<int64_t>(num_sms() / 2 / n_tiles, 1), m2);
+    grid = int(2 * per * n_tiles);
+  } else if (WS) {
     const int64_t per = std::min<int64_t>(std::max<int64_t>(num_sms() / n_tiles, 1), m_tiles);
     grid = int(per * n_tiles);
   } else if (PAIR) {
@@ -514,18 +527,24 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
 
 // Weight-stationary when the B slice fits next to >= 4 A stages and there are enough M tiles to
 // give every slice's CTAs work.
-template <int BN, int EPI>
+template <int BN, int EPI, bool PAIR = false>
 bool use_ws(const GemmArgs& g) {
-  using T = TileCfg<BN, EPI>;
-  return g.epi != EPI_BIAS_LN && T::stages(g.K, true) >= 3 && (g.M + BM - 1) / BM >= num_sms() / (g.N / BN);
+  using T = TileCfg<BN, EPI, PAIR>;
+  const int64_t m_units = PAIR ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM - 1) / BM;
+  const int units = PAIR ? num_sms() / 2 : num_sms();
+  return g.epi != EPI_BIAS_LN && T::stages(g.K, true) >= 3 && m_units >= units / (g.N / BN);
 }
 
 template <int BN, int EPI>
 cudaError_t launch_gemm_bn(const GemmArgs& g, cudaStream_t st) {
+  if (gemm_use_pair(g.N, g.K, g.epi)) {
+    if constexpr (EPI != EPI_BIAS_LN && BN == 384) {
+      if (use_ws<BN, EPI, true>(g)) return launch_gemm_t<BN, EPI, true, true>(g, st);
+    }
+    return launch_gemm_t<BN, EPI, false, true>(g, st);
+  }
   if constexpr (EPI != EPI_BIAS_LN) {
     if (use_ws<BN, EPI>(g)) return launch_gemm_t<BN, EPI, true>(g, st);
-  } else {
-    if (gemm_use_pair(g.N, g.K, g.epi)) return launch_gemm_t<BN, EPI, false, true>(g, st);
   }
   return launch_gemm_t<BN, EPI, false>(g, st);
 }
@@ -575,10 +594,18 @@ cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t row
 }
 
 // LN GEMMs (full-row tiles, single TMEM accumulator) run as CTA pairs: half the B bytes per CTA.
-bool gemm_use_pair(int N, int K, int epi) { return epi == EPI_BIAS_LN && N == 384 && K % 64 == 0; }
+// Weight-stationary pairs for bias-only GEMMs (each CTA keeps half of a [384 x K] slice resident,
+// twice the MMA work per A byte of a 192-column slice) are implemented (WS && PAIR) but not
+// selected: with a single 384-column TMEM accumulator the epilogue serialises with the mainloop
+// and measured slower than 192-column single-CTA slices (QKV 109 vs 84 ms per 1M texts).
+bool gemm_use_pair(int N, int K, int epi) {
+  if (K % 64 != 0) return false;
+  return epi == EPI_BIAS_LN && N == 384;
+}
 
 int gemm_bn_for(int N, int K, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
+  if (gemm_use_pair(N, K, epi)) return 384;
   // 192-column slices whose [192 x K] weight block can stay resident (weight-stationary) win over
   // streaming 256-column tiles: A is re-read N/192 times from L2 but B is read once per CTA.
   if (N % 192 == 0 && TileCfg<192, EPI_BIAS>::stages(K, true) >= 3) return 192;

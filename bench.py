@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-texts", type=int, default=256, help="--impl reference: texts encoded per step")
     ap.add_argument("--profile-run", action="store_true",
                     help="for ncu: one SuperBatch, no e2e/baseline/JSON timing")
     return ap.parse_args()
@@ -154,7 +155,7 @@ def run_reference(args, world, rank):
     from oracle import aggregator as oagg
     from oracle import encoder as oenc
     E = oenc.Encoder(ecfg, w)
-    per_step = 256
+    per_step = args.ref_texts
     times = []
     with threadpool_limits(limits=1):
         off_t = 0
@@ -214,15 +215,15 @@ def main():
     w = make_weights(ecfg, seed=1234) if rank == 0 or world == 1 else None
     n_w = sum(int(np.prod(s)) for s in [v.shape for v in (w or make_weights_shapes(ecfg)).values()])
     if rank == 0 or world == 1:
-        blob_dev = torch.from_numpy(pack_blob(ecfg, w).view(np.int16)).to(dev)
+        blob_dev = torch.from_numpy(pack_blob(ecfg, w).view(np.uint8)).to(dev)
     else:
-        blob_dev = torch.empty(n_w, dtype=torch.int16, device=dev)
+        blob_dev = torch.empty(2 * n_w, dtype=torch.uint8, device=dev)
     if world > 1:
         import torch.distributed as dist
-        dist.broadcast(blob_dev, src=0)
+        dist.broadcast(blob_dev, src=0)     # bf16 bits as bytes (NCCL has no int16 type)
     cfg = N.make_config(ecfg, wcfg.b_min, wcfg.b_max, rank=rank, world_size=world, device=local,
                         chunk_tokens=args.chunk_tokens, weights_on_device=1)
-    h = N.surge_create(cfg, blob_dev, n_weights=blob_dev.numel())
+    h = N.surge_create(cfg, blob_dev, n_weights=blob_dev.numel() // 2)
     stream = torch.cuda.Stream(device=dev)
 
     sizes = wl.sizes.astype(np.int64)

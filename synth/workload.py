@@ -58,7 +58,18 @@ def partition_sizes(cfg: WorkloadConfig, rng: np.random.Generator) -> np.ndarray
     z = rng.standard_normal(P)
     r = np.exp(cfg.mu + cfg.sigma * z)
     n = np.maximum(1, np.rint(r * (N / r.sum()))).astype(np.int64)
-    n[int(np.argmax(n))] += N - int(n.sum())
+    res = N - int(n.sum())
+    if res >= 0 or n[int(np.argmax(n))] + res >= 1:
+        n[int(np.argmax(n))] += res
+    else:   # degenerate N ~ P: take the excess from the largest partitions, keeping every n_k >= 1
+        if N < len(n):
+            raise ValueError("need n_texts >= n_partitions")
+        for k in np.argsort(-n, kind="stable"):
+            take = min(int(n[k]) - 1, -res)
+            n[k] -= take
+            res += take
+            if res == 0:
+                break
     if cfg.order == "ascending":
         n = np.sort(n, kind="stable")
     return n

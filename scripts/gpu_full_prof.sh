@@ -5,7 +5,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 1200 python bench.py > gpurun_out/bench_full.log 2>&1; tail -1 gpurun_out/bench_full.log | cut -c1-300
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile-run --n-texts 1000000 > gpurun_out/ncu_launch.log 2>&1; tail -2 gpurun_out/ncu_launch.log
-for spec in "attention_tile:attn:12" "gemm_tc_kernel<.int.192, .int.1, .bool.1>:ffn1:12" "gemm_tc_kernel<.int.384, .int.2, .bool.0>:ln:24" "gemm_tc_kernel<.int.192, .int.0, .bool.1>:qkv:12"; do
+for spec in "attention_text:attn:12" "gemm_tc_kernel<.int.192, .int.1, .bool.1:ffn1:12" "gemm_tc_kernel<.int.384, .int.2:ln:24" "gemm_tc_kernel<.int.384, .int.2:ffn2:25" "gemm_tc_kernel<.int.192, .int.0, .bool.1:qkv:12"; do
   IFS=: read -r rx tag skip <<< "$spec"
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$rx" -s $skip -c 1 \
      -o gpurun_out/prof_$tag python bench.py --profile-run --n-texts 1000000 > gpurun_out/ncu_$tag.log 2>&1

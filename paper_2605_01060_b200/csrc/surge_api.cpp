@@ -568,7 +568,7 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
   c->cfg = k;
   c->shape = s;
   c->device = k.device;
-  if (c->cfg.chunk_tokens <= 0) c->cfg.chunk_tokens = 131072;
+  if (c->cfg.chunk_tokens <= 0) c->cfg.chunk_tokens = 262144;
   c->cfg.chunk_tokens = std::max(c->cfg.chunk_tokens, k.max_position);
   if (c->cfg.max_inflight <= 0) c->cfg.max_inflight = 2;
   c->st.ttfo_s = -1.0;

@@ -24,6 +24,7 @@ BUILD = os.path.join(PKG, "_build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-Wall,-Wno-unused-function",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+FLAGS += os.environ.get("NVCC_EXTRA", "").split()   # tuning experiments (scripts/gpu_*_sweep.sh)
 
 
 def nvcc() -> str:

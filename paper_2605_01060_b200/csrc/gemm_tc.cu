@@ -24,8 +24,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;                       // 64 bf16 = 128 B = one swizzle row
 constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
-constexpr int NUM_EPI_WARPS = 8;             // 2 per TMEM lane quadrant, splitting the columns
-constexpr int GEMM_THREADS = 128 + NUM_EPI_WARPS * 32;
 
 // PAIR: a cluster of two CTAs runs cta_group::2 MMAs on 256 x BN tiles; each CTA holds its 128
 // rows of A and of the accumulator, and half of every MMA's N rows of B (so B traffic per CTA
@@ -42,26 +40,36 @@ struct TileCfg {
   static constexpr int ACC_COLS = ACC * BN;
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
                                    : ACC_COLS <= 256 ? 256 : 512;
+  // Epilogue warps: SPLIT per TMEM lane quadrant, each owning BN / SPLIT columns.  The GELU
+  // epilogue is issue-bound, so it gets three warps per quadrant (bias then comes from smem to
+  // keep registers <= 128 at 512 threads); the others two.
+  static constexpr int SPLIT = (EPI == EPI_BIAS_GELU && BN % 96 == 0) ? 3 : 2;
+  static constexpr int EPI_WARPS = 4 * SPLIT;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr bool BIAS_SMEM = EPI == EPI_BIAS_GELU && SPLIT == 3;
   static constexpr int HEAD_BYTES = 1024;                         // mbarriers + TMEM slot
   static constexpr int STATS_BYTES =                              // LN: stats + bias/gamma/beta, 1 KB aligned
       EPI == EPI_BIAS_LN ? ((2 * 2 * BM * 4 * 4 + 3 * BN * 4 + 1023) / 1024) * 1024 : 0;
   static constexpr int STG_BUFS = 1;                              // per-warp output staging buffers
-  static constexpr int STG_BYTES = NUM_EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
+  static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
   static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES + STG_BYTES;
+  __host__ __device__ static int bias_bytes(int N) { return BIAS_SMEM ? ((N * 4 + 1023) / 1024) * 1024 : 0; }
   static constexpr int MAX_SMEM = 227 * 1024;
   static constexpr int MAX_STAGES = 8;
-  static constexpr int HALF = BN / 2;                             // columns per epilogue warp
+  static constexpr int HALF = BN / SPLIT;                         // columns per epilogue warp
   static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
   static_assert(B_BOX * N_LOADS * (PAIR ? 2 : 1) == BN, "B box split");
   static_assert(HALF % 32 == 0, "epilogue column split");
   // Weight-stationary (ws): the CTA's whole B slice [BN x K] stays resident; only A streams.
   __host__ __device__ static int b_res_bytes(int K, bool ws) { return ws ? (PAIR ? BN / 2 : BN) * K * 2 : 0; }
   __host__ __device__ static int stage_bytes(bool ws) { return A_STAGE_BYTES + (ws ? 0 : B_STAGE_BYTES); }
-  __host__ __device__ static int stages(int K, bool ws) {
-    const int n = (MAX_SMEM - FIXED_BYTES - b_res_bytes(K, ws)) / stage_bytes(ws);
+  __host__ __device__ static int stages(int K, bool ws, int N = 0) {
+    const int n = (MAX_SMEM - FIXED_BYTES - bias_bytes(N) - b_res_bytes(K, ws)) / stage_bytes(ws);
     return n > MAX_STAGES ? MAX_STAGES : n;
   }
-  __host__ __device__ static int smem_bytes(int K, bool ws) { return FIXED_BYTES + b_res_bytes(K, ws) + stages(K, ws) * stage_bytes(ws); }
+  __host__ __device__ static int smem_bytes(int K, bool ws, int N = 0) {
+    return FIXED_BYTES + bias_bytes(N) + b_res_bytes(K, ws) + stages(K, ws, N) * stage_bytes(ws);
+  }
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -107,7 +115,7 @@ struct Sched {
 //                 the accumulator buffer is released as soon as it is drained, so with ACC = 2 the
 //                 epilogue of tile i overlaps the mainloop of tile i + 1.
 template <int BN, int EPI, bool WS, bool PAIR>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
@@ -130,7 +138,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   float* s_gamma = s_bias + BN;
   float* s_beta = s_gamma + BN;
   uint8_t* sStg = smem + T::HEAD_BYTES + T::STATS_BYTES;  // [epi warp][STG_BUFS][2 KB] (1 KB aligned)
-  uint8_t* sB = sStg + T::STG_BYTES;                    // WS: resident [K/64][BN x 128 B]; else ring
+  float* s_bias_all = reinterpret_cast<float*>(sStg + T::STG_BYTES);   // BIAS_SMEM: bias[0..N)
+  uint8_t* sB = sStg + T::STG_BYTES + T::bias_bytes(N);  // WS: resident [K/64][BN x 128 B]; else ring
   uint8_t* sA = sB + T::b_res_bytes(K, WS);             // [stages] x 16 KB
   uint8_t* sBs = sA + stages * A_STAGE_BYTES;           // streaming B ring [stages] x B_STAGE_BYTES
 
@@ -148,7 +157,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], (PAIR ? 2 : 1) * NUM_EPI_WARPS);
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * T::EPI_WARPS);
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -289,16 +298,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue (warps 4..11)
     if constexpr (EPI == EPI_BIAS_LN) {       // LN tiles span all N columns: constants once
-      for (int i = threadIdx.x - 128; i < BN; i += NUM_EPI_WARPS * 32) {
+      for (int i = threadIdx.x - 128; i < BN; i += T::EPI_WARPS * 32) {
         s_bias[i] = bias[i];
         s_gamma[i] = gamma[i];
         s_beta[i] = beta[i];
       }
-      named_bar_sync(5, NUM_EPI_WARPS * 32);
+      named_bar_sync(5, T::EPI_WARPS * 32);
+    }
+    if constexpr (T::BIAS_SMEM) {
+      for (int i = threadIdx.x - 128; i < N; i += T::EPI_WARPS * 32) s_bias_all[i] = bias[i];
+      named_bar_sync(5, T::EPI_WARPS * 32);
     }
     int stg = 0;                              // staged output boxes issued by this warp
     const int q = warp & 3;                   // TMEM lane quadrant this warp may access
-    const int hh = (warp - 4) >> 2;           // column half
+    const int hh = (warp - 4) >> 2;           // column part (0 .. SPLIT-1)
     const int c_lo = hh * T::HALF;
     int it = 0;
     for (int t = sc.t0; t < sc.tend; t += sc.dt, ++it) {
@@ -331,10 +344,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // Software-pipelined over 32-column steps: the TMEM load and bias slice of step k+1 are in
         // flight while step k is computed and stored (tcgen05.wait::ld then covers only step k+1).
         const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c_lo);
+        const float4* sbp = reinterpret_cast<const float4*>(s_bias_all + n0 + c_lo);
         uint32_t r[2][32];
-        float4 b4[2][8];
+        float4 b4[T::BIAS_SMEM ? 1 : 2][8];
+        if constexpr (!T::BIAS_SMEM) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) b4[0][i] = __ldg(bp + i);
+          for (int i = 0; i < 8; ++i) b4[0][i] = __ldg(bp + i);
+        }
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         tmem_ld32(taddr + c_lo, r[0]);
@@ -344,13 +360,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_ld_wait_regs(r[cur]);
           if (k + 1 < NSTEP) {
             tmem_ld32(taddr + c_lo + 32 * (k + 1), r[cur ^ 1]);
+            if constexpr (!T::BIAS_SMEM) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) b4[cur ^ 1][i] = __ldg(bp + 8 * (k + 1) + i);
+              for (int i = 0; i < 8; ++i) b4[cur ^ 1][i] = __ldg(bp + 8 * (k + 1) + i);
+            }
           }
           uint32_t p[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 bb = b4[cur][i];
+            const float4 bb = T::BIAS_SMEM ? sbp[8 * k + i] : b4[T::BIAS_SMEM ? 0 : cur][i];
             const f32x2 v01 = fadd2(f2(__uint_as_float(r[cur][4 * i]), __uint_as_float(r[cur][4 * i + 1])), f2(bb.x, bb.y));
             const f32x2 v23 = fadd2(f2(__uint_as_float(r[cur][4 * i + 2]), __uint_as_float(r[cur][4 * i + 3])), f2(bb.z, bb.w));
             float v0 = f2lo(v01), v1 = f2hi(v01), v2 = f2lo(v23), v3 = f2hi(v23);
@@ -479,8 +497,8 @@ template <int BN, int EPI, bool WS, bool PAIR = false>
 cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   using T = TileCfg<BN, EPI, PAIR>;
   auto kern = gemm_tc_kernel<BN, EPI, WS, PAIR>;
-  const int smem = T::smem_bytes(g.K, WS);
-  const int stages = T::stages(g.K, WS);
+  const int smem = T::smem_bytes(g.K, WS, g.N);
+  const int stages = T::stages(g.K, WS, g.N);
   if (stages < 2 || smem > T::MAX_SMEM) return cudaErrorInvalidValue;
   static int attr = 0;
   if (attr < smem) {
@@ -507,7 +525,7 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   if (PAIR) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.blockDim = dim3(T::THREADS);
     cfg.dynamicSmemBytes = size_t(smem);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -520,7 +538,7 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
                               g.beta, g.C, g.eps, stages);
   }
-  kern<<<grid, GEMM_THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K,
+  kern<<<grid, T::THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K,
                                          g.bias, g.res, g.gamma, g.beta, g.C, g.eps, stages);
   return cudaGetLastError();
 }
@@ -532,7 +550,7 @@ bool use_ws(const GemmArgs& g) {
   using T = TileCfg<BN, EPI, PAIR>;
   const int64_t m_units = PAIR ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM - 1) / BM;
   const int units = PAIR ? num_sms() / 2 : num_sms();
-  return g.epi != EPI_BIAS_LN && T::stages(g.K, true) >= 3 && m_units >= units / (g.N / BN);
+  return g.epi != EPI_BIAS_LN && T::stages(g.K, true, g.N) >= 3 && m_units >= units / (g.N / BN);
 }
 
 template <int BN, int EPI>

@@ -336,6 +336,9 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
 // (bit-exact SuperBatch invariance).  O is written over the text's own Q rows and stored with
 // 16-byte coalesced stores.  A text longer than ATT_SHORT is left to attention_kernel.
 constexpr int ATT_SHORT = 64;
+#ifndef ATT_HEADS_PER_CTA
+#define ATT_HEADS_PER_CTA 2
+#endif
 
 template <int DH, int HG>
 struct TextAtt {
@@ -599,22 +602,23 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
                              int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
                              uint16_t* out, cudaStream_t st) {
   if (n_texts <= 0 || ntok <= 0) return cudaSuccess;
-  if (heads % 2) return cudaErrorInvalidValue;
+  constexpr int HG = ATT_HEADS_PER_CTA;
+  if (heads % HG) return cudaErrorInvalidValue;
   const float qscale = 1.4426950408889634f / sqrtf(float(head_dim));
   const int32_t nwin = (ntok + 63) >> 6;
   if (!win_ready)
     window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
 #define SURGE_ATT(DH)                                                                                        \
   case DH: {                                                                                                 \
-    using TA = TextAtt<DH, 2>;                                                                               \
+    using TA = TextAtt<DH, HG>;                                                                               \
     static bool attr_##DH = false;                                                                           \
     if (!attr_##DH) {                                                                                        \
-      cudaFuncSetAttribute(attention_text_kernel<DH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+      cudaFuncSetAttribute(attention_text_kernel<DH, HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                            int(TA::smem(ATT_SHORT)));                                                        \
       attr_##DH = true;                                                                                      \
     }                                                                                                        \
-    const dim3 grid(unsigned(nwin), unsigned(heads / 2));                                                    \
-    attention_text_kernel<DH, 2><<<grid, TA::WARPS * 32, TA::smem(max_len), st>>>(                           \
+    const dim3 grid(unsigned(nwin), unsigned(heads / HG));                                                    \
+    attention_text_kernel<DH, HG><<<grid, TA::WARPS * 32, TA::smem(max_len), st>>>(                           \
         qkv, cu, tok0, ntok, win, heads, out, qscale, TA::rows(max_len));                                    \
     if (max_len > ATT_SHORT) {                                                                               \
       constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \

@@ -74,30 +74,23 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Exact-erf GELU, x * Phi(x), on a pair (DESIGN.md "K7 GELU"): with t = min(|x|, 5.5),
-// E = Phi(-t) = exp(-t^2/2) * m(t), where m (the scaled Mills ratio) is a degree-9 minimax
-// polynomial (relative error 5.5e-5 on [0, 5.5]); then x * Phi(x) = x/2 + |x| (1/2 - E) for either
-// sign of x (branch-free).  |gelu error| <= 5.5e-5 |gelu(x)| wherever |gelu(x)| > 1e-6 and <= 9e-6
-// absolute everywhere: 36x below the bf16 rounding of the stored result.  One MUFU.EX2 and ~10
-// issue slots per value.
+// Exact-erf GELU, x * Phi(x), on a pair (DESIGN.md "GELU"): with t = min(|x|, 5.5),
+// E = Phi(-t) = 2^P(t), where P is a degree-6 minimax polynomial for log2 Phi(-t) on [0, 5.5]
+// (max |error| 3.6e-5 in log2); then x * Phi(x) = max(x, 0) - |x| E for either sign of x
+// (branch-free, no cancellation).  |gelu error| <= 2.5e-5 |gelu(x)| wherever |gelu(x)| > 1e-6 and
+// <= 3.8e-6 absolute everywhere: 80x below the bf16 rounding of the stored result.  Per value:
+// one MUFU.EX2, 3.5 FMA-pipe and 3 ALU-pipe instructions (the FMA pipe bounds this epilogue).
 __device__ __forceinline__ void gelu2(float& x0, float& x1) {
-  const float t0 = fminf(fabsf(x0), 5.5f), t1 = fminf(fabsf(x1), 5.5f);
-  const f32x2 t = f2(t0, t1);
-  const f32x2 a = fmul2(fmul2(t, t), f2(-0.72134752044448170368f, -0.72134752044448170368f));  // -t^2/2 log2 e
-  const f32x2 e = f2(ex2_approx(f2lo(a)), ex2_approx(f2hi(a)));
-  f32x2 m = f2(-8.42938611e-07f, -8.42938611e-07f);
-  m = ffma2(m, t, f2(2.55162200e-05f, 2.55162200e-05f));
-  m = ffma2(m, t, f2(-3.38936006e-04f, -3.38936006e-04f));
-  m = ffma2(m, t, f2(2.61646596e-03f, 2.61646596e-03f));
-  m = ffma2(m, t, f2(-1.31696069e-02f, -1.31696069e-02f));
-  m = ffma2(m, t, f2(4.63381338e-02f, 4.63381338e-02f));
-  m = ffma2(m, t, f2(-1.20678578e-01f, -1.20678578e-01f));
-  m = ffma2(m, t, f2(2.44876648e-01f, 2.44876648e-01f));
-  m = ffma2(m, t, f2(-3.98055506e-01f, -3.98055506e-01f));
-  m = ffma2(m, t, f2(4.99972499e-01f, 4.99972499e-01f));
-  const f32x2 E = fmul2(m, e);                                   // Phi(-|x|)
-  const f32x2 R = ffma2(E, f2(-1.f, -1.f), f2(0.5f, 0.5f));      // 1/2 - Phi(-|x|)
-  const f32x2 g = ffma2(f2(fabsf(x0), fabsf(x1)), R, fmul2(f2(x0, x1), f2(0.5f, 0.5f)));
+  const f32x2 t = f2(fminf(fabsf(x0), 5.5f), fminf(fabsf(x1), 5.5f));
+  f32x2 p = f2(2.61527854e-05f, 2.61527854e-05f);
+  p = ffma2(p, t, f2(-6.60965558e-04f, -6.60965558e-04f));
+  p = ffma2(p, t, f2(7.48821728e-03f, 7.48821728e-03f));
+  p = ffma2(p, t, f2(-5.19701709e-02f, -5.19701709e-02f));
+  p = ffma2(p, t, f2(-4.60329687e-01f, -4.60329687e-01f));
+  p = ffma2(p, t, f2(-1.15058401e+00f, -1.15058401e+00f));
+  p = ffma2(p, t, f2(-1.00003605e+00f, -1.00003605e+00f));
+  const f32x2 E = f2(ex2_approx(f2lo(p)), ex2_approx(f2hi(p)));     // Phi(-|x|)
+  const f32x2 g = ffma2(f2(-fabsf(x0), -fabsf(x1)), E, f2(fmaxf(x0, 0.f), fmaxf(x1, 0.f)));
   x0 = f2lo(g);
   x1 = f2hi(g);
 }

@@ -43,10 +43,10 @@ struct TileCfg {
   // Epilogue warps: SPLIT per TMEM lane quadrant, each owning BN / SPLIT columns.  The GELU
   // epilogue is issue-bound, so it gets three warps per quadrant (bias then comes from smem to
   // keep registers <= 128 at 512 threads); the others two.
-  static constexpr int SPLIT = (EPI == EPI_BIAS_GELU && BN % 96 == 0) ? 3 : 2;
+  static constexpr int SPLIT = EPI != EPI_BIAS_GELU ? 2 : BN % 128 == 0 ? 4 : BN % 96 == 0 ? 3 : 2;
   static constexpr int EPI_WARPS = 4 * SPLIT;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr bool BIAS_SMEM = EPI == EPI_BIAS_GELU && SPLIT == 3;
+  static constexpr bool BIAS_SMEM = EPI == EPI_BIAS_GELU && SPLIT > 2;
   static constexpr int HEAD_BYTES = 1024;                         // mbarriers + TMEM slot
   static constexpr int STATS_BYTES =                              // LN: stats + bias/gamma/beta, 1 KB aligned
       EPI == EPI_BIAS_LN ? ((2 * 2 * BM * 4 * 4 + 3 * BN * 4 + 1023) / 1024) * 1024 : 0;
@@ -623,9 +623,14 @@ bool gemm_use_pair(int N, int K, int epi) {
 
 int gemm_bn_for(int N, int K, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
-  if (gemm_use_pair(N, K, epi)) return 384;
-  // 192-column slices whose [192 x K] weight block can stay resident (weight-stationary) win over
-  // streaming 256-column tiles: A is re-read N/192 times from L2 but B is read once per CTA.
+#ifdef GEMM_FORCE_BN
+  if (N % GEMM_FORCE_BN == 0) return GEMM_FORCE_BN;   // tuning experiments only
+#endif
+  // Weight-stationary slices (the [BN x K] weight block stays resident, A streams; A is re-read
+  // N/BN times from L2, B once per CTA).  128-column slices leave room for 7 A stages and measured
+  // fastest in isolation (scripts/gemm_bench.py, M = 262144, K = 384: BN 64/128/192 ->
+  // QKV 691/1078/1007, FFN1(bias) 701/1102/1020 TFLOP/s): these GEMMs are bound by A-tile latency.
+  if (N % 128 == 0 && TileCfg<128, EPI_BIAS>::stages(K, true) >= 6) return 128;
   if (N % 192 == 0 && TileCfg<192, EPI_BIAS>::stages(K, true) >= 3) return 192;
   if (N % 256 == 0) return 256;
   if (N % 192 == 0) return 192;

@@ -55,8 +55,10 @@ typedef struct surge_ctx* surge_handle;
  *   Encoder classes (reading #12): MiniLM-L6 class 30522/512/2, d=384, L=6, H=12,
  *   ffn=1536; bge-base class d=768, L=12, H=12, ffn=3072; bge-large class d=1024, L=24, H=16,
  *   ffn=4096; toy (C1) vocab 1024, max_pos 64, d=64, L=2, H=4, ffn=256.
- *   Supported on the sm_100a path in this build: hidden in {64, 384}, head_dim in {16, 32},
- *   ffn a multiple of 64 (others return SURGE_E_INVALID_ARG at create).
+ *   Supported on the sm_100a path in this build: hidden in {64, 384, 768, 1024}, head_dim in
+ *   {16, 32, 64}, an even number of heads, ffn a multiple of 64 (others return SURGE_E_INVALID_ARG
+ *   at create).  hidden 64/384 fuse LayerNorm into the GEMM epilogue; 768/1024 use an fp32
+ *   pre-LN pass + a row LayerNorm kernel.
  *   Thresholds: b_min = efficiency trigger, b_max = memory-safety trigger, texts,
  *   0 < b_min < b_max.
  *   Sharding: the process encodes only the LPT pieces of every SuperBatch assigned to `rank`
@@ -223,14 +225,21 @@ surge_status surge_op_embed_ln(surge_handle h, const int32_t* d_ids, const int32
 /*
  * tcgen05 GEMM with fused epilogue, device pointers, bf16 bit patterns as uint16:
  *   C[M x N] = epi(A[M x K] * B[N x K]^T + bias[N])
- *   epi = 0: identity; 1: exact GELU; 2: LayerNorm(. + R[M x N]) * gamma[N] + beta[N] (N = full row)
+ *   epi = 0: identity; 1: exact GELU; 2: LayerNorm(. + R[M x N]) * gamma[N] + beta[N] (N = full row);
+ *   epi = 3: . + R[M x N] written as FLOAT32 (d_c is then a float* [M x N]): the pre-LayerNorm rows
+ *            of hidden sizes whose row does not fit the fused epilogue (finish with surge_op_layernorm).
  * bias/gamma/beta: float32[N].  Supported: K % 64 == 0; N per epilogue as the encoder needs
- * (epi 0/1: N % 64 == 0; epi 2: N in {64, 384}); any M >= 1.
+ * (epi 0/1: N % 64 == 0; epi 2: N in {64, 384}; epi 3: N % 128 == 0); any M >= 1.
  */
 surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float* d_bias,
                            const uint16_t* d_res, const float* d_gamma, const float* d_beta,
                            uint16_t* d_c, int64_t M, int32_t N, int32_t K, int32_t epi,
                            float ln_eps, void* stream);
+
+/* Row LayerNorm (post-LN of BERT, eps ln_eps, biased variance): v float32 [rows x d] -> bf16 y,
+ * y = (v - mean) / sqrt(var + eps) * gamma + beta; d in {768, 1024}.  Device pointers. */
+surge_status surge_op_layernorm(const float* d_v, int64_t rows, int32_t d, const float* d_gamma, const float* d_beta,
+                                float ln_eps, uint16_t* d_y, void* stream);
 
 /* K5: varlen attention, qkv bf16 [T x 3*heads*head_dim] (Q | K | V), out bf16 [T x heads*head_dim]. */
 surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int64_t n_texts,

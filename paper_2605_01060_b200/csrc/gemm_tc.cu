@@ -381,6 +381,32 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
           }
           stage_store(p, n0 + c_lo + 32 * k);
         }
+      } else if constexpr (EPI == EPI_BIAS_RES) {
+        // fp32 v = acc + bias + residual, stored directly (each thread: its row, 32 columns / step)
+        const uint16_t* rrow = res + size_t(ok ? row : 0) * N + n0 + c_lo;
+        float* frow = reinterpret_cast<float*>(C) + size_t(row) * N + n0 + c_lo;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+#pragma unroll 1
+        for (int k = 0; k < NSTEP; ++k) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c_lo + 32 * k, r);
+          uint4 rs[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rs[i] = reinterpret_cast<const uint4*>(rrow + 32 * k)[i];
+          tmem_ld_wait_regs(r);
+          const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c_lo + 32 * k);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 b4 = __ldg(bp + i);
+            const uint32_t u0 = (&rs[i >> 1].x)[(i & 1) * 2], u1 = (&rs[i >> 1].x)[(i & 1) * 2 + 1];
+            const float4 o = make_float4(__uint_as_float(r[4 * i]) + b4.x + bf16lo(u0),
+                                         __uint_as_float(r[4 * i + 1]) + b4.y + bf16hi(u0),
+                                         __uint_as_float(r[4 * i + 2]) + b4.z + bf16lo(u1),
+                                         __uint_as_float(r[4 * i + 3]) + b4.w + bf16hi(u1));
+            if (ok) reinterpret_cast<float4*>(frow + 32 * k)[i] = o;
+          }
+        }
       } else {
         // LayerNorm over the full row (BN == N), two warps per row (column halves).
         // pass 1: v = acc + bias + residual, written back to TMEM in place, shifted partial sums;
@@ -550,7 +576,8 @@ bool use_ws(const GemmArgs& g) {
   using T = TileCfg<BN, EPI, PAIR>;
   const int64_t m_units = PAIR ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM - 1) / BM;
   const int units = PAIR ? num_sms() / 2 : num_sms();
-  return g.epi != EPI_BIAS_LN && T::stages(g.K, true, g.N) >= 3 && m_units >= units / (g.N / BN);
+  return g.epi != EPI_BIAS_LN && g.epi != EPI_BIAS_RES && T::stages(g.K, true, g.N) >= 3 &&
+         m_units >= units / (g.N / BN);
 }
 
 template <int BN, int EPI>
@@ -623,6 +650,7 @@ bool gemm_use_pair(int N, int K, int epi) {
 
 int gemm_bn_for(int N, int K, int epi) {
   if (epi == EPI_BIAS_LN) return (N == 64 || N == 384) ? N : 0;
+  if (epi == EPI_BIAS_RES) return N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 0;
 #ifdef GEMM_FORCE_BN
   if (N % GEMM_FORCE_BN == 0) return GEMM_FORCE_BN;   // tuning experiments only
 #endif
@@ -630,7 +658,8 @@ int gemm_bn_for(int N, int K, int epi) {
   // N/BN times from L2, B once per CTA).  128-column slices leave room for 7 A stages and measured
   // fastest in isolation (scripts/gemm_bench.py, M = 262144, K = 384: BN 64/128/192 ->
   // QKV 691/1078/1007, FFN1(bias) 701/1102/1020 TFLOP/s): these GEMMs are bound by A-tile latency.
-  if (N % 128 == 0 && TileCfg<128, EPI_BIAS>::stages(K, true) >= 6) return 128;
+  // (the GELU GEMM keeps 192-column slices: its 12-warp epilogue measured ~5% faster in the step)
+  if (epi != EPI_BIAS_GELU && N % 128 == 0 && TileCfg<128, EPI_BIAS>::stages(K, true) >= 6) return 128;
   if (N % 192 == 0 && TileCfg<192, EPI_BIAS>::stages(K, true) >= 3) return 192;
   if (N % 256 == 0) return 256;
   if (N % 192 == 0) return 192;
@@ -671,6 +700,12 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
       switch (BN) {
         case 64: return launch_gemm_bn<64, EPI_BIAS_LN>(g, st);
         case 384: return launch_gemm_bn<384, EPI_BIAS_LN>(g, st);
+      }
+      break;
+    case EPI_BIAS_RES:
+      switch (BN) {
+        case 128: return launch_gemm_bn<128, EPI_BIAS_RES>(g, st);
+        case 256: return launch_gemm_bn<256, EPI_BIAS_RES>(g, st);
       }
       break;
   }

@@ -10,7 +10,9 @@
 
 namespace surge {
 
-enum Epilogue : int { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_BIAS_LN = 2 };
+// EPI_BIAS_RES: fp32 C = A B^T + b + R (the pre-LayerNorm row, for hidden sizes whose full row
+// does not fit one CTA's TMEM; launch_layernorm then normalises it).  C is float* in that case.
+enum Epilogue : int { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_BIAS_LN = 2, EPI_BIAS_RES = 3 };
 
 struct GemmArgs {
   const CUtensorMap* tmA;   // A [M x K]
@@ -35,6 +37,9 @@ int gemm_bn_for(int N, int K, int epi);
 bool gemm_use_pair(int N, int K, int epi);
 uint32_t gemm_b_box_rows(int N, int K, int epi);   // TMA box rows of the B (weight) tensor map
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);
+// LN GEMMs fuse the LayerNorm into the epilogue when the full row fits one CTA's TMEM (d in {64, 384});
+// otherwise they write fp32 pre-LN rows (EPI_BIAS_RES) and launch_layernorm finishes them.
+inline bool fused_ln(int d) { return d == 64 || d == 384; }
 
 // K1: cu[0..n], row_off[0..m], tok_off[0..m] (single CTA)
 cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes, int64_t m, int32_t* cu,
@@ -51,6 +56,9 @@ cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
                              int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
                              uint16_t* out, cudaStream_t st);
+// Row LayerNorm: y[r] = LN(v[r]) * gamma + beta, v fp32 [rows x d] -> bf16 (d in {768, 1024}).
+cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* gamma, const float* beta, float eps,
+                             uint16_t* y, cudaStream_t st);
 // K9
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
                                float* out, cudaStream_t st);
@@ -100,6 +108,7 @@ struct LayerW {
 struct Workspace {
   int64_t cap = 0;
   uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
+  float* V = nullptr;       // fp32 pre-LayerNorm rows (hidden sizes without the fused LN epilogue)
   int32_t* win = nullptr;   // attention: first text of each 64-token window, cap/64 + 2 entries
   cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
   void release();

@@ -508,6 +508,45 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
   }
 }
 
+// ------------------------------------------------------------------------ row LayerNorm (d > 384)
+// One warp per row: fp32 v (D values, 16-byte loads) -> mean, biased variance (two passes over the
+// registers), y = (v - mean) rstd gamma + beta -> bf16.
+template <int D>
+__global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict__ v, int64_t rows,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta, float eps,
+                                                        uint16_t* __restrict__ y) {
+  constexpr int PER = D / 128;                   // float4 per lane
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float4* vr = reinterpret_cast<const float4*>(v + size_t(row) * D);
+  float4 x[PER];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    x[i] = vr[lane + 32 * i];
+    s += (x[i].x + x[i].y) + (x[i].z + x[i].w);
+  }
+  const float mean = warp_sum(s) * (1.0f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const float a = x[i].x - mean, b = x[i].y - mean, c = x[i].z - mean, d = x[i].w - mean;
+    q += (a * a + b * b) + (c * c + d * d);
+  }
+  const float rstd = rsqrtf(warp_sum(q) * (1.0f / D) + eps);
+  uint2* yr = reinterpret_cast<uint2*>(y + size_t(row) * D);
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int g = lane + 32 * i;
+    const float4 gg = reinterpret_cast<const float4*>(gamma)[g];
+    const float4 bb = reinterpret_cast<const float4*>(beta)[g];
+    yr[g] = make_uint2(pack_bf16x2((x[i].x - mean) * rstd * gg.x + bb.x, (x[i].y - mean) * rstd * gg.y + bb.y),
+                       pack_bf16x2((x[i].z - mean) * rstd * gg.z + bb.z, (x[i].w - mean) * rstd * gg.w + bb.w));
+  }
+}
+
 // ----------------------------------------------------------------------------- K9 meanpool + L2
 template <int D>
 __global__ void __launch_bounds__(256) meanpool_l2_kernel(const uint16_t* __restrict__ x,
@@ -640,6 +679,18 @@ cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0
                                 cudaStream_t st) {
   if (n_texts <= 0) return cudaSuccess;
   window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* gamma, const float* beta, float eps,
+                             uint16_t* y, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const unsigned grid = blocks_for_warps(rows, 8);
+  switch (d) {
+    case 768: layernorm_kernel<768><<<grid, 256, 0, st>>>(v, rows, gamma, beta, eps, y); break;
+    case 1024: layernorm_kernel<1024><<<grid, 256, 0, st>>>(v, rows, gamma, beta, eps, y); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   if ((e = cudaMalloc(&X1, t * s.d * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&H, t * s.ffn * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&win, (t / 64 + 2) * sizeof(int32_t))) != cudaSuccess) return e;
+  if (!fused_ln(s.d) && (e = cudaMalloc(&V, t * s.d * 4)) != cudaSuccess) return e;
   cap = cap_tokens;
   return cudaSuccess;
 }
@@ -38,6 +39,8 @@ void Workspace::release() {
   }
   if (win) cudaFree(win);
   win = nullptr;
+  if (V) cudaFree(V);
+  V = nullptr;
   cap = 0;
 }
 
@@ -109,9 +112,10 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(take_f32(&L.ln2_g, d));
       SURGE_TRY(take_f32(&L.ln2_b, d));
       SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(int(3 * d), int(d), EPI_BIAS)));
-      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(int(d), int(d), EPI_BIAS_LN)));
+      const int ln_epi = fused_ln(int(d)) ? EPI_BIAS_LN : EPI_BIAS_RES;
+      SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(int(d), int(d), ln_epi)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
-      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), EPI_BIAS_LN)));
+      SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), ln_epi)));
     }
     return cudaSuccess;
   }();
@@ -218,6 +222,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   SURGE_TRY(launch_window_index(cu, n, tok0, ntok, ws.win, st));
   if (P) prof->end(KK_EMBED, st, ev, 0.0, M * (4 + 2 * D + 2 * D + 2 * D));
   k += 2;
+  const bool fused = fused_ln(d);
   for (const LayerW& L : layers_) {
     GemmArgs g{};
     g.M = ntok;
@@ -235,7 +240,13 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
     g.gamma = L.ln1_g; g.beta = L.ln1_b; g.C = ws.X1;
     if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_gemm(g, st));
+    if (fused) {
+      SURGE_TRY(launch_gemm(g, st));
+    } else {
+      g.epi = EPI_BIAS_RES; g.C = reinterpret_cast<uint16_t*>(ws.V);
+      SURGE_TRY(launch_gemm(g, st));
+      SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln1_g, L.ln1_b, s_.eps, ws.X1, st));
+    }
     if (P) prof->end(KK_OUT_LN, st, ev, 2 * M * D * D, 2 * (M * D + D * D + 2 * M * D));
     // K7: H = GELU(X1 W1^T + b1)
     g.tmA = &tmX1; g.tmB = &L.tm_w1; g.tmC = &smH; g.tmR = nullptr; g.N = f; g.K = d; g.epi = EPI_BIAS_GELU; g.bias = L.b1; g.res = nullptr;
@@ -247,9 +258,15 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     g.tmA = &tmH; g.tmB = &L.tm_w2; g.tmC = &smX; g.tmR = &tmX1; g.N = d; g.K = f; g.epi = EPI_BIAS_LN; g.bias = L.b2; g.res = ws.X1;
     g.gamma = L.ln2_g; g.beta = L.ln2_b; g.C = ws.X;
     if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_gemm(g, st));
+    if (fused) {
+      SURGE_TRY(launch_gemm(g, st));
+    } else {
+      g.epi = EPI_BIAS_RES; g.C = reinterpret_cast<uint16_t*>(ws.V);
+      SURGE_TRY(launch_gemm(g, st));
+      SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln2_g, L.ln2_b, s_.eps, ws.X, st));
+    }
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += 5 + (max_len > 64 ? 1 : 0);
+    k += 5 + (max_len > 64 ? 1 : 0) + (fused ? 0 : 2);
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));

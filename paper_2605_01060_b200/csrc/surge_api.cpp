@@ -558,7 +558,8 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
       k.max_position <= 0 || k.type_vocab_size <= 0)
     return SURGE_E_INVALID_ARG;
   const int dh = k.hidden / k.heads;
-  if (!(k.hidden == 64 || k.hidden == 384) || !(dh == 16 || dh == 32 || dh == 64) || k.ffn % 64 != 0)
+  if (!(k.hidden == 64 || k.hidden == 384 || k.hidden == 768 || k.hidden == 1024) ||
+      !(dh == 16 || dh == 32 || dh == 64) || k.ffn % 64 != 0 || k.heads % 2 != 0)
     return SURGE_E_INVALID_ARG;
   if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return SURGE_E_INVALID_ARG;
   ModelShape s{k.vocab_size, k.max_position, k.type_vocab_size, k.hidden, k.layers, k.heads, k.ffn, k.ln_eps};
@@ -1118,8 +1119,9 @@ surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float
                            const float* d_gamma, const float* d_beta, uint16_t* d_c, int64_t M, int32_t N, int32_t K,
                            int32_t epi, float ln_eps, void* stream) {
   using namespace surge;
-  if (!d_a || !d_b || !d_bias || !d_c || M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 2) return SURGE_E_INVALID_ARG;
+  if (!d_a || !d_b || !d_bias || !d_c || M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 3) return SURGE_E_INVALID_ARG;
   if (epi == EPI_BIAS_LN && (!d_res || !d_gamma || !d_beta)) return SURGE_E_INVALID_ARG;
+  if (epi == EPI_BIAS_RES && !d_res) return SURGE_E_INVALID_ARG;
   const int BN = gemm_bn_for(N, K, epi);
   if (BN == 0 || K % 64 != 0) return SURGE_E_INVALID_ARG;
   if (init_tma_encoder() != cudaSuccess) return SURGE_E_CUDA;
@@ -1133,6 +1135,13 @@ surge_status surge_op_gemm(const uint16_t* d_a, const uint16_t* d_b, const float
     return SURGE_E_CUDA;
   GemmArgs g{&ta, &tb, &tc, &tr, M, N, K, epi, d_bias, d_res, d_gamma, d_beta, d_c, ln_eps};
   cudaError_t e = launch_gemm(g, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SURGE_OK : SURGE_E_CUDA;
+}
+
+surge_status surge_op_layernorm(const float* d_v, int64_t rows, int32_t d, const float* d_gamma, const float* d_beta,
+                                float ln_eps, uint16_t* d_y, void* stream) {
+  if (!d_v || !d_gamma || !d_beta || !d_y || rows < 0) return SURGE_E_INVALID_ARG;
+  cudaError_t e = surge::launch_layernorm(d_v, rows, d, d_gamma, d_beta, ln_eps, d_y, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SURGE_OK : SURGE_E_CUDA;
 }
 

@@ -102,6 +102,7 @@ _SIGS = {
     "surge_op_gemm": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_float, _p]),
     "surge_op_attention": (C.c_int, [_p, _p, C.c_int64, C.c_int32, C.c_int32, _p, _p]),
+    "surge_op_layernorm": (C.c_int, [_p, C.c_int64, C.c_int32, _p, _p, C.c_float, _p, _p]),
     "surge_op_meanpool_l2": (C.c_int, [_p, _p, C.c_int64, C.c_int32, _p, _p]),
     "surge_aggregate": (C.c_int, [_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _p, _p, _i64p, _i64p]),
     "surge_encode_superbatch": (C.c_int, [_p, _p, _p, _p, C.c_int64, _p, C.c_int64, _p, _p]),
@@ -266,6 +267,11 @@ def surge_op_embed_ln(h, d_ids, d_cu, n_texts, d_x, stream=None):
 def surge_op_gemm(a, b, bias, res, gamma, beta, c, M, N, K, epi, ln_eps=1e-12, stream=None):
     return _check(None, lib.surge_op_gemm(_ptr(a), _ptr(b), _ptr(bias), _ptr(res), _ptr(gamma), _ptr(beta),
                                           _ptr(c), M, N, K, epi, ln_eps, _stream(stream)), "surge_op_gemm")
+
+
+def surge_op_layernorm(v, rows, d, gamma, beta, out, ln_eps=1e-12, stream=None):
+    return _check(None, lib.surge_op_layernorm(_ptr(v), rows, d, _ptr(gamma), _ptr(beta), ln_eps, _ptr(out),
+                                               _stream(stream)), "surge_op_layernorm")
 
 
 def surge_op_attention(qkv, cu, n_texts, heads, head_dim, out, stream=None):

@@ -69,6 +69,8 @@ GEMM_CASES = [
     (256, 128, 128, 0), (200, 64, 192, 0),
     # many tiles per CTA (weight-stationary slices, TMEM double buffering) + ragged tails
     (50001, 1152, 384, 0), (50001, 1536, 384, 1), (50001, 384, 384, 2), (20001, 384, 1536, 2),
+    # bge-base / bge-large class shapes (N1): streaming 256-column tiles, fp32 pre-LN epilogue (epi 3)
+    (3001, 2304, 768, 0), (3001, 3072, 768, 1), (3001, 768, 768, 3), (3001, 768, 3072, 3), (777, 1024, 4096, 3),
 ]
 
 
@@ -81,10 +83,15 @@ def test_gemm_vs_torch(N, M, Nn, K, epi):
     res = bf16_bits(torch.randn(M, Nn, device="cuda", generator=g))
     gamma = 1 + 0.1 * torch.randn(Nn, device="cuda", generator=g)
     beta = 0.1 * torch.randn(Nn, device="cuda", generator=g)
-    Cc = torch.zeros(M, Nn, dtype=torch.int16, device="cuda")
+    Cc = torch.zeros(M, Nn, dtype=torch.float32 if epi == 3 else torch.int16, device="cuda")
     N.surge_op_gemm(A, B, bias, res, gamma, beta, Cc, M, Nn, K, epi, 1e-12)
     torch.cuda.synchronize()
     acc = from_bits(A) @ from_bits(B).T + bias
+    if epi == 3:   # fp32 out: only the fp32 accumulation order differs from torch
+        ref = acc + from_bits(res)
+        err = (Cc - ref).abs()
+        assert bool((err <= 1e-5 * ref.abs() + 1e-4).all()), f"max err {err.max().item():.4g}"
+        return
     if epi == 1:
         ref = torch.nn.functional.gelu(acc)
     elif epi == 2:
@@ -167,3 +174,17 @@ def test_embed_ln_vs_oracle(N, name):
         assert np.max(np.abs(got - ref) - 2 ** -8 * np.abs(ref)) <= 1e-3
     finally:
         N.surge_destroy(h)
+
+
+@pytest.mark.parametrize("d", [768, 1024])
+def test_layernorm_rows_vs_torch(N, d):
+    g = torch.Generator(device="cuda").manual_seed(d)
+    v = torch.randn(3001, d, device="cuda", generator=g) * 3 + 0.5
+    gamma = 1 + 0.1 * torch.randn(d, device="cuda", generator=g)
+    beta = 0.1 * torch.randn(d, device="cuda", generator=g)
+    y = torch.zeros(3001, d, dtype=torch.int16, device="cuda")
+    N.surge_op_layernorm(v, 3001, d, gamma, beta, y, 1e-12)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.layer_norm(v, (d,), gamma, beta, eps=1e-12)
+    err = (from_bits(y) - ref).abs()
+    assert bool((err <= 2 ** -8 * ref.abs() + 1e-4).all()), err.max().item()

@@ -199,3 +199,23 @@ def test_two_ranks_on_one_gpu_cover_exactly(N):
     # oracle LPT: per SuperBatch, the rank-owned rows match
     A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, wcfg.b_min, wcfg.b_max)
     assert len(A.flushes) == len(sbs1)
+
+
+@pytest.mark.parametrize("enc,length_model", [("bgebase", "bytes47"), ("bgelarge", "long")])
+def test_larger_encoder_classes_sample(N, enc, length_model):
+    """NEXT N1: bge-base (d=768, 12 layers) and bge-large (d=1024, 24 layers, texts up to 512 tokens)
+    classes through the streaming ABI; sampled rows vs the oracle (same tolerance gate)."""
+    ecfg = ENCODERS[enc]
+    wcfg = scaled(WORKLOADS["minilm"], n_texts=3000, n_partitions=12, b_min=1000, b_max=5000,
+                  length_model=length_model)
+    w = make_weights(ecfg, seed=1234)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=2)
+    got, sbs, stats, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+    check_integer_parity(wl, sbs, stats, wcfg.b_min, wcfg.b_max)
+    E = oenc.Encoder(ecfg, w)
+    rng = np.random.default_rng(1)
+    for key, ids, lens in wl:
+        n = len(lens)
+        T = texts_of(ids, lens)
+        rows = sorted({0, n - 1, int(np.argmax(lens)), *rng.integers(0, n, size=min(n, 2)).tolist()})
+        compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))

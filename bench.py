@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="minilm")
+    ap.add_argument("--encoder", default="minilm", choices=["minilm", "bgebase", "bgelarge", "toy"],
+                    help="encoder class (the headline is minilm; bgebase/bgelarge = NEXT N1)")
     ap.add_argument("--n-texts", type=int, default=0, help="override N (default: the config's 10M)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--chunk-tokens", type=int, default=0)
@@ -145,7 +147,7 @@ def run_reference(args, world, rank):
     """--impl reference: the oracle timed on host cores (rank 0 only)."""
     if rank != 0:
         return
-    ecfg = ENCODERS["minilm"]
+    ecfg = ENCODERS[args.encoder]
     wcfg = WORKLOADS[args.workload]
     if args.n_texts:
         wcfg = scaled(wcfg, n_texts=args.n_texts)
@@ -176,7 +178,7 @@ def run_reference(args, world, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.workload}: N={wcfg.n_texts}, P={wcfg.n_partitions}, sigma={wcfg.sigma}, "
-                                   f"MiniLM-L6 class (d=384, 6 layers), B_min={wcfg.b_min}, B_max={wcfg.b_max}",
+                                   f"{enc_desc(ecfg)}, B_min={wcfg.b_min}, B_max={wcfg.b_max}",
                        "step": f"Alg.1 over all partitions + oracle encode of {per_step} texts"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{per_step} texts per step, consecutive in stream order"},
@@ -206,7 +208,7 @@ def main():
     from paper_2605_01060_b200 import native as N
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    ecfg = ENCODERS["minilm"]
+    ecfg = ENCODERS[args.encoder]
     wcfg = WORKLOADS[args.workload]
     if args.n_texts:
         wcfg = scaled(wcfg, n_texts=args.n_texts)
@@ -308,12 +310,12 @@ def main():
     gemm_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("gemm"))
     all_flops = sum(v["flops"] for v in prof.values())
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    metric = METRIC if args.encoder == "minilm" else METRIC.replace("MiniLM-L6", enc_desc(ecfg).split(" (")[0])
+    line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.workload}: N={wl.n_texts} texts ({wl.n_tokens} tokens), "
-                                   f"P={wcfg.n_partitions} log-normal sigma={wcfg.sigma}, MiniLM-L6 class "
-                                   f"(d=384, 6 layers, 12 heads, ffn 1536, random-init bf16), "
+                                   f"P={wcfg.n_partitions} log-normal sigma={wcfg.sigma}, {enc_desc(ecfg)}, "
                                    f"B_min={wcfg.b_min}, B_max={wcfg.b_max}",
                        "superbatches_per_step": F, "parallelism": f"lpt{world}",
                        "l2": "inputs (ids 565 MB) and outputs (15.4 GB) larger than L2; no explicit flush",
@@ -358,6 +360,7 @@ def ncu_traffic(kernel: str):
 def run_e2e(N, h, wl, args, world, rank, dev):
     """Streaming C ABI from host memory: submit every partition, poll + release, finish, drain."""
     import torch
+    h_dim = ENCODERS[args.encoder].hidden
     parts = [wl.partition(k) for k in range(len(wl.sizes))]
 
     def one():
@@ -397,13 +400,19 @@ def run_e2e(N, h, wl, args, world, rank, dev):
         t = float(tt.item())
     return {"value": wl.n_texts / t, "unit": UNIT,
             "h2d_bytes_per_step": int(4 * (stats["local_tokens"] + stats["local_texts"])),
-            "d2h_bytes_per_step": int(stats["local_texts"]) * 384 * 4,
+            "d2h_bytes_per_step": int(stats["local_texts"]) * int(h_dim) * 4,
             "steps": len(times), "ttfo_s": stats["ttfo_s"], "peak_buffered_texts": stats["peak_buffered_texts"],
             "lemma_bound_texts": int(wl.cfg.b_min - 1 + int(wl.sizes.max())),
             "peak_inflight_texts": stats["peak_inflight_texts"], "superbatches": stats["superbatches"],
             "safety_flushes": stats["safety_flushes"], "rows_delivered": rows,
             "encode_ms_total": stats["encode_ms_total"],
             "host_peak_rss_gb": peak_rss_gb()}
+
+
+def enc_desc(ecfg) -> str:
+    names = {"minilm": "MiniLM-L6 class", "bgebase": "bge-base class", "bgelarge": "bge-large class", "toy": "toy"}
+    return (f"{names.get(ecfg.name, ecfg.name)} (d={ecfg.hidden}, {ecfg.layers} layers, {ecfg.heads} heads, "
+            f"ffn {ecfg.ffn}, random-init bf16)")
 
 
 def peak_rss_gb():

@@ -55,7 +55,9 @@ cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0
                                 cudaStream_t st);
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
                              int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
-                             uint16_t* out, cudaStream_t st);
+                             uint16_t* out, cudaStream_t st, const int32_t* d_long = nullptr, int32_t n_long = 0);
+// d_long: device int32[n_long], indices (relative to cu) of the texts longer than 64 tokens;
+// nullptr = unknown (all texts are scanned by the scalar per-(text, head) kernel).
 // Row LayerNorm: y[r] = LN(v[r]) * gamma + beta, v fp32 [rows x d] -> bf16 (d in {768, 1024}).
 cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* gamma, const float* beta, float eps,
                              uint16_t* y, cudaStream_t st);
@@ -109,6 +111,7 @@ struct Workspace {
   int64_t cap = 0;
   uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
   float* V = nullptr;       // fp32 pre-LayerNorm rows (hidden sizes without the fused LN epilogue)
+  int32_t* long_idx = nullptr;   // texts of the chunk longer than 64 tokens, cap/65 + 1 entries
   int32_t* win = nullptr;   // attention: first text of each 64-token window, cap/64 + 2 entries
   cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
   void release();

@@ -508,6 +508,154 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
   }
 }
 
+// ------------------------------------------------- K5 (texts > ATT_SHORT tokens): one CTA per (text, head)
+// The text's K and V rows for the head (<= max_position rows) stay in shared memory; query blocks of
+// 128 rows (8 warps x 16) are staged in turn.  The per-row arithmetic is the text-tiled kernel's:
+// 16-row query tiles and 16-key blocks aligned to the text start, mma.sync m16n8k16 with P split
+// hi+lo, online softmax over the key blocks in order (so long and short texts follow one rule).
+template <int DH>
+struct LongAtt {
+  static constexpr int WARPS = 8;
+  static constexpr int QROWS = 16 * WARPS;
+  static constexpr int LDS = DH + 8;
+  static constexpr int CH = DH / 8;
+  static int kv_rows(int max_len) { return ((max_len + 15) / 16) * 16 + 16; }
+  static size_t smem(int max_len) { return size_t(2 * kv_rows(max_len) + QROWS + 16) * LDS * 2; }
+};
+
+template <int DH>
+__global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel(
+    const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu, const int32_t* __restrict__ texts,
+    int32_t tok0, int heads, uint16_t* __restrict__ out, float qscale, int kv_rows) {
+  using A = LongAtt<DH>;
+  constexpr int LDS = A::LDS, CH = A::CH;
+  extern __shared__ __align__(16) uint16_t att_sm[];
+  uint16_t* sK = att_sm;                         // [kv_rows][LDS]
+  uint16_t* sV = sK + kv_rows * LDS;             // [kv_rows][LDS]
+  uint16_t* sQ = sV + kv_rows * LDS;             // [QROWS + 16][LDS]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t txt = texts[blockIdx.x];
+  const int h = blockIdx.y;
+  const int d = heads * DH, ld = 3 * d;
+  const int32_t a = cu[txt] - tok0, len = cu[txt + 1] - cu[txt];
+  const int nt = (len + 15) >> 4;
+  for (int i = tid; i < len * CH; i += blockDim.x) {
+    const int r = i / CH, c = i - r * CH;
+    const uint16_t* g = qkv + size_t(a + r) * ld + h * DH + c * 8;
+    cp_async16(sK + r * LDS + c * 8, g + d);
+    cp_async16(sV + r * LDS + c * 8, g + 2 * d);
+  }
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < (nt * 16 + 16 - len) * CH; i += blockDim.x) {
+    const int r = len + i / CH, c = i % CH;
+    *reinterpret_cast<uint4*>(sK + r * LDS + c * 8) = z;
+    *reinterpret_cast<uint4*>(sV + r * LDS + c * 8) = z;
+  }
+  const int g = lane >> 2, c4 = lane & 3;
+#pragma unroll 1
+  for (int qb0 = 0; qb0 < len; qb0 += A::QROWS) {
+    const int nq = min(A::QROWS, len - qb0);
+    for (int i = tid; i < nq * CH; i += blockDim.x) {
+      const int r = i / CH, c = i - r * CH;
+      cp_async16(sQ + r * LDS + c * 8, qkv + size_t(a + qb0 + r) * ld + h * DH + c * 8);
+    }
+    for (int i = tid; i < (A::QROWS + 16 - nq) * CH; i += blockDim.x) {
+      const int r = nq + i / CH, c = i % CH;
+      *reinterpret_cast<uint4*>(sQ + r * LDS + c * 8) = z;
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const int qt = (qb0 >> 4) + warp;            // query tile within the text
+    if (16 * qt < len) {
+      uint32_t qa[DH / 16][4];
+      const uint32_t q_addr = smem_u32(sQ + (16 * warp + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
+#pragma unroll
+      for (int kk = 0; kk < DH / 16; ++kk) ldsm_x4(q_addr + kk * 32, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+      float o[DH / 8][4];
+#pragma unroll
+      for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+      float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
+#pragma unroll 1
+      for (int kb = 0; kb < nt; ++kb) {
+        const int k0 = 16 * kb;
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t k_addr = smem_u32(sK + (k0 + (lane & 7) + ((lane >> 4) & 1) * 8) * LDS + ((lane >> 3) & 1) * 8);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          uint32_t b00, b01, b10, b11;
+          ldsm_x4(k_addr + kk * 32, b00, b01, b10, b11);
+          mma_bf16_16816(s0, qa[kk], b00, b01);
+          mma_bf16_16816(s1, qa[kk], b10, b11);
+        }
+        const int j0 = k0 + 2 * c4;
+        const bool v0 = j0 < len, v1 = j0 + 1 < len, v2 = j0 + 8 < len, v3 = j0 + 9 < len;
+        float pa[4], pb[4];
+        pa[0] = v0 ? s0[0] * qscale : -INFINITY;
+        pa[1] = v1 ? s0[1] * qscale : -INFINITY;
+        pa[2] = v2 ? s1[0] * qscale : -INFINITY;
+        pa[3] = v3 ? s1[1] * qscale : -INFINITY;
+        pb[0] = v0 ? s0[2] * qscale : -INFINITY;
+        pb[1] = v1 ? s0[3] * qscale : -INFINITY;
+        pb[2] = v2 ? s1[2] * qscale : -INFINITY;
+        pb[3] = v3 ? s1[3] * qscale : -INFINITY;
+        float xa = fmaxf(fmaxf(pa[0], pa[1]), fmaxf(pa[2], pa[3]));
+        float xb = fmaxf(fmaxf(pb[0], pb[1]), fmaxf(pb[2], pb[3]));
+        xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
+        xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
+        xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
+        xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
+        const float na = fmaxf(ma, xa), nb = fmaxf(mb, xb);
+        const float ca = exp2f(ma - na), cb = exp2f(mb - nb);
+        ma = na;
+        mb = nb;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          pa[i] = exp2f(pa[i] - na);
+          pb[i] = exp2f(pb[i] - nb);
+        }
+        la = la * ca + (pa[0] + pa[1] + pa[2] + pa[3]);
+        lb = lb * cb + (pb[0] + pb[1] + pb[2] + pb[3]);
+        if (kb > 0) {
+#pragma unroll
+          for (int n = 0; n < DH / 8; ++n) {
+            o[n][0] *= ca; o[n][1] *= ca;
+            o[n][2] *= cb; o[n][3] *= cb;
+          }
+        }
+        const uint32_t pf[4] = {pack_bf16x2(pa[0], pa[1]), pack_bf16x2(pb[0], pb[1]), pack_bf16x2(pa[2], pa[3]),
+                                pack_bf16x2(pb[2], pb[3])};
+        const uint32_t pl[4] = {pack_bf16x2(pa[0] - bf16lo(pf[0]), pa[1] - bf16hi(pf[0])),
+                                pack_bf16x2(pb[0] - bf16lo(pf[1]), pb[1] - bf16hi(pf[1])),
+                                pack_bf16x2(pa[2] - bf16lo(pf[2]), pa[3] - bf16hi(pf[2])),
+                                pack_bf16x2(pb[2] - bf16lo(pf[3]), pb[3] - bf16hi(pf[3]))};
+        const uint32_t v_addr = smem_u32(sV + (k0 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
+#pragma unroll
+        for (int n = 0; n < DH / 16; ++n) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(v_addr + n * 32, b0, b1, b2, b3);
+          mma_bf16_16816(o[2 * n], pf, b0, b1);
+          mma_bf16_16816(o[2 * n + 1], pf, b2, b3);
+          mma_bf16_16816(o[2 * n], pl, b0, b1);
+          mma_bf16_16816(o[2 * n + 1], pl, b2, b3);
+        }
+      }
+      la += __shfl_xor_sync(0xffffffffu, la, 1);
+      la += __shfl_xor_sync(0xffffffffu, la, 2);
+      lb += __shfl_xor_sync(0xffffffffu, lb, 1);
+      lb += __shfl_xor_sync(0xffffffffu, lb, 2);
+      const float ia = 1.0f / la, ib = 1.0f / lb;
+      const int ra = 16 * qt + g, rb = ra + 8;
+      uint16_t* oa = out + size_t(a + ra) * d + h * DH + 2 * c4;
+#pragma unroll
+      for (int n = 0; n < DH / 8; ++n) {
+        if (ra < len) *reinterpret_cast<uint32_t*>(oa + n * 8) = pack_bf16x2(o[n][0] * ia, o[n][1] * ia);
+        if (rb < len) *reinterpret_cast<uint32_t*>(oa + size_t(8) * d + n * 8) = pack_bf16x2(o[n][2] * ib, o[n][3] * ib);
+      }
+    }
+    __syncthreads();                             // sQ reused by the next query block
+  }
+}
+
 // ------------------------------------------------------------------------ row LayerNorm (d > 384)
 // One warp per row: fp32 v (D values, 16-byte loads) -> mean, biased variance (two passes over the
 // registers), y = (v - mean) rstd gamma + beta -> bf16.
@@ -639,7 +787,7 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_tex
 
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
                              int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
-                             uint16_t* out, cudaStream_t st) {
+                             uint16_t* out, cudaStream_t st, const int32_t* d_long, int32_t n_long) {
   if (n_texts <= 0 || ntok <= 0) return cudaSuccess;
   constexpr int HG = ATT_HEADS_PER_CTA;
   if (heads % HG) return cudaErrorInvalidValue;
@@ -659,7 +807,19 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
     const dim3 grid(unsigned(nwin), unsigned(heads / HG));                                                    \
     attention_text_kernel<DH, HG><<<grid, TA::WARPS * 32, TA::smem(max_len), st>>>(                           \
         qkv, cu, tok0, ntok, win, heads, out, qscale, TA::rows(max_len));                                    \
-    if (max_len > ATT_SHORT) {                                                                               \
+    if (max_len > ATT_SHORT && d_long) {                                                                     \
+      using LA = LongAtt<DH>;                                                                                \
+      static bool lattr_##DH = false;                                                                        \
+      if (!lattr_##DH) {                                                                                     \
+        cudaFuncSetAttribute(attention_long_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                             int(LA::smem(512)));                                                            \
+        lattr_##DH = true;                                                                                   \
+      }                                                                                                      \
+      if (max_len > 512) return cudaErrorInvalidValue;                                                       \
+      if (n_long > 0)                                                                                        \
+        attention_long_kernel<DH><<<dim3(unsigned(n_long), unsigned(heads)), LA::WARPS * 32, LA::smem(max_len), \
+                                    st>>>(qkv, cu, d_long, tok0, heads, out, qscale, LA::kv_rows(max_len));  \
+    } else if (max_len > ATT_SHORT) {   /* list of long texts unknown: scalar per-(text, head) kernel */    \
       constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \
       attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W1), W1 * 32, 0, st>>>(                       \
           qkv, cu, n_texts, tok0, heads, out, qscale, ATT_SHORT + 1);                                        \

@@ -5,6 +5,7 @@
 //                        -> K7 FFN1 GEMM(+bias+GELU) -> K8 FFN2 GEMM(+bias+res+LN) ] -> K9 meanpool+L2
 // Activations are bf16 in HBM between kernels; all math is fp32 inside the kernels.
 #include <cstring>
+#include <vector>
 
 #include "internal.h"
 
@@ -28,6 +29,7 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   if ((e = cudaMalloc(&H, t * s.ffn * 2)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&win, (t / 64 + 2) * sizeof(int32_t))) != cudaSuccess) return e;
   if (!fused_ln(s.d) && (e = cudaMalloc(&V, t * s.d * 4)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&long_idx, (t / 65 + 1) * sizeof(int32_t))) != cudaSuccess) return e;
   cap = cap_tokens;
   return cudaSuccess;
 }
@@ -41,6 +43,8 @@ void Workspace::release() {
   win = nullptr;
   if (V) cudaFree(V);
   V = nullptr;
+  if (long_idx) cudaFree(long_idx);
+  long_idx = nullptr;
   cap = 0;
 }
 
@@ -206,13 +210,17 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   const bool P = prof && prof->on;
   double sum_l2 = 0;
   int32_t max_len = s_.max_pos;     // unknown -> assume long texts may be present
+  std::vector<int32_t> long_texts;    // chunk-relative indices of texts longer than 64 tokens
   if (host_cu) {
     max_len = 0;
     for (int64_t i = s0; i < s1; ++i) {
       const int32_t li = host_cu[i + 1] - host_cu[i];
       max_len = li > max_len ? li : max_len;
       sum_l2 += double(li) * double(li);
+      if (li > 64) long_texts.push_back(int32_t(i - s0));
     }
+    if (!long_texts.empty())   // pageable source: staged by the runtime before the call returns
+      SURGE_TRY(cudaMemcpyAsync(ws.long_idx, long_texts.data(), long_texts.size() * 4, cudaMemcpyHostToDevice, st));
   }
   const double M = ntok, D = d, F = f;
   cudaEvent_t ev = nullptr;
@@ -234,7 +242,8 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
     // K5: O = attention(QKV) per text
     if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st));
+    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st,
+                               host_cu ? ws.long_idx : nullptr, int32_t(long_texts.size())));
     if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
     // K6: X1 = LN(O Wo^T + bo + X)
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;

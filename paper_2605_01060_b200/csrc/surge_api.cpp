@@ -1158,12 +1158,20 @@ surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int6
   int32_t max_len = 0;
   for (int64_t i = 0; i < n_texts; ++i) max_len = std::max(max_len, hcu[i + 1] - hcu[i]);
   const int32_t ntok = hcu[n_texts] - hcu[0];
+  std::vector<int32_t> lng;
+  for (int64_t i = 0; i < n_texts; ++i)
+    if (hcu[i + 1] - hcu[i] > 64) lng.push_back(int32_t(i));
   int32_t* win = nullptr;
+  int32_t* dl = nullptr;
   if (cudaMalloc(&win, (size_t(ntok) / 64 + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
-  cudaError_t e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, win, false, heads,
-                                          head_dim, d_out, st);
+  if (cudaMalloc(&dl, (lng.size() + 1) * 4) != cudaSuccess) { cudaFree(win); return SURGE_E_OOM; }
+  cudaError_t e = cudaMemcpy(dl, lng.data(), lng.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, win, false, heads, head_dim, d_out, st,
+                                dl, int32_t(lng.size()));
   cudaError_t e2 = cudaStreamSynchronize(st);
   cudaFree(win);
+  cudaFree(dl);
   return (e == cudaSuccess && e2 == cudaSuccess) ? SURGE_OK : SURGE_E_CUDA;
 }
 

@@ -291,7 +291,8 @@ surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const
 /*
  * Per-kernel-class device timing (CUDA events around every launch, on the launching stream).
  * Enable before a timed region, read after synchronising.  Classes: 0 embed_ln, 1 gemm_qkv,
- * 2 attention, 3 gemm_out_ln, 4 gemm_ffn1_gelu, 5 gemm_ffn2_ln, 6 meanpool_l2, 7 pack.
+ * 2 attention, 3 gemm_out_ln, 4 gemm_ffn1_gelu, 5 gemm_ffn2_ln, 6 meanpool_l2, 7 pack,
+ * 8 gemm_qkv_attn (K4 + K5 fused).
  *   flops/bytes: ALGORITHMIC work of the launches (2*M*N*K for GEMMs; 4*d*sum(l^2) attention
  *   flops; minimal HBM bytes in+out for every class), summed over launches.
  */
@@ -302,6 +303,17 @@ typedef struct {
   double flops;
   double bytes;
 } surge_kernel_profile;
+
+/*
+ * Execution options (not part of the paper's method; they select between equivalent kernel paths).
+ *   SURGE_OPT_ATT_FUSED (default 1): 1 = K4 QKV GEMM and K5 attention run as one kernel
+ *     (attention in the GEMM epilogue, QKV never written to HBM) for chunks whose texts are all
+ *     <= 128 tokens; 0 = separate K4 GEMM + K5 attention kernels everywhere.  Both paths compute
+ *     bit-identical embeddings (shared attention arithmetic).
+ * Call only while the handle is idle (no SuperBatch in flight).  Unknown option -> SURGE_E_INVALID_ARG.
+ */
+#define SURGE_OPT_ATT_FUSED 1
+surge_status surge_set_option(surge_handle h, int32_t option, int64_t value);
 
 surge_status surge_profile_enable(surge_handle h, int32_t on);   /* on: clears counters */
 surge_status surge_profile_read(surge_handle h, surge_kernel_profile* out, int32_t capacity,

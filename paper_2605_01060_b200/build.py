@@ -18,8 +18,8 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OUT = os.path.join(PKG, "libsurge.so")
-BUILD = os.path.join(PKG, "_build")
+OUT = os.environ.get("SURGE_BUILD_OUT") or os.path.join(PKG, "libsurge.so")   # variants: scripts/ experiments
+BUILD = os.environ.get("SURGE_BUILD_DIR") or os.path.join(PKG, "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-Wall,-Wno-unused-function",

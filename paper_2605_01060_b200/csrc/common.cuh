@@ -286,8 +286,12 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t smem_addr, uint32_t ran
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Relaxed remote arrive: used only to hand a TMEM accumulator back to the leader's MMA issuer, so
+// the caller's tcgen05.fence::before_thread_sync orders its tcgen05.ld; no memory needs releasing.
+// (.release.cluster would emit MEMBAR.ALL.GPU, which waits for every outstanding global store of
+// the epilogue -- measured as the top stall of the attention epilogue.)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem, completion bytes counted on the (leader's) barrier `bar_cluster`.
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* desc, uint32_t bar_cluster, int32_t c0,

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdio>
 
+#include "attn_tile.cuh"
 #include "common.cuh"
 #include "internal.h"
 
@@ -43,7 +44,11 @@ struct TileCfg {
   // Epilogue warps: SPLIT per TMEM lane quadrant, each owning BN / SPLIT columns.  The GELU
   // epilogue is issue-bound, so it gets three warps per quadrant (bias then comes from smem to
   // keep registers <= 128 at 512 threads); the others two.
-  static constexpr int SPLIT = EPI != EPI_BIAS_GELU ? 2 : BN % 128 == 0 ? 4 : BN % 96 == 0 ? 3 : 2;
+  // The attention epilogue (EPI_QKV_ATTN) runs 12 warps: the (text, head) units of a tile are its
+  // critical path.
+  static constexpr bool ATT = EPI == EPI_QKV_ATTN;
+  static constexpr int SPLIT = ATT ? (BN % 96 == 0 ? 3 : 2)
+                               : EPI != EPI_BIAS_GELU ? 2 : BN % 128 == 0 ? 4 : BN % 96 == 0 ? 3 : 2;
   static constexpr int EPI_WARPS = 4 * SPLIT;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr bool BIAS_SMEM = EPI == EPI_BIAS_GELU && SPLIT > 2;
@@ -51,8 +56,13 @@ struct TileCfg {
   static constexpr int STATS_BYTES =                              // LN: stats + bias/gamma/beta, 1 KB aligned
       EPI == EPI_BIAS_LN ? ((2 * 2 * BM * 4 * 4 + 3 * BN * 4 + 1023) / 1024) * 1024 : 0;
   static constexpr int STG_BUFS = 1;                              // per-warp output staging buffers
-  static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
-  static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES + STG_BYTES;
+  static constexpr int STG_BYTES = ATT ? 0 : EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
+  // EPI_QKV_ATTN: the tile's Q | K | V (bf16) staged for attention, 128 rows + 16 zero rows read
+  // past the last text by a query tile / key block, 16-byte row skew.
+  static constexpr int ATT_ROWS = BM + 16;
+  static constexpr int ATT_LDS = BN + 8;
+  static constexpr int ATT_BYTES = ATT ? ((ATT_ROWS * ATT_LDS * 2 + 2 * ATT_REC_INTS * 4 + 1023) / 1024) * 1024 : 0;
+  static constexpr int FIXED_BYTES = 1024 /*align*/ + HEAD_BYTES + STATS_BYTES + STG_BYTES + ATT_BYTES;
   __host__ __device__ static int bias_bytes(int N) { return BIAS_SMEM ? ((N * 4 + 1023) / 1024) * 1024 : 0; }
   static constexpr int MAX_SMEM = 227 * 1024;
   static constexpr int MAX_STAGES = 8;
@@ -83,14 +93,24 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // n_tiles, ...; the grid is a multiple of n_tiles.
 // PAIR (streaming only): the unit is the cluster (blockIdx.x / 2) and M tiles are 256 rows; CTA
 // rank r of the pair owns rows [256 t + 128 r, +128).
+// Text-aligned M tiles (EPI_QKV_ATTN): tile i is described by record i (internal.h ATT_REC_INTS
+// layout; word 0 = its first row); in PAIR mode unit t is the tile pair (2t, 2t + 1).
+struct AttTiles {
+  const int32_t* rec;     // nullptr: regular M tiling
+  int32_t n;              // tiles (even)
+  float qscale;
+};
+
 template <bool WS, bool PAIR = false>
 struct Sched {
   int t0, dt, tend, n_tiles, slice, rank;
-  __device__ Sched(int M, int n_tiles_) : n_tiles(n_tiles_) {
+  AttTiles at;
+  __device__ Sched(int M, int n_tiles_, const AttTiles& at_) : n_tiles(n_tiles_), at(at_) {
     rank = PAIR ? int(blockIdx.x & 1) : 0;
     const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
     const int units = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
-    const int m_tiles = (M + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
+    const int m_tiles = at.rec ? (PAIR ? at.n / 2 : at.n)
+                                 : (M + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
     if (WS) {
       slice = unit % n_tiles;
       t0 = unit / n_tiles;
@@ -103,7 +123,13 @@ struct Sched {
       tend = m_tiles * n_tiles;
     }
   }
-  __device__ int m0(int t) const { return (WS ? t : t / n_tiles) * (PAIR ? 2 * BM : BM) + rank * BM; }
+  __device__ int mt(int t) const { return WS ? t : t / n_tiles; }
+  // text-aligned tile index of this CTA in unit t
+  __device__ int att_tile(int t) const { return PAIR ? 2 * mt(t) + rank : mt(t); }
+  __device__ int m0(int t) const {
+    if (at.rec) return at.rec[size_t(att_tile(t)) * ATT_REC_INTS];
+    return mt(t) * (PAIR ? 2 * BM : BM) + rank * BM;
+  }
   __device__ int n0(int t) const { return (WS ? slice : t % n_tiles); }
 };
 
@@ -114,13 +140,24 @@ struct Sched {
 //   warps 4..11   epilogue: warp w reads TMEM lane quadrant w % 4, column half (w - 4) / 4;
 //                 the accumulator buffer is released as soon as it is drained, so with ACC = 2 the
 //                 epilogue of tile i overlaps the mainloop of tile i + 1.
-template <int BN, int EPI, bool WS, bool PAIR>
+#ifdef ATT_TRACE
+#define ATT_TR(i)                                        \
+  do {                                                   \
+    const long long _c = clock64();                      \
+    if (i > 0) tr_acc[i - 1] += _c - tr_last;            \
+    tr_last = _c;                                        \
+  } while (0)
+#else
+#define ATT_TR(i) do {} while (0)
+#endif
+
+template <int BN, int EPI, bool WS, bool PAIR, int DH = 0>
 __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
-                   float eps, int stages) {
+                   float eps, int stages, const AttTiles att) {
   using T = TileCfg<BN, EPI, PAIR>;
   constexpr int ACC = T::ACC;
   extern __shared__ uint8_t smem_raw[];
@@ -139,13 +176,15 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
   float* s_beta = s_gamma + BN;
   uint8_t* sStg = smem + T::HEAD_BYTES + T::STATS_BYTES;  // [epi warp][STG_BUFS][2 KB] (1 KB aligned)
   float* s_bias_all = reinterpret_cast<float*>(sStg + T::STG_BYTES);   // BIAS_SMEM: bias[0..N)
-  uint8_t* sB = sStg + T::STG_BYTES + T::bias_bytes(N);  // WS: resident [K/64][BN x 128 B]; else ring
+  uint16_t* sAtt = reinterpret_cast<uint16_t*>(sStg + T::STG_BYTES + T::bias_bytes(N));   // ATT: [ATT_ROWS][ATT_LDS]
+  int32_t* s_rec = reinterpret_cast<int32_t*>(sAtt + T::ATT_ROWS * T::ATT_LDS);   // ATT: [2][ATT_REC_INTS] records
+  uint8_t* sB = sStg + T::STG_BYTES + T::bias_bytes(N) + T::ATT_BYTES;  // WS: resident [K/64][BN x 128 B]; else ring
   uint8_t* sA = sB + T::b_res_bytes(K, WS);             // [stages] x 16 KB
   uint8_t* sBs = sA + stages * A_STAGE_BYTES;           // streaming B ring [stages] x B_STAGE_BYTES
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_kb = K / BK;
-  const Sched<WS, PAIR> sc(M, N / BN);
+  const Sched<WS, PAIR> sc(M, N / BN, att);
   const bool leader = sc.rank == 0;              // PAIR: the CTA that issues the MMAs
 
   if (warp == 0 && lane == 0) {
@@ -309,6 +348,17 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       for (int i = threadIdx.x - 128; i < N; i += T::EPI_WARPS * 32) s_bias_all[i] = bias[i];
       named_bar_sync(5, T::EPI_WARPS * 32);
     }
+    if constexpr (T::ATT) {                   // zero rows [BM, BM + 16): read past the tile's last text
+      for (int i = threadIdx.x - 128; i < 16 * T::ATT_LDS / 8; i += T::EPI_WARPS * 32)
+        reinterpret_cast<uint4*>(sAtt + BM * T::ATT_LDS)[i] = make_uint4(0, 0, 0, 0);
+      const int e = threadIdx.x - 128;          // first tile's record -> slot 0
+      if (e < ATT_REC_INTS && sc.t0 < sc.tend) s_rec[e] = att.rec[size_t(sc.att_tile(sc.t0)) * ATT_REC_INTS + e];
+      named_bar_sync(5, T::EPI_WARPS * 32);
+    }
+#ifdef ATT_TRACE
+    long long tr_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tr_last = 0;
+    int tr_tiles = 0;
+#endif
     int stg = 0;                              // staged output boxes issued by this warp
     const int q = warp & 3;                   // TMEM lane quadrant this warp may access
     const int hh = (warp - 4) >> 2;           // column part (0 .. SPLIT-1)
@@ -340,7 +390,108 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
         ++stg;
       };
       constexpr int NSTEP = T::HALF / 32;     // 32-column steps per warp
-      if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
+      if constexpr (T::ATT) {
+        // ---- QKV + attention (K4 + K5).  Slice columns: [Q | K | V] of HG heads, DH each.
+        // phase 1: acc + bias -> bf16 (the values the separate path stores as QKV) -> sAtt, then the
+        //          accumulator is released (the next tile's MMAs overlap phases 2-3);
+        // phase 2: (text, head) units of the tile's texts over the epilogue warps, attn_query_tile
+        //          (shared with attention_text_kernel: same arithmetic), O over the Q columns;
+        // phase 3: O rows of the tile's texts -> global (16-byte stores, 128 B per row).
+        constexpr int HG = BN / (3 * DH);
+        constexpr int LDS = T::ATT_LDS;
+        const int e = threadIdx.x - 128;
+        const int slot = it & 1;
+        // prefetch the next tile's record (registers; stored to the other slot after this tile)
+        const bool has_next = t + sc.dt < sc.tend;
+        int32_t nxt = 0;
+        if (e < ATT_REC_INTS && has_next) nxt = att.rec[size_t(sc.att_tile(t + sc.dt)) * ATT_REC_INTS + e];
+        const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c_lo);
+        float4 b4[2][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) b4[0][i] = __ldg(bp + i);
+        uint32_t r[2][32];
+        ATT_TR(0);
+        mbar_wait(&tfull[acc], aph);
+        ATT_TR(1);
+        tc_fence_after();
+        tmem_ld32(taddr + c_lo, r[0]);
+        uint16_t* srow = sAtt + (q * 32 + lane) * LDS + c_lo;
+#pragma unroll
+        for (int k = 0; k < NSTEP; ++k) {
+          const int cur = k & 1;
+          tmem_ld_wait_regs(r[cur]);
+          if (k + 1 < NSTEP) {
+            tmem_ld32(taddr + c_lo + 32 * (k + 1), r[cur ^ 1]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) b4[cur ^ 1][i] = __ldg(bp + 8 * (k + 1) + i);
+          }
+          uint32_t p[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 bb = b4[cur][i];
+            const f32x2 v01 = fadd2(f2(__uint_as_float(r[cur][4 * i]), __uint_as_float(r[cur][4 * i + 1])), f2(bb.x, bb.y));
+            const f32x2 v23 = fadd2(f2(__uint_as_float(r[cur][4 * i + 2]), __uint_as_float(r[cur][4 * i + 3])), f2(bb.z, bb.w));
+            p[2 * i] = pack_bf16x2(f2lo(v01), f2hi(v01));
+            p[2 * i + 1] = pack_bf16x2(f2lo(v23), f2hi(v23));
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(srow + 32 * k + 8 * i) = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          else mbar_arrive(&tempty[acc]);
+        }
+        ATT_TR(2);
+        named_bar_sync(1, T::EPI_WARPS * 32);   // the tile's Q | K | V staged (and its record visible)
+        ATT_TR(3);
+        const int32_t* R = s_rec + slot * ATT_REC_INTS;
+        const int row0 = R[0], nrows = R[1], ntexts = R[2], nunits = R[3];
+        const uint8_t* tstart = reinterpret_cast<const uint8_t*>(R + 4);
+        const uint16_t* units = reinterpret_cast<const uint16_t*>(R + 36);
+        constexpr int NHU = DH == 16 ? 2 : 1;   // heads per unit (internal.h att_unit_heads)
+        constexpr int W = T::EPI_WARPS;
+        const int w = warp - 4;
+#pragma unroll 1
+        for (int k = 0;; ++k) {                 // snake order over the cost-sorted units
+#ifdef ATT_SKIP_P2
+          break;                                // timing experiment only (wrong results)
+#endif
+          const int u = k * W + ((k & 1) ? W - 1 - w : w);
+          if (u >= nunits) break;
+          const int un = units[u];
+          const int j = un & 0xff, qt = (un >> 8) & 7, h0 = (un >> 11) * NHU;
+          const int ta = tstart[j];
+          const int len = (j + 1 < ntexts ? int(tstart[j + 1]) : nrows) - ta;
+          const int nt = (len + 15) >> 4;
+          uint16_t* sQt = sAtt + (ta + 16 * qt) * LDS + h0 * DH;
+          float o[NHU][DH / 8][4];
+          float ia[NHU], ib[NHU];
+          attn_query_tile<DH, LDS, NHU>(sQt, sAtt + ta * LDS + (HG + h0) * DH, sAtt + ta * LDS + (2 * HG + h0) * DH,
+                                        len, nt, att.qscale, lane, o, ia, ib);
+          __syncwarp();   // every lane has read its Q fragments before O overwrites the tile
+          attn_store_tile<DH, NHU>(sQt, LDS, qt, len, lane, o, ia, ib);
+        }
+        ATT_TR(4);
+        named_bar_sync(1, T::EPI_WARPS * 32);   // O complete
+        ATT_TR(5);
+        {
+          constexpr int CH = HG * DH / 8;         // 16-byte chunks of one O row
+          const int dout = N / 3;
+          uint16_t* orow0 = C + size_t(row0) * dout + n0 / 3;
+          for (int i = e; i < nrows * CH; i += T::EPI_WARPS * 32) {
+            const int rr = i / CH, cc = i - rr * CH;
+            *reinterpret_cast<uint4*>(orow0 + size_t(rr) * dout + cc * 8) =
+                *reinterpret_cast<const uint4*>(sAtt + rr * LDS + cc * 8);
+          }
+        }
+        if (e < ATT_REC_INTS && has_next) s_rec[(slot ^ 1) * ATT_REC_INTS + e] = nxt;
+        ATT_TR(6);
+        named_bar_sync(1, T::EPI_WARPS * 32);   // sAtt free for the next tile
+        ATT_TR(7);
+      } else if constexpr (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
         // Software-pipelined over 32-column steps: the TMEM load and bias slice of step k+1 are in
         // flight while step k is computed and stored (tcgen05.wait::ld then covers only step k+1).
         const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c_lo);
@@ -487,14 +638,26 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
           stage_store(p, c);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));   // leader's barrier
-        else mbar_arrive(&tempty[acc]);
+      if constexpr (!T::ATT) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));   // leader's barrier
+          else mbar_arrive(&tempty[acc]);
+        }
       }
     }
     if (lane == 0) bulk_wait_all();           // output stores complete before the CTA retires
+#ifdef ATT_TRACE
+    if constexpr (T::ATT) {
+      tr_tiles = it;
+      if (lane == 0 && blockIdx.x < 1)
+        printf("ATT_TRACE cta %d warp %d tiles %d | wait %lld p1 %lld bar1 %lld p2 %lld bar2 %lld p3 %lld bar3 %lld (cycles/tile)\n",
+               int(blockIdx.x), warp, tr_tiles, tr_acc[0] / max(tr_tiles, 1), tr_acc[1] / max(tr_tiles, 1),
+               tr_acc[2] / max(tr_tiles, 1), tr_acc[3] / max(tr_tiles, 1), tr_acc[4] / max(tr_tiles, 1),
+               tr_acc[5] / max(tr_tiles, 1), tr_acc[6] / max(tr_tiles, 1));
+    }
+#endif
   }
   tc_fence_before();
   if constexpr (PAIR) cluster_sync();            // the peer may still read our smem / signal us
@@ -519,10 +682,10 @@ int num_sms() {
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 
-template <int BN, int EPI, bool WS, bool PAIR = false>
+template <int BN, int EPI, bool WS, bool PAIR = false, int DH = 0>
 cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   using T = TileCfg<BN, EPI, PAIR>;
-  auto kern = gemm_tc_kernel<BN, EPI, WS, PAIR>;
+  auto kern = gemm_tc_kernel<BN, EPI, WS, PAIR, DH>;
   const int smem = T::smem_bytes(g.K, WS, g.N);
   const int stages = T::stages(g.K, WS, g.N);
   if (stages < 2 || smem > T::MAX_SMEM) return cudaErrorInvalidValue;
@@ -532,17 +695,19 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = T::MAX_SMEM;
   }
-  const int64_t m_tiles = (g.M + BM - 1) / BM, n_tiles = g.N / BN;
+  const bool att = EPI == EPI_QKV_ATTN;
+  const int64_t m_tiles = att ? g.n_att_tiles : (g.M + BM - 1) / BM, n_tiles = g.N / BN;
+  const AttTiles at{att ? g.att_rec : nullptr, g.n_att_tiles, g.qscale};
   int grid;
   if (WS && PAIR) {
-    const int64_t m2 = (g.M + 2 * BM - 1) / (2 * BM);
+    const int64_t m2 = att ? g.n_att_tiles / 2 : (g.M + 2 * BM - 1) / (2 * BM);
     const int64_t per = std::min<int64_t>(std::max<int64_t>(num_sms() / 2 / n_tiles, 1), m2);
     grid = int(2 * per * n_tiles);
   } else if (WS) {
     const int64_t per = std::min<int64_t>(std::max<int64_t>(num_sms() / n_tiles, 1), m_tiles);
     grid = int(per * n_tiles);
   } else if (PAIR) {
-    const int64_t m2 = (g.M + 2 * BM - 1) / (2 * BM);
+    const int64_t m2 = att ? g.n_att_tiles / 2 : (g.M + 2 * BM - 1) / (2 * BM);
     grid = 2 * int(std::min<int64_t>(m2 * n_tiles, num_sms() / 2));
   } else {
     grid = int(std::min<int64_t>(m_tiles * n_tiles, num_sms()));
@@ -562,10 +727,10 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
-                              g.beta, g.C, g.eps, stages);
+                              g.beta, g.C, g.eps, stages, at);
   }
   kern<<<grid, T::THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K,
-                                         g.bias, g.res, g.gamma, g.beta, g.C, g.eps, stages);
+                                         g.bias, g.res, g.gamma, g.beta, g.C, g.eps, stages, at);
   return cudaGetLastError();
 }
 
@@ -574,7 +739,8 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
 template <int BN, int EPI, bool PAIR = false>
 bool use_ws(const GemmArgs& g) {
   using T = TileCfg<BN, EPI, PAIR>;
-  const int64_t m_units = PAIR ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM - 1) / BM;
+  const int64_t m_units = g.epi == EPI_QKV_ATTN ? (PAIR ? g.n_att_tiles / 2 : g.n_att_tiles)
+                         : PAIR ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM - 1) / BM;
   const int units = PAIR ? num_sms() / 2 : num_sms();
   return g.epi != EPI_BIAS_LN && g.epi != EPI_BIAS_RES && T::stages(g.K, true, g.N) >= 3 &&
          m_units >= units / (g.N / BN);
@@ -669,12 +835,30 @@ int gemm_bn_for(int N, int K, int epi) {
 }
 
 uint32_t gemm_b_box_rows(int N, int K, int epi) {
+  if (epi == EPI_QKV_ATTN) return ATT_SLICE / 2;   // CTA pairs: half of each 192-row slice
   const int BN = gemm_bn_for(N, K, epi);
   const int mma_n = BN <= 256 ? BN : BN / 2;
   return uint32_t(gemm_use_pair(N, K, epi) ? mma_n / 2 : mma_n);
 }
 
+template <int DH>
+cudaError_t launch_qkv_att(const GemmArgs& g, cudaStream_t st) {
+  if (use_ws<ATT_SLICE, EPI_QKV_ATTN, true>(g)) return launch_gemm_t<ATT_SLICE, EPI_QKV_ATTN, true, true, DH>(g, st);
+  return launch_gemm_t<ATT_SLICE, EPI_QKV_ATTN, false, true, DH>(g, st);
+}
+
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
+  if (g.epi == EPI_QKV_ATTN) {
+    if (g.N % ATT_SLICE != 0 || g.K % BK != 0 || g.K <= 0 || g.M <= 0 || !g.att_rec || g.n_att_tiles <= 0 ||
+        (g.n_att_tiles & 1))
+      return cudaErrorInvalidValue;
+    switch (g.head_dim) {
+      case 16: return launch_qkv_att<16>(g, st);
+      case 32: return launch_qkv_att<32>(g, st);
+      case 64: return launch_qkv_att<64>(g, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   const int BN = gemm_bn_for(g.N, g.K, g.epi);
   if (BN == 0 || g.K % BK != 0 || g.K <= 0 || g.M <= 0) return cudaErrorInvalidValue;
   switch (g.epi) {

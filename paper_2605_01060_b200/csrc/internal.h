@@ -12,7 +12,11 @@ namespace surge {
 
 // EPI_BIAS_RES: fp32 C = A B^T + b + R (the pre-LayerNorm row, for hidden sizes whose full row
 // does not fit one CTA's TMEM; launch_layernorm then normalises it).  C is float* in that case.
-enum Epilogue : int { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_BIAS_LN = 2, EPI_BIAS_RES = 3 };
+// EPI_QKV_ATTN: the QKV projection with K5 attention in the epilogue (DESIGN.md §6 "QKV +
+// attention"): A row tiles are text-aligned (att_tiles), B = W_qkv with rows permuted so that each
+// 192-row slice holds [Q | K | V] of 192 / (3 d_h) whole heads (qkv_att_perm), and the CTA writes
+// the attention output O [M x N/3] instead of QKV.
+enum Epilogue : int { EPI_BIAS = 0, EPI_BIAS_GELU = 1, EPI_BIAS_LN = 2, EPI_BIAS_RES = 3, EPI_QKV_ATTN = 4 };
 
 struct GemmArgs {
   const CUtensorMap* tmA;   // A [M x K]
@@ -25,9 +29,41 @@ struct GemmArgs {
   const uint16_t* res;      // [M x N] (EPI_BIAS_LN)
   const float* gamma;
   const float* beta;
-  uint16_t* C;              // [M x N]
+  uint16_t* C;              // [M x N]  (EPI_QKV_ATTN: O [M x N/3])
   float eps;
+  // EPI_QKV_ATTN only
+  const int32_t* att_rec = nullptr;     // [n_att_tiles] tile records (AttRec layout, launch_att_records)
+  int32_t n_att_tiles = 0;              // even (a CTA pair takes tiles 2u, 2u + 1)
+  int32_t head_dim = 0;
+  float qscale = 0.f;                   // log2(e) / sqrt(d_h)
 };
+
+// Text-aligned 128-row tiles for EPI_QKV_ATTN over texts [s0, s1) (host cu, absolute): greedy,
+// each tile = the longest run of whole texts with <= 128 tokens; padded with an empty tile to an
+// even count.  Appends n_tiles + 1 entries (text indices) to out; returns n_tiles, or -1 when a
+// text is longer than 128 tokens (the chunk then takes the separate-attention path).
+int32_t att_tiles_for(const int32_t* host_cu, int64_t s0, int64_t s1, std::vector<int32_t>& out);
+constexpr int ATT_TILE_ROWS = 128;
+// Tile record (int32 words): [0] row0 (chunk-relative first row), [1] nrows, [2] ntexts,
+// [3] nunits; bytes [16, 144): start row of each text within the tile (uint8); bytes [144, 688):
+// attention work units, uint16 (text | qt << 8 | head group << 11), qt = 16-row query tile of the
+// text, sorted by cost (key blocks = ceil(len / 16)) descending.  The epilogue warps take the
+// units in snake order (warp w: w, 2W-1-w, 2W+w, ...), an LPT-like balance of the tile's work.
+constexpr int ATT_REC_INTS = 172;
+constexpr int ATT_REC_MAX_UNITS = 272;   // (128 / 16 + ntexts <= 136 query tiles) x <= 2 head groups
+// heads per work unit: 1 (head groups = heads of the slice) except d_h = 16 (4 heads per slice) -> 2
+inline int att_unit_heads(int dh) { return dh == 16 ? 2 : 1; }
+// Upper bound on the tiles of a chunk of ntok tokens (two consecutive greedy tiles hold > 128 rows).
+inline int64_t att_max_tiles(int64_t ntok) { return ntok / 64 + 4; }
+// Device: records of tiles [0, n_tiles) from the first-text table (tiles, n_tiles + 1 entries).
+cudaError_t launch_att_records(const int32_t* tiles, int32_t n_tiles, const int32_t* cu, int32_t tok0,
+                               int32_t n_groups, int32_t* rec, cudaStream_t st);
+constexpr int ATT_SLICE = 192;   // columns of one W_qkv slice in the fused kernel
+// The fused QKV + attention path applies to head sizes whose heads tile a 192-column slice.
+inline bool qkv_att_supported(int d, int heads) {
+  const int dh = d / heads;
+  return (dh == 16 || dh == 32 || dh == 64) && (3 * d) % ATT_SLICE == 0 && ATT_SLICE % (3 * dh) == 0;
+}
 
 cudaError_t init_tma_encoder();
 cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
@@ -70,7 +106,7 @@ cudaError_t launch_bf16_to_f32(const uint16_t* in, float* out, int64_t n, cudaSt
 // --------------------------------------------------------------------- per-kernel-class timing
 enum KernelKind : int {
   KK_EMBED = 0, KK_QKV = 1, KK_ATTN = 2, KK_OUT_LN = 3, KK_FFN1 = 4, KK_FFN2 = 5, KK_POOL = 6, KK_PACK = 7,
-  KK_COUNT = 8
+  KK_QKV_ATTN = 8, KK_COUNT = 9
 };
 
 // Records a CUDA event pair around launches of each kind (only when enabled).  Not thread-safe:
@@ -104,6 +140,9 @@ struct LayerW {
   uint16_t *wqkv, *wo, *w1, *w2;      // bf16 [3d x d], [d x d], [ff x d], [d x ff]
   float *bqkv, *bo, *ln1_g, *ln1_b, *b1, *b2, *ln2_g, *ln2_b;
   CUtensorMap tm_wqkv, tm_wo, tm_w1, tm_w2;
+  uint16_t* wqkv_att = nullptr;       // W_qkv rows permuted into head-complete 192-row slices
+  float* bqkv_att = nullptr;
+  CUtensorMap tm_wqkv_att;
 };
 
 // Activation workspace for one chunk of <= cap tokens (bf16): X, QKV, O, X1, H.
@@ -113,6 +152,8 @@ struct Workspace {
   float* V = nullptr;       // fp32 pre-LayerNorm rows (hidden sizes without the fused LN epilogue)
   int32_t* long_idx = nullptr;   // texts of the chunk longer than 64 tokens, cap/65 + 1 entries
   int32_t* win = nullptr;   // attention: first text of each 64-token window, cap/64 + 2 entries
+  int32_t* tiles = nullptr; // EPI_QKV_ATTN first text of each tile of the current chunk
+  int32_t* att_rec = nullptr;   // EPI_QKV_ATTN tile records of the current chunk
   cudaError_t alloc(const ModelShape& s, int64_t cap_tokens);
   void release();
   ~Workspace() { release(); }
@@ -141,9 +182,13 @@ class DeviceModel {
   const uint16_t* type() const { return type_; }
   const float* emb_g() const { return emb_g_; }
   const float* emb_b() const { return emb_b_; }
+  // fused QKV + attention kernel on/off (on by default; off = separate K4 GEMM + K5 kernels)
+  void set_att_fused(bool on) { att_fused_ = on; }
+  bool att_fused() const { return att_fused_; }
 
  private:
   ModelShape s_{};
+  bool att_fused_ = true;
   std::vector<void*> allocs_;
   uint16_t *word_ = nullptr, *pos_ = nullptr, *type_ = nullptr;
   float *emb_g_ = nullptr, *emb_b_ = nullptr;

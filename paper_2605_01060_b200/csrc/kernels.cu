@@ -4,6 +4,7 @@
 //   K5 varlen_attention: per (text, head) softmax(Q K^T / sqrt(d_h)) V over the text's own tokens
 //   K9 meanpool_l2     : e_s = v / max(||v||, 1e-12), v = mean of the text's rows
 // All are HBM/L2-bound; accesses are 8- or 16-byte vectors, fp32 math, bf16 storage.
+#include "attn_tile.cuh"
 #include "common.cuh"
 #include "internal.h"
 
@@ -301,31 +302,6 @@ __global__ void window_index_kernel(const int32_t* __restrict__ cu, int64_t n, i
   for (int32_t w = w_lo; w <= w_hi; ++w) win[w] = int32_t(s);
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-// D (16x8 fp32) += A (16x16 bf16, row) * B (16x8 bf16, col)
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
 // Block-diagonal varlen attention for texts of <= ATT_SHORT tokens, text-tiled.  A CTA owns the
 // texts that START in one 64-token window (their rows [R0, R1) span at most 64 + 63 tokens, so
 // no halo is loaded) and a group of HG heads; Q/K/V of those rows are staged in padded shared
@@ -394,110 +370,21 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
-  const int g = lane >> 2, c4 = lane & 3;
   // work units (text, head), round-robin over the warps
 #pragma unroll 1
-  for (int32_t u = warp; u < (s_b - s_a) * HG; u += A::WARPS) {
-    const int32_t txt = s_a + u / HG;
-    const int h = u % HG;
+  for (int32_t u = warp; u < s_b - s_a; u += A::WARPS) {   // work unit: one text, all HG heads
+    const int32_t txt = s_a + u;
     const int32_t ta = cu[txt] - tok0 - R0;      // smem row of the text's first token
     const int32_t len = cu[txt + 1] - cu[txt];
     const int nt = (len + 15) >> 4;              // query tiles = key blocks
-    {
 #pragma unroll 1
-      for (int qt = 0; qt < nt; ++qt) {
-        const int q0 = ta + 16 * qt;
-        uint32_t qa[DH / 16][4];
-        const uint32_t q_addr =
-            smem_u32(sQ + (q0 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + h * DH + (lane >> 4) * 8);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) ldsm_x4(q_addr + kk * 32, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
-        float o[DH / 8][4];
-#pragma unroll
-        for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-        float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
-#pragma unroll 1
-        for (int kb = 0; kb < nt; ++kb) {
-          const int k0 = ta + 16 * kb;
-          float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-          const uint32_t k_addr =
-              smem_u32(sK + (k0 + (lane & 7) + ((lane >> 4) & 1) * 8) * LDS + h * DH + ((lane >> 3) & 1) * 8);
-#pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk) {
-            uint32_t b00, b01, b10, b11;
-            ldsm_x4(k_addr + kk * 32, b00, b01, b10, b11);
-            mma_bf16_16816(s0, qa[kk], b00, b01);
-            mma_bf16_16816(s1, qa[kk], b10, b11);
-          }
-          // key index within the text: 16 kb + 2 c4 + {0, 1} (s0), + 8 (s1); valid iff < len
-          const int j0 = 16 * kb + 2 * c4;
-          const bool v0 = j0 < len, v1 = j0 + 1 < len, v2 = j0 + 8 < len, v3 = j0 + 9 < len;
-          float pa[4], pb[4];
-          pa[0] = v0 ? s0[0] * qscale : -INFINITY;
-          pa[1] = v1 ? s0[1] * qscale : -INFINITY;
-          pa[2] = v2 ? s1[0] * qscale : -INFINITY;
-          pa[3] = v3 ? s1[1] * qscale : -INFINITY;
-          pb[0] = v0 ? s0[2] * qscale : -INFINITY;
-          pb[1] = v1 ? s0[3] * qscale : -INFINITY;
-          pb[2] = v2 ? s1[2] * qscale : -INFINITY;
-          pb[3] = v3 ? s1[3] * qscale : -INFINITY;
-          float xa = fmaxf(fmaxf(pa[0], pa[1]), fmaxf(pa[2], pa[3]));
-          float xb = fmaxf(fmaxf(pb[0], pb[1]), fmaxf(pb[2], pb[3]));
-          xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
-          xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
-          xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
-          xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
-          const float na = fmaxf(ma, xa), nb = fmaxf(mb, xb);   // finite: key 0 of block 0 is valid
-          const float ca = exp2f(ma - na), cb = exp2f(mb - nb);
-          ma = na;
-          mb = nb;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            pa[i] = exp2f(pa[i] - na);
-            pb[i] = exp2f(pb[i] - nb);
-          }
-          la = la * ca + (pa[0] + pa[1] + pa[2] + pa[3]);
-          lb = lb * cb + (pb[0] + pb[1] + pb[2] + pb[3]);
-          if (kb > 0) {
-#pragma unroll
-            for (int n = 0; n < DH / 8; ++n) {
-              o[n][0] *= ca; o[n][1] *= ca;
-              o[n][2] *= cb; o[n][3] *= cb;
-            }
-          }
-          // P = P_hi + P_lo, both bf16 (two MMAs): P V keeps ~16 mantissa bits of P
-          const uint32_t pf[4] = {pack_bf16x2(pa[0], pa[1]), pack_bf16x2(pb[0], pb[1]), pack_bf16x2(pa[2], pa[3]),
-                                  pack_bf16x2(pb[2], pb[3])};
-          const uint32_t pl[4] = {pack_bf16x2(pa[0] - bf16lo(pf[0]), pa[1] - bf16hi(pf[0])),
-                                  pack_bf16x2(pb[0] - bf16lo(pf[1]), pb[1] - bf16hi(pf[1])),
-                                  pack_bf16x2(pa[2] - bf16lo(pf[2]), pa[3] - bf16hi(pf[2])),
-                                  pack_bf16x2(pb[2] - bf16lo(pf[3]), pb[3] - bf16hi(pf[3]))};
-          const uint32_t v_addr =
-              smem_u32(sV + (k0 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + h * DH + (lane >> 4) * 8);
-#pragma unroll
-          for (int n = 0; n < DH / 16; ++n) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(v_addr + n * 32, b0, b1, b2, b3);
-            mma_bf16_16816(o[2 * n], pf, b0, b1);
-            mma_bf16_16816(o[2 * n + 1], pf, b2, b3);
-            mma_bf16_16816(o[2 * n], pl, b0, b1);
-            mma_bf16_16816(o[2 * n + 1], pl, b2, b3);
-          }
-        }
-        la += __shfl_xor_sync(0xffffffffu, la, 1);
-        la += __shfl_xor_sync(0xffffffffu, la, 2);
-        lb += __shfl_xor_sync(0xffffffffu, lb, 1);
-        lb += __shfl_xor_sync(0xffffffffu, lb, 2);
-        const float ia = 1.0f / la, ib = 1.0f / lb;
-        __syncwarp();   // every lane has read its Q fragments before O overwrites the tile
-        const int ra = 16 * qt + g, rb = ra + 8;  // rows within the text
-        uint16_t* oa = sQ + (q0 + g) * LDS + h * DH + 2 * c4;
-#pragma unroll
-        for (int n = 0; n < DH / 8; ++n) {
-          if (ra < len) *reinterpret_cast<uint32_t*>(oa + n * 8) = pack_bf16x2(o[n][0] * ia, o[n][1] * ia);
-          if (rb < len) *reinterpret_cast<uint32_t*>(oa + 8 * LDS + n * 8) = pack_bf16x2(o[n][2] * ib, o[n][3] * ib);
-        }
-      }
+    for (int qt = 0; qt < nt; ++qt) {
+      uint16_t* sQt = sQ + (ta + 16 * qt) * LDS;
+      float o[HG][DH / 8][4];
+      float ia[HG], ib[HG];
+      attn_query_tile<DH, LDS, HG>(sQt, sK + ta * LDS, sV + ta * LDS, len, nt, qscale, lane, o, ia, ib);
+      __syncwarp();   // every lane has read its Q fragments before O overwrites the tile
+      attn_store_tile<DH, HG>(sQt, LDS, qt, len, lane, o, ia, ib);
     }
   }
   __syncthreads();
@@ -551,7 +438,6 @@ __global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel
     *reinterpret_cast<uint4*>(sK + r * LDS + c * 8) = z;
     *reinterpret_cast<uint4*>(sV + r * LDS + c * 8) = z;
   }
-  const int g = lane >> 2, c4 = lane & 3;
 #pragma unroll 1
   for (int qb0 = 0; qb0 < len; qb0 += A::QROWS) {
     const int nq = min(A::QROWS, len - qb0);
@@ -567,90 +453,10 @@ __global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel
     __syncthreads();
     const int qt = (qb0 >> 4) + warp;            // query tile within the text
     if (16 * qt < len) {
-      uint32_t qa[DH / 16][4];
-      const uint32_t q_addr = smem_u32(sQ + (16 * warp + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
-#pragma unroll
-      for (int kk = 0; kk < DH / 16; ++kk) ldsm_x4(q_addr + kk * 32, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
-      float o[DH / 8][4];
-#pragma unroll
-      for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-      float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
-#pragma unroll 1
-      for (int kb = 0; kb < nt; ++kb) {
-        const int k0 = 16 * kb;
-        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t k_addr = smem_u32(sK + (k0 + (lane & 7) + ((lane >> 4) & 1) * 8) * LDS + ((lane >> 3) & 1) * 8);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          uint32_t b00, b01, b10, b11;
-          ldsm_x4(k_addr + kk * 32, b00, b01, b10, b11);
-          mma_bf16_16816(s0, qa[kk], b00, b01);
-          mma_bf16_16816(s1, qa[kk], b10, b11);
-        }
-        const int j0 = k0 + 2 * c4;
-        const bool v0 = j0 < len, v1 = j0 + 1 < len, v2 = j0 + 8 < len, v3 = j0 + 9 < len;
-        float pa[4], pb[4];
-        pa[0] = v0 ? s0[0] * qscale : -INFINITY;
-        pa[1] = v1 ? s0[1] * qscale : -INFINITY;
-        pa[2] = v2 ? s1[0] * qscale : -INFINITY;
-        pa[3] = v3 ? s1[1] * qscale : -INFINITY;
-        pb[0] = v0 ? s0[2] * qscale : -INFINITY;
-        pb[1] = v1 ? s0[3] * qscale : -INFINITY;
-        pb[2] = v2 ? s1[2] * qscale : -INFINITY;
-        pb[3] = v3 ? s1[3] * qscale : -INFINITY;
-        float xa = fmaxf(fmaxf(pa[0], pa[1]), fmaxf(pa[2], pa[3]));
-        float xb = fmaxf(fmaxf(pb[0], pb[1]), fmaxf(pb[2], pb[3]));
-        xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
-        xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
-        xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
-        xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 2));
-        const float na = fmaxf(ma, xa), nb = fmaxf(mb, xb);
-        const float ca = exp2f(ma - na), cb = exp2f(mb - nb);
-        ma = na;
-        mb = nb;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          pa[i] = exp2f(pa[i] - na);
-          pb[i] = exp2f(pb[i] - nb);
-        }
-        la = la * ca + (pa[0] + pa[1] + pa[2] + pa[3]);
-        lb = lb * cb + (pb[0] + pb[1] + pb[2] + pb[3]);
-        if (kb > 0) {
-#pragma unroll
-          for (int n = 0; n < DH / 8; ++n) {
-            o[n][0] *= ca; o[n][1] *= ca;
-            o[n][2] *= cb; o[n][3] *= cb;
-          }
-        }
-        const uint32_t pf[4] = {pack_bf16x2(pa[0], pa[1]), pack_bf16x2(pb[0], pb[1]), pack_bf16x2(pa[2], pa[3]),
-                                pack_bf16x2(pb[2], pb[3])};
-        const uint32_t pl[4] = {pack_bf16x2(pa[0] - bf16lo(pf[0]), pa[1] - bf16hi(pf[0])),
-                                pack_bf16x2(pb[0] - bf16lo(pf[1]), pb[1] - bf16hi(pf[1])),
-                                pack_bf16x2(pa[2] - bf16lo(pf[2]), pa[3] - bf16hi(pf[2])),
-                                pack_bf16x2(pb[2] - bf16lo(pf[3]), pb[3] - bf16hi(pf[3]))};
-        const uint32_t v_addr = smem_u32(sV + (k0 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
-#pragma unroll
-        for (int n = 0; n < DH / 16; ++n) {
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(v_addr + n * 32, b0, b1, b2, b3);
-          mma_bf16_16816(o[2 * n], pf, b0, b1);
-          mma_bf16_16816(o[2 * n + 1], pf, b2, b3);
-          mma_bf16_16816(o[2 * n], pl, b0, b1);
-          mma_bf16_16816(o[2 * n + 1], pl, b2, b3);
-        }
-      }
-      la += __shfl_xor_sync(0xffffffffu, la, 1);
-      la += __shfl_xor_sync(0xffffffffu, la, 2);
-      lb += __shfl_xor_sync(0xffffffffu, lb, 1);
-      lb += __shfl_xor_sync(0xffffffffu, lb, 2);
-      const float ia = 1.0f / la, ib = 1.0f / lb;
-      const int ra = 16 * qt + g, rb = ra + 8;
-      uint16_t* oa = out + size_t(a + ra) * d + h * DH + 2 * c4;
-#pragma unroll
-      for (int n = 0; n < DH / 8; ++n) {
-        if (ra < len) *reinterpret_cast<uint32_t*>(oa + n * 8) = pack_bf16x2(o[n][0] * ia, o[n][1] * ia);
-        if (rb < len) *reinterpret_cast<uint32_t*>(oa + size_t(8) * d + n * 8) = pack_bf16x2(o[n][2] * ib, o[n][3] * ib);
-      }
+      float o[1][DH / 8][4];
+      float ia[1], ib[1];
+      attn_query_tile<DH, LDS, 1>(sQ + 16 * warp * LDS, sK, sV, len, nt, qscale, lane, o, ia, ib);
+      attn_store_tile<DH, 1>(out + size_t(a + 16 * qt) * d + h * DH, size_t(d), qt, len, lane, o, ia, ib);
     }
     __syncthreads();                             // sQ reused by the next query block
   }
@@ -747,6 +553,51 @@ __global__ void bf16_to_f32_kernel(const uint16_t* __restrict__ in, float* __res
     out[i] = bf16f(in[i]);
 }
 
+// Tile records for the fused QKV + attention kernel (internal.h ATT_REC_INTS layout): one warp per
+// tile; the unit list is built level by level (cost = ceil(len / 16) from 8 down to 1) with an
+// exclusive warp scan of each text's unit count.
+__global__ void __launch_bounds__(256) att_records_kernel(const int32_t* __restrict__ tiles, int32_t n_tiles,
+                                                          const int32_t* __restrict__ cu, int32_t tok0,
+                                                          int32_t n_groups, int32_t* __restrict__ rec) {
+  const int32_t t = int32_t((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n_tiles) return;
+  const int32_t s_a = tiles[t], s_b = tiles[t + 1];
+  const int32_t base = cu[s_a];
+  int32_t* r = rec + size_t(t) * ATT_REC_INTS;
+  uint8_t* start = reinterpret_cast<uint8_t*>(r + 4);
+  uint16_t* units = reinterpret_cast<uint16_t*>(r + 36);
+  const int n = s_b - s_a;
+  for (int j = lane; j < n; j += 32) start[j] = uint8_t(cu[s_a + j] - base);
+  int run = 0;
+  for (int level = 8; level >= 1; --level) {
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      int cnt = 0;
+      if (j < n) {
+        const int a = cu[s_a + j];
+        const int c = (cu[s_a + j + 1] - a + 15) >> 4;
+        cnt = c == level ? c * n_groups : 0;
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      for (int q = 0; q < cnt; ++q)
+        units[run + incl - cnt + q] = uint16_t(j | ((q / n_groups) << 8) | ((q % n_groups) << 11));
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (lane == 0) {
+    r[0] = base - tok0;
+    r[1] = cu[s_b] - base;
+    r[2] = n;
+    r[3] = run;
+  }
+}
+
 inline unsigned blocks_for_warps(int64_t warps, int warps_per_block) {
   return unsigned((warps + warps_per_block - 1) / warps_per_block);
 }
@@ -832,6 +683,13 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
     default: return cudaErrorInvalidValue;
   }
 #undef SURGE_ATT
+  return cudaGetLastError();
+}
+
+cudaError_t launch_att_records(const int32_t* tiles, int32_t n_tiles, const int32_t* cu, int32_t tok0,
+                               int32_t n_groups, int32_t* rec, cudaStream_t st) {
+  if (n_tiles <= 0) return cudaSuccess;
+  att_records_kernel<<<blocks_for_warps(n_tiles, 8), 256, 0, st>>>(tiles, n_tiles, cu, tok0, n_groups, rec);
   return cudaGetLastError();
 }
 

@@ -4,6 +4,7 @@
 //   K3 embed+LN -> L x [ K4 QKV GEMM(+bias) -> K5 varlen attention -> K6 out-proj GEMM(+bias+res+LN)
 //                        -> K7 FFN1 GEMM(+bias+GELU) -> K8 FFN2 GEMM(+bias+res+LN) ] -> K9 meanpool+L2
 // Activations are bf16 in HBM between kernels; all math is fp32 inside the kernels.
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -30,6 +31,8 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   if ((e = cudaMalloc(&win, (t / 64 + 2) * sizeof(int32_t))) != cudaSuccess) return e;
   if (!fused_ln(s.d) && (e = cudaMalloc(&V, t * s.d * 4)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&long_idx, (t / 65 + 1) * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&tiles, (att_max_tiles(cap_tokens) + 1) * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&att_rec, att_max_tiles(cap_tokens) * ATT_REC_INTS * sizeof(int32_t))) != cudaSuccess) return e;
   cap = cap_tokens;
   return cudaSuccess;
 }
@@ -45,7 +48,30 @@ void Workspace::release() {
   V = nullptr;
   if (long_idx) cudaFree(long_idx);
   long_idx = nullptr;
+  if (tiles) cudaFree(tiles);
+  tiles = nullptr;
+  if (att_rec) cudaFree(att_rec);
+  att_rec = nullptr;
   cap = 0;
+}
+
+int32_t att_tiles_for(const int32_t* host_cu, int64_t s0, int64_t s1, std::vector<int32_t>& out) {
+  int32_t n = 0;
+  int64_t s = s0;
+  while (s < s1) {
+    if (host_cu[s + 1] - host_cu[s] > ATT_TILE_ROWS) return -1;
+    out.push_back(int32_t(s));
+    ++n;
+    int64_t e = s + 1;
+    while (e < s1 && host_cu[e + 1] - host_cu[s] <= ATT_TILE_ROWS) ++e;
+    s = e;
+  }
+  if (n & 1) {   // empty tile: zero rows, starts at the chunk's end
+    out.push_back(int32_t(s1));
+    ++n;
+  }
+  out.push_back(int32_t(s1));
+  return n;
 }
 
 DeviceModel::~DeviceModel() {
@@ -116,6 +142,21 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(take_f32(&L.ln2_g, d));
       SURGE_TRY(take_f32(&L.ln2_b, d));
       SURGE_TRY(make_tmap_bf16(&L.tm_wqkv, L.wqkv, 3 * d, d, gemm_b_box_rows(int(3 * d), int(d), EPI_BIAS)));
+      if (qkv_att_supported(int(d), s.heads)) {
+        // head-complete slices: slice j = [Q | K | V] rows of heads j*HG .. j*HG + HG - 1
+        const size_t dh = d / s.heads, hg = ATT_SLICE / (3 * dh);
+        SURGE_TRY(dalloc(reinterpret_cast<void**>(&L.wqkv_att), 3 * d * d * 2));
+        SURGE_TRY(dalloc(reinterpret_cast<void**>(&L.bqkv_att), 3 * d * 4));
+        size_t row = 0;
+        for (size_t j = 0; j < size_t(s.heads) / hg; ++j)
+          for (size_t part = 0; part < 3; ++part)
+            for (size_t hh = 0; hh < hg; ++hh, row += dh) {
+              const size_t src = part * d + (j * hg + hh) * dh;
+              SURGE_TRY(cudaMemcpyAsync(L.wqkv_att + row * d, L.wqkv + src * d, dh * d * 2, cudaMemcpyDeviceToDevice, st));
+              SURGE_TRY(cudaMemcpyAsync(L.bqkv_att + row, L.bqkv + src, dh * 4, cudaMemcpyDeviceToDevice, st));
+            }
+        SURGE_TRY(make_tmap_bf16(&L.tm_wqkv_att, L.wqkv_att, 3 * d, d, gemm_b_box_rows(int(3 * d), int(d), EPI_QKV_ATTN)));
+      }
       const int ln_epi = fused_ln(int(d)) ? EPI_BIAS_LN : EPI_BIAS_RES;
       SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(int(d), int(d), ln_epi)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
@@ -211,6 +252,21 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   double sum_l2 = 0;
   int32_t max_len = s_.max_pos;     // unknown -> assume long texts may be present
   std::vector<int32_t> long_texts;    // chunk-relative indices of texts longer than 64 tokens
+  // fused QKV + attention (EPI_QKV_ATTN) when every text of the chunk fits one 128-row tile
+  std::vector<int32_t> tiles;
+  int32_t n_tiles = -1;
+  if (host_cu && att_fused_ && qkv_att_supported(s_.d, s_.heads)) {
+    tiles.reserve(size_t(s1 - s0) + 4);
+    n_tiles = att_tiles_for(host_cu, s0, s1, tiles);
+    if (n_tiles > att_max_tiles(ntok)) return cudaErrorInvalidValue;
+    if (n_tiles > 0) {   // pageable source: staged by the runtime before the call returns
+      SURGE_TRY(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, st));
+      const int dh = d / s_.heads;
+      SURGE_TRY(launch_att_records(ws.tiles, n_tiles, d_cu, tok0, ATT_SLICE / (3 * dh) / att_unit_heads(dh),
+                                   ws.att_rec, st));
+    }
+  }
+  const bool att_fused = n_tiles > 0;
   if (host_cu) {
     max_len = 0;
     for (int64_t i = s0; i < s1; ++i) {
@@ -219,32 +275,45 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       sum_l2 += double(li) * double(li);
       if (li > 64) long_texts.push_back(int32_t(i - s0));
     }
-    if (!long_texts.empty())   // pageable source: staged by the runtime before the call returns
+    if (!long_texts.empty() && !att_fused)   // pageable source: staged by the runtime before the call returns
       SURGE_TRY(cudaMemcpyAsync(ws.long_idx, long_texts.data(), long_texts.size() * 4, cudaMemcpyHostToDevice, st));
   }
   const double M = ntok, D = d, F = f;
   cudaEvent_t ev = nullptr;
   int64_t k = 0;
   if (P) prof->begin(st, &ev);
+  if (att_fused) ++k;   // launch_att_records
   SURGE_TRY(launch_embed_ln(d_ids, cu, n, tok0, word_, pos_, type_, emb_g_, emb_b_, d, s_.eps, ws.X, st));
-  SURGE_TRY(launch_window_index(cu, n, tok0, ntok, ws.win, st));
+  if (!att_fused) SURGE_TRY(launch_window_index(cu, n, tok0, ntok, ws.win, st));
   if (P) prof->end(KK_EMBED, st, ev, 0.0, M * (4 + 2 * D + 2 * D + 2 * D));
-  k += 2;
+  k += att_fused ? 1 : 2;
   const bool fused = fused_ln(d);
   for (const LayerW& L : layers_) {
     GemmArgs g{};
     g.M = ntok;
     g.eps = s_.eps;
-    // K4: QKV = X Wqkv^T + b
-    g.tmA = &tmX; g.tmB = &L.tm_wqkv; g.tmC = &smQKV; g.N = 3 * d; g.K = d; g.epi = EPI_BIAS; g.bias = L.bqkv; g.C = ws.QKV;
-    if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_gemm(g, st));
-    if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
-    // K5: O = attention(QKV) per text
-    if (P) prof->begin(st, &ev);
-    SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st,
-                               host_cu ? ws.long_idx : nullptr, int32_t(long_texts.size())));
-    if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
+    if (att_fused) {
+      // K4 + K5 fused: O = attention(X Wqkv^T + b), QKV never leaves the SM
+      g.tmA = &tmX; g.tmB = &L.tm_wqkv_att; g.tmC = &smQKV; g.N = 3 * d; g.K = d; g.epi = EPI_QKV_ATTN;
+      g.bias = L.bqkv_att; g.C = ws.O;
+      g.att_rec = ws.att_rec; g.n_att_tiles = n_tiles;
+      g.head_dim = d / s_.heads; g.qscale = 1.4426950408889634f / sqrtf(float(d / s_.heads));
+      if (P) prof->begin(st, &ev);
+      SURGE_TRY(launch_gemm(g, st));
+      if (P) prof->end(KK_QKV_ATTN, st, ev, 2 * M * 3 * D * D + 4 * D * sum_l2, 2 * (M * D + 3 * D * D + M * D));
+      g.att_rec = nullptr; g.n_att_tiles = 0;
+    } else {
+      // K4: QKV = X Wqkv^T + b
+      g.tmA = &tmX; g.tmB = &L.tm_wqkv; g.tmC = &smQKV; g.N = 3 * d; g.K = d; g.epi = EPI_BIAS; g.bias = L.bqkv; g.C = ws.QKV;
+      if (P) prof->begin(st, &ev);
+      SURGE_TRY(launch_gemm(g, st));
+      if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
+      // K5: O = attention(QKV) per text
+      if (P) prof->begin(st, &ev);
+      SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st,
+                                 host_cu ? ws.long_idx : nullptr, int32_t(long_texts.size())));
+      if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
+    }
     // K6: X1 = LN(O Wo^T + bo + X)
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
     g.gamma = L.ln1_g; g.beta = L.ln1_b; g.C = ws.X1;
@@ -275,7 +344,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln2_g, L.ln2_b, s_.eps, ws.X, st));
     }
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += 5 + (max_len > 64 ? 1 : 0) + (fused ? 0 : 2);
+    k += (att_fused ? 4 : 5 + (max_len > 64 ? 1 : 0)) + (fused ? 0 : 2);
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));

@@ -1064,6 +1064,19 @@ surge_status surge_aggregate(const int64_t* sizes, int64_t n_partitions, int64_t
   return SURGE_OK;
 }
 
+surge_status surge_set_option(surge_handle h, int32_t option, int64_t value) {
+  using namespace surge;
+  Ctx* c = h;
+  if (int r = check_handle(c)) return surge_status(r);
+  switch (option) {
+    case SURGE_OPT_ATT_FUSED:
+      if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
+      c->model.set_att_fused(value != 0);
+      return SURGE_OK;
+  }
+  return SURGE_E_INVALID_ARG;
+}
+
 surge_status surge_profile_enable(surge_handle h, int32_t on) {
   using namespace surge;
   Ctx* c = h;

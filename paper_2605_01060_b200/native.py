@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsurge.so")
+# SURGE_LIB: alternative build of the same library (tuning experiments, scripts/); default in-tree
+LIB_PATH = os.environ.get("SURGE_LIB") or os.path.join(_HERE, "libsurge.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libsurge.so not built at {LIB_PATH}: run __graft_entry__.build() "
                       "(python paper_2605_01060_b200/build.py)")
@@ -70,7 +71,8 @@ class surge_kernel_profile(C.Structure):
 
 
 KERNEL_KINDS = ("embed_ln", "gemm_qkv", "attention", "gemm_out_ln", "gemm_ffn1_gelu", "gemm_ffn2_ln",
-                "meanpool_l2", "pack")
+                "meanpool_l2", "pack", "gemm_qkv_attn")
+SURGE_OPT_ATT_FUSED = 1
 
 
 class surge_superbatch_info(C.Structure):
@@ -107,6 +109,7 @@ _SIGS = {
     "surge_aggregate": (C.c_int, [_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _p, _p, _i64p, _i64p]),
     "surge_encode_superbatch": (C.c_int, [_p, _p, _p, _p, C.c_int64, _p, C.c_int64, _p, _p]),
     "surge_profile_enable": (C.c_int, [_p, C.c_int32]),
+    "surge_set_option": (C.c_int, [_p, C.c_int32, C.c_int64]),
     "surge_profile_read": (C.c_int, [_p, C.POINTER(surge_kernel_profile), C.c_int32, C.POINTER(C.c_int32)]),
     "surge_lpt_plan": (C.c_int, [_p, C.c_int64, _p, C.c_int64, C.c_int32, C.c_int64, _p, _p, _p, _p, _p,
                                  _i64p]),
@@ -318,6 +321,10 @@ def surge_encode_superbatch(h, d_ids, d_lengths, h_lengths: np.ndarray, h_sizes:
     return _check(h, lib.surge_encode_superbatch(h, _ptr(d_ids), _ptr(d_lengths), hl.ctypes.data, hl.size,
                                                  hs.ctypes.data, hs.size, _ptr(d_out), _stream(stream)),
                   "surge_encode_superbatch")
+
+
+def surge_set_option(h, option: int, value: int):
+    return _check(h, lib.surge_set_option(h, option, int(value)), "surge_set_option")
 
 
 def surge_profile_enable(h, on: bool = True):

@@ -105,14 +105,19 @@ def test_gemm_vs_torch(N, M, Nn, K, epi):
 
 
 def ref_attention(qkv, cu, heads, dh):
+    """fp32 SDPA per text; also returns, per output element, max |v| over the text's keys for its
+    head (the scale of the bf16 rounding error of P, see test_attention_vs_torch)."""
     d = heads * dh
     out = torch.empty(qkv.shape[0], d, device=qkv.device)
+    vmax = torch.empty(qkv.shape[0], d, device=qkv.device)
     for s in range(len(cu) - 1):
         a, b = cu[s], cu[s + 1]
         x = qkv[a:b].view(b - a, 3, heads, dh).permute(1, 2, 0, 3)
         o = torch.nn.functional.scaled_dot_product_attention(x[0][None], x[1][None], x[2][None])[0]
         out[a:b] = o.permute(1, 0, 2).reshape(b - a, d)
-    return out
+        vm = x[2].abs().amax(dim=(1, 2))                      # [heads]
+        vmax[a:b] = vm.repeat_interleave(dh)[None, :].expand(b - a, d)
+    return out, vmax
 
 
 @pytest.mark.parametrize("heads,dh,maxlen", [(12, 32, 128), (4, 16, 64), (12, 32, 20), (16, 64, 300), (12, 32, 65)])
@@ -128,9 +133,12 @@ def test_attention_vs_torch(N, heads, dh, maxlen):
     out = torch.zeros(T, heads * dh, dtype=torch.int16, device="cuda")
     N.surge_op_attention(qkv, dev(cu), len(lens), heads, dh, out)
     torch.cuda.synchronize()
-    ref = ref_attention(from_bits(qkv), cu.tolist(), heads, dh)
+    ref, vmax = ref_attention(from_bits(qkv), cu.tolist(), heads, dh)
     err = (from_bits(out) - ref).abs()
-    assert bool((err <= 2 ** -7 * ref.abs() + 2e-3).all()), err.max().item()
+    # bf16 output rounding (2^-9 relative, 2^-7 with margin) + P entering P V as bf16: each p_j is
+    # rounded to 2^-9 relative and the normaliser uses the unrounded sum, so |dO| <= 2^-8 max_j |v_j|
+    tol = 2 ** -7 * ref.abs() + 2 ** -8 * vmax + 1e-3
+    assert bool((err <= tol).all()), (err - tol).max().item()
     # length-1 texts: softmax of one score is 1 -> output = v (bit-exact after bf16 rounding of v)
     v0 = from_bits(qkv)[0, 2 * heads * dh:]
     assert torch.equal(from_bits(out)[0], v0)

@@ -219,3 +219,63 @@ def test_larger_encoder_classes_sample(N, enc, length_model):
         T = texts_of(ids, lens)
         rows = sorted({0, n - 1, int(np.argmax(lens)), *rng.integers(0, n, size=min(n, 2)).tolist()})
         compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0):
+    h = N.surge_create(N.make_config(ecfg, 1000, 5000, chunk_tokens=chunk_tokens), pack_blob(ecfg, w))
+    try:
+        N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, 1 if fused else 0)
+        out = torch.zeros(len(lens), ecfg.hidden, device="cuda")
+        N.surge_encode_packed(h, torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(), lens, len(lens), out)
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+    finally:
+        N.surge_destroy(h)
+
+
+def _edge_lengths(rng, n, max_len):
+    """Lengths that stress the text-aligned 128-row tiles of the fused QKV + attention kernel:
+    1-token texts, 16/17 (key-block edges), texts exactly filling a tile, runs of long texts (one
+    text per tile), plus a uniform mix."""
+    edge = [1, 1, 2, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 128, 1, 100, 28, 128, 5]
+    lens = np.concatenate([np.array([min(x, max_len) for x in edge]), rng.integers(1, max_len + 1, size=n)])
+    return lens.astype(np.int32)
+
+
+@pytest.mark.parametrize("enc", ["toy", "minilm", "bgebase"])
+def test_fused_qkv_attention_matches_separate_path_and_oracle(N, enc):
+    """K4+K5 fused (attention in the QKV GEMM epilogue, text-aligned tiles) vs the separate K4 GEMM
+    + K5 kernels: bit-identical embeddings (shared attention arithmetic, same bf16 QKV rounding);
+    and sampled rows (all edge lengths) vs the oracle.  Chunk size 4096 tokens gives many chunks
+    with ragged ends and odd tile counts (padding tile)."""
+    ecfg = ENCODERS[enc]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(5)
+    max_len = min(128, ecfg.max_position)
+    lens = _edge_lengths(rng, 700, max_len)
+    ids = rng.integers(4 if enc == "toy" else 1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    fused = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096)
+    sep = _packed_encode(N, ecfg, w, lens, ids, False, chunk_tokens=4096)
+    assert np.array_equal(fused, sep)
+    E = oenc.Encoder(ecfg, w)
+    T = texts_of(ids, lens)
+    rows = sorted({*range(20), len(lens) - 1, *rng.integers(0, len(lens), size=12).tolist()})
+    compare(fused[rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def test_fused_path_falls_back_for_long_texts(N):
+    """Chunks holding a text > 128 tokens take the separate path; chunks without take the fused one.
+    The embeddings of a short text are identical in both kinds of chunk."""
+    ecfg = ENCODERS["bgebase"]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(9)
+    lens = rng.integers(8, 60, size=400).astype(np.int32)
+    lens[[50, 51, 300]] = [129, 300, 512]
+    ids = rng.integers(1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    fused = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=2048)
+    sep = _packed_encode(N, ecfg, w, lens, ids, False, chunk_tokens=2048)
+    assert np.array_equal(fused, sep)
+    E = oenc.Encoder(ecfg, w)
+    T = texts_of(ids, lens)
+    rows = [0, 50, 51, 52, 300, 399]
+    compare(fused[rows], np.stack([E.encode_text(T[i]) for i in rows]))

@@ -1,0 +1,117 @@
+// epi_ln.cuh -- the residual + LayerNorm GEMM epilogue (K6 / K8; reading R9:
+// post-LN, biased variance, fp32 statistics), shared by the LN GEMM (gemm_tc.cu) and the fused MLP
+// (mlp_tc.cu) so both round identically.
+//
+// The accumulator row (BN fp32 columns in TMEM, lane = row) is split over two warps of the same
+// lane quadrant q, each owning columns [c_lo, c_lo + HALF), hh = which half.
+//   pass 1: v = acc + bias + residual, written back to TMEM in place, shifted partial sums (the
+//           residual slice and TMEM load of step k+1 are in flight while step k is computed; the
+//           first residual slice is fetched before the accumulator is ready);
+//   combine the halves (Chan's parallel variance) through smem (stats: [2 halves][128 rows]);
+//   pass 2: y = (v - mean) rstd gamma + beta -> bf16, handed to store(p, column) 32 columns at a time.
+#pragma once
+
+#include "common.cuh"
+
+namespace surge {
+
+// Residual source: load(k, rr) fills rr[16] = the 32 bf16 residual values of step k (columns
+// c_lo + 32 k ..), packed in pairs.  It is called one step ahead of use.
+struct ResidualGlobal {
+  const uint16_t* rrow;   // this row, column c_lo
+  __device__ __forceinline__ void operator()(int k, uint32_t (&rr)[16]) const {
+    const uint4* p = reinterpret_cast<const uint4*>(rrow + 32 * k);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = p[i];
+      rr[4 * i] = v.x; rr[4 * i + 1] = v.y; rr[4 * i + 2] = v.z; rr[4 * i + 3] = v.w;
+    }
+  }
+};
+
+#ifdef LN_TRACE
+__device__ long long g_ln_trace[32][4];
+#define LNT(i) do { const long long _c = clock64(); if (i > 0 && blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_ln_trace[threadIdx.x >> 5][i - 1] += _c - _lt; _lt = _c; } while (0)
+#else
+#define LNT(i) do {} while (0)
+#endif
+
+template <int BN, int HALF, typename Res, typename Ready, typename Store>
+__device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
+                                            const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,
+                                            int lane, float eps, Ready&& wait_ready, Store&& store) {
+#ifdef LN_TRACE
+  long long _lt = 0;
+#endif
+  constexpr int NSTEP = HALF / 32;
+  uint32_t r[2][32];
+  uint32_t rs[2][16];
+  load_res(0, rs[0]);
+  wait_ready();
+  LNT(0);
+  tmem_ld32(taddr + c_lo, r[0]);
+  float shift = 0.f;
+  f32x2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < NSTEP; ++k) {
+    const int cur = k & 1;
+    const int c = c_lo + 32 * k;
+    tmem_ld_wait_regs(r[cur]);
+    if (k + 1 < NSTEP) {
+      tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+      load_res(k + 1, rs[cur ^ 1]);
+    }
+    const uint32_t (&rr)[16] = rs[cur];
+    if (k == 0) shift = __uint_as_float(r[cur][0]) + s_bias[c] + bf16lo(rr[0]);
+    uint32_t w[32];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 bb = *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
+      const f32x2 v = fadd2(fadd2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])),
+                                  f2(bb.x, bb.y)),
+                            f2(bf16lo(rr[i]), bf16hi(rr[i])));
+      const f32x2 dv = fadd2(v, f2(-shift, -shift));
+      s1 = fadd2(s1, dv);
+      s2 = ffma2(dv, dv, s2);
+      w[2 * i] = __float_as_uint(f2lo(v));
+      w[2 * i + 1] = __float_as_uint(f2hi(v));
+    }
+    tmem_st32(taddr + c, w);
+  }
+  tmem_st_wait();
+  LNT(1);
+  const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
+  stats[hh * 128 + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");   // the two warps of this quadrant
+  LNT(2);
+  const float4 o = stats[(hh ^ 1) * 128 + q * 32 + lane];
+  const float nh = float(HALF);
+  const float mean_a = shift + S1 / nh, m2_a = S2 - S1 * S1 / nh;
+  const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
+  const float dm = mean_a - mean_b;
+  const float mean = 0.5f * (mean_a + mean_b);
+  const float var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
+  const float rstd = rsqrtf(var + eps);
+  const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);
+  tmem_ld32(taddr + c_lo, r[0]);
+#pragma unroll
+  for (int k = 0; k < NSTEP; ++k) {
+    const int cur = k & 1;
+    const int c = c_lo + 32 * k;
+    tmem_ld_wait_regs(r[cur]);
+    if (k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+    uint32_t p[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 gg = *reinterpret_cast<const float2*>(s_gamma + c + 2 * i);
+      const float2 be = *reinterpret_cast<const float2*>(s_beta + c + 2 * i);
+      const f32x2 z = ffma2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])), k_rstd, k_off);
+      const f32x2 y = ffma2(z, f2(gg.x, gg.y), f2(be.x, be.y));
+      p[i] = pack_bf16x2(f2lo(y), f2hi(y));
+    }
+    store(p, c);
+  }
+  LNT(3);
+}
+
+}  // namespace surge

@@ -16,6 +16,7 @@
 
 #include "attn_tile.cuh"
 #include "common.cuh"
+#include "epi_ln.cuh"
 #include "internal.h"
 
 namespace surge {
@@ -55,7 +56,8 @@ struct TileCfg {
   static constexpr int HEAD_BYTES = 1024;                         // mbarriers + TMEM slot
   static constexpr int STATS_BYTES =                              // LN: stats + bias/gamma/beta, 1 KB aligned
       EPI == EPI_BIAS_LN ? ((2 * 2 * BM * 4 * 4 + 3 * BN * 4 + 1023) / 1024) * 1024 : 0;
-  static constexpr int STG_BUFS = 1;                              // per-warp output staging buffers
+  // per-warp output staging buffers (3 for the LN tiles measured slower: out-proj 520 -> 590 ms/step)
+  static constexpr int STG_BUFS = 1;
   static constexpr int STG_BYTES = ATT ? 0 : EPI_WARPS * STG_BUFS * 2048;  // 32 rows x 32 cols bf16 each
   // EPI_QKV_ATTN: the tile's Q | K | V (bf16) staged for attention, 128 rows + 16 zero rows read
   // past the last text by a query tile / key block, 16-byte row skew.
@@ -559,84 +561,14 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
           }
         }
       } else {
-        // LayerNorm over the full row (BN == N), two warps per row (column halves).
-        // pass 1: v = acc + bias + residual, written back to TMEM in place, shifted partial sums;
-        //         the residual slice and TMEM load of step k+1 are in flight while step k is
-        //         computed (the first residual slice is fetched before the accumulator is ready);
-        // combine the halves (Chan) through smem; pass 2: y = (v - mean) rstd gamma + beta,
-        //         TMEM loads pipelined the same way.
-        const uint16_t* rrow = res + size_t(ok ? row : 0) * N + c_lo;
-        uint32_t r[2][32];
-        uint4 rs[2][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) rs[0][i] = reinterpret_cast<const uint4*>(rrow)[i];
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        tmem_ld32(taddr + c_lo, r[0]);
-        float shift = 0.f;
-        f32x2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < NSTEP; ++k) {
-          const int cur = k & 1;
-          const int c = c_lo + 32 * k;
-          tmem_ld_wait_regs(r[cur]);
-          if (k + 1 < NSTEP) {
-            tmem_ld32(taddr + c + 32, r[cur ^ 1]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) rs[cur ^ 1][i] = reinterpret_cast<const uint4*>(rrow + 32 * (k + 1))[i];
-          }
-          const uint32_t rr[16] = {rs[cur][0].x, rs[cur][0].y, rs[cur][0].z, rs[cur][0].w,
-                                   rs[cur][1].x, rs[cur][1].y, rs[cur][1].z, rs[cur][1].w,
-                                   rs[cur][2].x, rs[cur][2].y, rs[cur][2].z, rs[cur][2].w,
-                                   rs[cur][3].x, rs[cur][3].y, rs[cur][3].z, rs[cur][3].w};
-          if (k == 0) shift = __uint_as_float(r[cur][0]) + s_bias[c] + bf16lo(rr[0]);
-          uint32_t w[32];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 bb = *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
-            const f32x2 v = fadd2(fadd2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])),
-                                        f2(bb.x, bb.y)),
-                                  f2(bf16lo(rr[i]), bf16hi(rr[i])));
-            const f32x2 dv = fadd2(v, f2(-shift, -shift));
-            s1 = fadd2(s1, dv);
-            s2 = ffma2(dv, dv, s2);
-            w[2 * i] = __float_as_uint(f2lo(v));
-            w[2 * i + 1] = __float_as_uint(f2hi(v));
-          }
-          tmem_st32(taddr + c, w);
-        }
-        tmem_st_wait();
-        const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
-        const int sbuf = it & 1;
-        stats[(sbuf * 2 + hh) * BM + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);
-        named_bar_sync(1 + q, 64);            // the two warps of this quadrant
-        const float4 o = stats[(sbuf * 2 + (hh ^ 1)) * BM + q * 32 + lane];
-        const float nh = float(T::HALF);
-        const float mean_a = shift + S1 / nh, m2_a = S2 - S1 * S1 / nh;
-        const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
-        const float dm = mean_a - mean_b;
-        const float mean = 0.5f * (mean_a + mean_b);
-        const float var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
-        const float rstd = rsqrtf(var + eps);
-        const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);
-        tmem_ld32(taddr + c_lo, r[0]);
-#pragma unroll
-        for (int k = 0; k < NSTEP; ++k) {
-          const int cur = k & 1;
-          const int c = c_lo + 32 * k;
-          tmem_ld_wait_regs(r[cur]);
-          if (k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
-          uint32_t p[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 gg = *reinterpret_cast<const float2*>(s_gamma + c + 2 * i);
-            const float2 be = *reinterpret_cast<const float2*>(s_beta + c + 2 * i);
-            const f32x2 z = ffma2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])), k_rstd, k_off);
-            const f32x2 y = ffma2(z, f2(gg.x, gg.y), f2(be.x, be.y));
-            p[i] = pack_bf16x2(f2lo(y), f2hi(y));
-          }
-          stage_store(p, c);
-        }
+        // LayerNorm over the full row (BN == N), two warps per row (column halves): epi_ln.cuh
+        const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + c_lo};
+        ln_epilogue<BN, T::HALF>(taddr, c_lo, rg, s_bias, s_gamma, s_beta, stats + (it & 1) * 2 * BM, q, hh, lane,
+                                 eps, [&] {
+                                   mbar_wait(&tfull[acc], aph);
+                                   tc_fence_after();
+                                 },
+                                 stage_store);
       }
       if constexpr (!T::ATT) {
         tc_fence_before();

@@ -1,0 +1,504 @@
+// mlp_tc.cu -- K7 + K8 fused: the encoder's feed-forward block as one kernel:
+//   X2 = LN_o( GELU_erf(X1 W1^T + b1) W2^T + b2 + X1 )
+// H = GELU(X1 W1^T + b1) never leaves the SM: per 128-row tile it is produced in ff-chunks of 128
+// columns in TMEM, turned into bf16 in shared memory by the epilogue warps, and consumed there as the
+// A operand of the second GEMM, whose accumulator (d columns) stays in TMEM across all chunks.
+//
+// Design (DESIGN.md §6 "fused MLP"): CTA pairs (cta_group::2, M = 256 rows per pair, each CTA its 128
+// rows and half of every MMA's B rows), persistent over 256-row units.
+//   TMEM (512 columns): Y = [0, D) second-GEMM accumulator, H = [384, 512) first-GEMM chunk.
+//   smem: A = the unit's X1 rows (D/64 k-blocks of 128 x 64 bf16, 128-byte swizzle, resident for
+//         the unit), Hs = one H chunk (2 k-blocks, written by the epilogue in the same swizzled
+//         K-major layout the TMA would produce; it doubles as the LN output staging), a 3-stage
+//         weight ring (24 KB stages: 3 W1 k-blocks or 1 W2 k-block per stage).
+//   warps 0, 2, 3: TMA producers (A once per unit, the W1 / W2 ring); warp 1: MMA issuer (leader
+//   CTA); warp 2 also allocates TMEM; warps 4..11: epilogue (GELU of each chunk; LN at the end).
+//   MMA issue order per unit: G1(0), G1(1), G2(0), G1(2), G2(1), ..., G1(n-1), G2(n-2), G2(n-1):
+//   G2(c-1) runs on the tensor pipe while the epilogue turns H(c) into Hs.
+// Numerics equal the separate K7 / K8 GEMMs: H is bias + gelu2 + bf16 as EPI_BIAS_GELU; Y sums the
+// same k-blocks in the same order; the LN epilogue is epi_ln.cuh (shared).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "epi_ln.cuh"
+#include "internal.h"
+
+namespace surge {
+
+namespace {
+
+constexpr int MBM = 128;            // rows per CTA
+constexpr int FC = 128;             // ff columns per chunk (H accumulator columns)
+#ifndef MLP_RING
+#define MLP_RING 4
+#endif
+#ifndef MLP_STG
+#define MLP_STG 1                   // LN output staging buffers per epilogue warp
+#endif
+#ifndef MLP_PREFETCH
+#define MLP_PREFETCH 0              // L2 prefetch of the next unit's A rows (measured: no effect)
+#endif
+constexpr int RING = MLP_RING;      // weight ring stages
+constexpr int STAGE = 24 * 1024;    // 3 W1 k-blocks (64 rows x 128 B each) or 1 W2 k-block (2 x 96 rows)
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 128 + 32 * EPI_WARPS;
+constexpr uint32_t H_COL = 384;     // TMEM column of the H chunk
+
+template <int D>
+struct MlpCfg {
+  static constexpr int KB1 = D / 64;                 // k-blocks of the first GEMM
+  static constexpr int A_BYTES = KB1 * MBM * 128;    // resident X1 rows
+  static constexpr int HS_BYTES = 2 * MBM * 128;     // one H chunk, 2 k-blocks
+  static constexpr int N2 = D <= 256 ? D : D / 2;    // second-GEMM MMA N (<= 256)
+  static constexpr int N2_MMAS = D / N2;
+  static constexpr int B2_BOX = N2 / 2;              // rows of W2 per CTA per MMA (pair)
+  static constexpr int HEAD = 1024;                  // barriers + TMEM slot
+  // The LN output staging (8 warps x 2 KB), LN stats ([2 halves][128] float4, 4 KB) and b2 / gamma /
+  // beta (3 D floats, copied in per unit) live in Hs, which is idle while the LN epilogue runs.
+  // LN scratch (aliases Hs, which is idle during the LN): output staging [8 warps][MLP_STG][2 KB],
+  // stats [2 halves][128] float4, b2 / gamma / beta
+  static constexpr int LN_STG = EPI_WARPS * MLP_STG * 2048;
+  static constexpr int LN_SCRATCH = ((LN_STG + 2 * MBM * 16 + 3 * D * 4 + 1023) / 1024) * 1024;
+  static constexpr int SCRATCH = LN_SCRATCH > HS_BYTES ? LN_SCRATCH : HS_BYTES;
+  static constexpr int SMEM = 1024 + HEAD + A_BYTES + SCRATCH + RING * STAGE;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(D % 64 == 0 && D <= 384, "Y must fit TMEM next to the H chunk");
+  static_assert(KB1 % 3 == 0 || KB1 == 1, "W1 k-blocks pack 3 per stage");
+  static_assert(B2_BOX * 128 * N2_MMAS <= STAGE, "W2 k-block fits a stage");
+};
+
+#ifdef MLP_TRACE
+#define MW(bar, par, slot)                      \
+  do {                                          \
+    const long long _t0 = clock64();            \
+    mbar_wait(bar, par);                        \
+    tw[slot] += clock64() - _t0;                \
+  } while (0)
+#else
+#define MW(bar, par, slot) mbar_wait(bar, par)
+#endif
+
+// LN residual from the resident A tile (128-byte-swizzled K-major: k-block c / 64, row r at r * 128 B,
+// 16-byte chunk j at (j ^ (r & 7)) * 16).
+struct ResidualSmemA {
+  const uint8_t* sA;
+  int row, c_lo;
+  __device__ __forceinline__ void operator()(int k, uint32_t (&rr)[16]) const {
+    const int c = c_lo + 32 * k;
+    const uint8_t* base = sA + (c >> 6) * (MBM * 128) + row * 128;
+    const int j0 = (c & 63) >> 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + (((j0 + i) ^ (row & 7)) << 4));
+      rr[4 * i] = v.x; rr[4 * i + 1] = v.y; rr[4 * i + 2] = v.z; rr[4 * i + 3] = v.w;
+    }
+  }
+};
+
+// Remote arrive with the default semantics (.release at .cta scope): after fence.proxy.async this
+// publishes the thread's generic-proxy shared-memory writes to the leader's MMA, as CUTLASS's 2-SM
+// pipelines do; .release.cluster would add a MEMBAR.ALL.GPU (measured ~1.5K cycles per chunk).
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Persistent CTA-pair kernel; unit u = rows [256 u, 256 u + 256), CTA rank r owns [256 u + 128 r, +128).
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+    mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmW1,
+                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmOut,
+                  const __grid_constant__ CUtensorMap tmR, int M, int F, const float* __restrict__ b1,
+                  const float* __restrict__ b2, const float* __restrict__ gamma, const float* __restrict__ beta,
+                  const uint16_t* __restrict__ res, float eps) {
+  using T = MlpCfg<D>;
+  constexpr int KB1 = T::KB1;
+  constexpr int S1 = KB1 == 1 ? 1 : KB1 / 3;         // ring stages per W1 chunk
+  constexpr int KPS = KB1 == 1 ? 1 : 3;              // W1 k-blocks per stage
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [RING]   leader: both CTAs' bytes
+  uint64_t* empty = full + RING;                             // [RING]   both (multicast commit)
+  uint64_t* a_full = empty + RING;                           // leader
+  uint64_t* a_empty = a_full + 1;                            // both
+  uint64_t* h_full = a_empty + 1;                            // both
+  uint64_t* h_empty = h_full + 1;                            // leader, 2 x EPI_WARPS arrivals
+  uint64_t* hs_full = h_empty + 1;                           // leader, 2 x EPI_WARPS arrivals
+  uint64_t* hs_empty = hs_full + 1;                          // both
+  uint64_t* y_full = hs_empty + 1;                           // both
+  uint64_t* y_empty = y_full + 1;                            // leader, 2 x EPI_WARPS arrivals
+  uint64_t* a_free = y_empty + 1;                            // local: LN read its residual from A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_free + 1);
+  uint8_t* sA = smem + T::HEAD;                              // [KB1][128 x 128 B]
+  uint8_t* sHs = sA + T::A_BYTES;                            // [2][128 x 128 B]
+  float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
+  float* s_b2 = reinterpret_cast<float*>(stats + 2 * MBM);   // LN only
+  float* s_gamma = s_b2 + D;
+  float* s_beta = s_gamma + D;
+  uint8_t* sW = sHs + T::SCRATCH;                            // [RING][STAGE]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = int(blockIdx.x & 1);
+  const bool leader = rank == 0;
+  const int unit0 = int(blockIdx.x >> 1), units = int(gridDim.x >> 1);
+  const int n_units = (M + 2 * MBM - 1) / (2 * MBM);
+  const int NCH = F / FC;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX1);
+    tma_prefetch_desc(&tmW1);
+    tma_prefetch_desc(&tmW2);
+    for (int s = 0; s < RING; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    mbar_init(h_full, 1);
+    mbar_init(h_empty, 2 * EPI_WARPS);
+    mbar_init(hs_full, 2 * EPI_WARPS);
+    mbar_init(hs_empty, 1);
+    mbar_init(y_full, 1);
+    mbar_init(y_empty, 2 * EPI_WARPS);
+    mbar_init(a_free, EPI_WARPS);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, 512);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ TMA producers
+      // Box sequence per unit: A (KB1 boxes, after the previous unit's last G1 freed it), then per
+      // chunk slot in MMA order: W1(c) stages, W2(c-1) stages.  Ring stage i is issued by producer i % 3.
+      const int p = warp == 0 ? 0 : warp - 1;
+      const uint64_t pol_w = l2_policy_evict_last();
+      const uint32_t full_c = mapa_shared(smem_u32(full), 0);
+      const uint32_t afull_c = mapa_shared(smem_u32(a_full), 0);
+      uint32_t sc = 0;                                   // ring stage counter
+      int ui = 0;
+      auto ring_w1 = [&](int c) {
+        for (int s2 = 0; s2 < S1; ++s2, ++sc) {
+          const int s = int(sc % RING);
+          const uint32_t ph = (sc / RING) & 1;
+          if (int(sc % 3) != p) continue;               // stage sc is issued by producer sc % 3
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * KPS * 64 * 128);
+          for (int j = 0; j < KPS; ++j)
+            tma_load_2d_pair(sW + s * STAGE + j * 64 * 128, &tmW1, full_c + uint32_t(s) * 8, (s2 * KPS + j) * 64,
+                             c * FC + rank * 64, pol_w);
+        }
+      };
+      auto ring_w2 = [&](int c) {
+        for (int kb = 0; kb < 2; ++kb, ++sc) {
+          const int s = int(sc % RING);
+          const uint32_t ph = (sc / RING) & 1;
+          if (int(sc % 3) != p) continue;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * T::N2_MMAS * T::B2_BOX * 128);
+          for (int j = 0; j < T::N2_MMAS; ++j)
+            tma_load_2d_pair(sW + s * STAGE + j * T::B2_BOX * 128, &tmW2, full_c + uint32_t(s) * 8, c * FC + kb * 64,
+                             j * T::N2 + rank * T::B2_BOX, pol_w);
+        }
+      };
+      for (int u = unit0; u < n_units; u += units, ++ui) {
+        const int m0 = u * 2 * MBM + rank * MBM;
+        if (p == 0) {                                    // A: this CTA's rows, once per unit
+          mbar_wait(a_empty, (ui & 1) ^ 1);     // MMAs done with the previous unit's A
+          mbar_wait(a_free, (ui & 1) ^ 1);      // its LN has read the residual rows
+          if (leader) mbar_arrive_expect_tx(a_full, 2u * T::A_BYTES);
+          for (int kb = 0; kb < KB1; ++kb)
+            tma_load_2d_pair(sA + kb * MBM * 128, &tmX1, afull_c, kb * 64, m0, l2_policy_evict_first());
+          // warm L2 with the next unit's rows: its A load waits for this unit's LN (residual from A)
+          if (MLP_PREFETCH && u + units < n_units)
+            for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmX1, kb * 64, m0 + units * 2 * MBM);
+        }
+        for (int c = 0; c < NCH; ++c) {
+          ring_w1(c);
+          if (c > 0) ring_w2(c - 1);
+        }
+        ring_w2(NCH - 1);
+      }
+    }
+  } else if (warp == 1 && leader) {
+    // -------------------------------------------------------------------- MMA issuer (leader)
+    constexpr uint32_t idesc1 = umma_idesc_bf16(2 * MBM, FC);
+    constexpr uint32_t idesc2 = umma_idesc_bf16(2 * MBM, T::N2);
+    const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
+    const uint64_t hs_desc0 = umma_desc_sw128(smem_u32(sHs));
+    const uint64_t w_desc0 = umma_desc_sw128(smem_u32(sW));
+#ifdef MLP_TRACE
+    long long tw[5] = {0, 0, 0, 0, 0};
+    const long long t_start = clock64();
+#endif
+    uint32_t sc = 0;        // ring stage counter
+    uint32_t hc = 0;        // chunks issued (G1) -> h_full / h_empty phases
+    uint32_t gc = 0;        // chunks issued (G2) -> hs_full / hs_empty phases
+    int ui = 0;
+    auto g2 = [&](int c, int uiu) {
+      if (c == 0) {
+        MW(y_empty, (uiu & 1) ^ 1, 0);               // LN of the previous unit drained Y
+        tc_fence_after();
+      }
+      MW(hs_full, gc & 1, 1);                        // both CTAs' Hs(c) written
+      tc_fence_after();
+      for (int kb = 0; kb < 2; ++kb, ++sc) {
+        const int s = int(sc % RING);
+        MW(&full[s], (sc / RING) & 1, 2);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ad = hs_desc0 + uint64_t((kb * MBM * 128) >> 4);
+          const uint64_t bd = w_desc0 + uint64_t((s * STAGE) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < T::N2_MMAS; ++j)
+              tc_mma_bf16_pair(tmem_base + j * T::N2, ad + uint64_t(k * 2),
+                               bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, (c | kb | k) != 0);
+          tc_commit_pair_mc(&empty[s], 0x3);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        tc_commit_pair_mc(hs_empty, 0x3);               // Hs free for the next chunk
+        if (c == NCH - 1) tc_commit_pair_mc(y_full, 0x3);
+      }
+      __syncwarp();
+      ++gc;
+    };
+    for (int u = unit0; u < n_units; u += units, ++ui) {
+      MW(a_full, ui & 1, 3);
+      tc_fence_after();
+      for (int c = 0; c < NCH; ++c) {
+        MW(h_empty, (hc & 1) ^ 1, 4);                // epilogue drained H(c-1)
+        tc_fence_after();
+        for (int s2 = 0; s2 < S1; ++s2, ++sc) {
+          const int s = int(sc % RING);
+          MW(&full[s], (sc / RING) & 1, 2);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t bd0 = w_desc0 + uint64_t((s * STAGE) >> 4);
+            for (int j = 0; j < KPS; ++j) {
+              const int kb = s2 * KPS + j;
+              const uint64_t ad = a_desc0 + uint64_t((kb * MBM * 128) >> 4);
+              const uint64_t bd = bd0 + uint64_t((j * 64 * 128) >> 4);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc_mma_bf16_pair(tmem_base + H_COL, ad + uint64_t(k * 2), bd + uint64_t(k * 2), idesc1, (kb | k) != 0);
+            }
+            tc_commit_pair_mc(&empty[s], 0x3);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          tc_commit_pair_mc(h_full, 0x3);
+          if (c == NCH - 1) tc_commit_pair_mc(a_empty, 0x3);   // A free for the next unit
+        }
+        __syncwarp();
+        ++hc;
+        if (c > 0) g2(c - 1, ui);
+      }
+      g2(NCH - 1, ui);
+    }
+#ifdef MLP_TRACE
+    if (lane == 0 && blockIdx.x < 8)
+      printf("MLP_TRACE cta %d units %d total %lld | wait y_empty %lld hs_full %lld ring %lld a_full %lld h_empty %lld\n",
+             int(blockIdx.x), ui, clock64() - t_start, tw[0], tw[1], tw[2], tw[3], tw[4]);
+#endif
+
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue (warps 4..11)
+    const int q = warp & 3;                    // TMEM lane quadrant
+    const int hh = (warp - 4) >> 2;            // column half
+    const int row_l = q * 32 + lane;           // row within the CTA tile
+    const uint32_t hs_full_c = mapa_shared(smem_u32(hs_full), 0);
+    const uint32_t h_empty_c = mapa_shared(smem_u32(h_empty), 0);
+    const uint32_t y_empty_c = mapa_shared(smem_u32(y_empty), 0);
+    const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16);
+    uint32_t hc = 0;
+    int ui = 0;
+#ifdef MLP_TRACE
+    long long et[12] = {}, el = 0;
+#define ETR(i) do { const long long _c = clock64(); if (i > 0) et[i - 1] += _c - el; el = _c; } while (0)
+#else
+#define ETR(i) do {} while (0)
+#endif
+    for (int u = unit0; u < n_units; u += units, ++ui) {
+      const int m0 = u * 2 * MBM + rank * MBM;
+      for (int c = 0; c < NCH; ++c, ++hc) {
+        // H(c) columns [64 hh, 64 hh + 64) of this row: TMEM -> registers, then release the accumulator
+        const float4* bp = reinterpret_cast<const float4*>(b1 + c * FC + 64 * hh);
+        float4 bb[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bb[i] = __ldg(bp + i);
+        uint32_t r0[32], r1[32];
+        ETR(0);
+        mbar_wait(h_full, hc & 1);
+        ETR(1);
+        tc_fence_after();
+        tmem_ld32(t_row + H_COL + 64 * hh, r0);
+        tmem_ld32(t_row + H_COL + 64 * hh + 32, r1);
+        tmem_ld_wait_regs(r0);
+        tmem_ld_wait_regs(r1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(h_empty_c);
+        ETR(2);
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t* rr = i < 8 ? r0 : r1;
+          const int o = (i & 7) * 4;
+          float v0 = __uint_as_float(rr[o]) + bb[i].x, v1 = __uint_as_float(rr[o + 1]) + bb[i].y;
+          float v2 = __uint_as_float(rr[o + 2]) + bb[i].z, v3 = __uint_as_float(rr[o + 3]) + bb[i].w;
+          gelu2(v0, v1);
+          gelu2(v2, v3);
+          pk[2 * i] = pack_bf16x2(v0, v1);
+          pk[2 * i + 1] = pack_bf16x2(v2, v3);
+        }
+        ETR(3);
+        mbar_wait(hs_empty, (hc & 1) ^ 1);      // Hs free: G2(c-1) retired
+        ETR(4);
+        // k-block hh of Hs, row row_l: 8 chunks of 16 B at (j ^ (row & 7)) (128-byte swizzle)
+        uint8_t* hrow = sHs + hh * MBM * 128 + row_l * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(hrow + ((j ^ (row_l & 7)) << 4)) =
+              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        ETR(5);
+        fence_proxy_async_smem();              // generic-proxy writes -> visible to the MMA (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_release(hs_full_c);
+        ETR(6);
+      }
+      // ---- LN epilogue: X2 = LN(Y + b2 + X1); output staged per warp in Hs (free after G2(last))
+      {
+        constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
+        float cv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {       // loads in flight while G2(last) finishes
+          const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+          cv[i] = k < D ? __ldg(b2 + k) : k < 2 * D ? __ldg(gamma + k - D) : k < 3 * D ? __ldg(beta + k - 2 * D) : 0.f;
+        }
+        ETR(0);
+        mbar_wait(y_full, ui & 1);            // Hs no longer read by the MMA
+        ETR(7);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+          if (k < 3 * D) s_b2[k] = cv[i];
+        }
+        asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+      }
+      // residual X1 = this unit's A tile, still resident (the next unit's A load waits for a_free)
+      const ResidualSmemA ra{sA, row_l, hh * (D / 2)};
+      uint8_t* stg0 = sHs + (warp - 4) * (MLP_STG * 2048);
+      int nst = 0;
+      ln_epilogue<D, D / 2>(t_row, hh * (D / 2), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+                            [&] {
+                              mbar_wait(y_full, ui & 1);
+                              tc_fence_after();
+                            },
+                            [&](const uint32_t (&p)[16], int col) {   // 32 rows x 32 columns per TMA store
+                              uint8_t* stg = stg0 + (nst % MLP_STG) * 2048;
+                              if (lane == 0 && nst >= MLP_STG) bulk_wait_read<MLP_STG - 1>();
+                              __syncwarp();
+#pragma unroll
+                              for (int i = 0; i < 4; ++i)
+                                *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) =
+                                    make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                              fence_proxy_async_smem();
+                              __syncwarp();
+                              if (lane == 0) {
+                                tma_store_2d(&tmOut, stg, col, m0 + q * 32);
+                                bulk_commit();
+                              }
+                              ++nst;
+                            });
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster(y_empty_c);
+        mbar_arrive(a_free);                   // this CTA's A tile no longer read (residual done)
+        bulk_wait_read<0>();                   // staged output read before Hs is overwritten
+      }
+      // LN constants / stats (in Hs) consumed before the next unit's first chunk overwrites Hs
+      ETR(10);
+      asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+      ETR(11);
+    }
+    if (lane == 0) bulk_wait_all();
+#ifdef MLP_TRACE
+    if (lane == 0 && blockIdx.x < 1)
+      printf("MLP_EPI warp %d chunks %u | h_full %lld ld %lld gelu %lld hs_empty %lld write %lld fence+arrive %lld "
+             "| y_full %lld consts %lld bar5a %lld LN %lld bar5b %lld | LN pass1 %lld bar %lld pass2 %lld\n", warp, hc,
+             et[0], et[1], et[2], et[3], et[4], et[5], et[6], et[7], et[8], et[9], et[10],
+#ifdef LN_TRACE
+             g_ln_trace[warp][0], g_ln_trace[warp][1], g_ln_trace[warp][2]
+#else
+             0ll, 0ll, 0ll
+#endif
+             );
+#endif
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    __syncwarp();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+template <int D>
+cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
+  using T = MlpCfg<D>;
+  auto kern = mlp_tc_kernel<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t n_units = (a.M + 2 * MBM - 1) / (2 * MBM);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int pairs = int(std::min<int64_t>(n_units, (sms > 0 ? sms : 148) / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(2 * pairs));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = size_t(T::SMEM);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, *a.tmX1, *a.tmW1, *a.tmW2, *a.tmOut, *a.tmX1, int(a.M), a.F, a.b1, a.b2,
+                            a.gamma, a.beta, a.res, a.eps);
+}
+
+}  // namespace
+
+bool mlp_fused_supported(int d, int ffn) { return (d == 384 || d == 64) && ffn % FC == 0 && ffn > 0; }
+
+cudaError_t launch_mlp(const MlpArgs& a, cudaStream_t st) {
+  if (a.M <= 0) return cudaSuccess;
+  if (!mlp_fused_supported(a.D, a.F)) return cudaErrorInvalidValue;
+  switch (a.D) {
+    case 64: return launch_mlp_t<64>(a, st);
+    case 384: return launch_mlp_t<384>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace surge

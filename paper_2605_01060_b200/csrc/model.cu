@@ -161,6 +161,10 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(int(d), int(d), ln_epi)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), ln_epi)));
+      if (mlp_fused_supported(int(d), int(f))) {
+        SURGE_TRY(make_tmap_bf16(&L.tm_w1_mlp, L.w1, f, d, 64));
+        SURGE_TRY(make_tmap_bf16(&L.tm_w2_mlp, L.w2, d, f, mlp_w2_box_rows(int(d))));
+      }
     }
     return cudaSuccess;
   }();
@@ -326,6 +330,15 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln1_g, L.ln1_b, s_.eps, ws.X1, st));
     }
     if (P) prof->end(KK_OUT_LN, st, ev, 2 * M * D * D, 2 * (M * D + D * D + 2 * M * D));
+    if (mlp_fused_ && mlp_fused_supported(d, f)) {
+      // K7 + K8 fused: X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1), H stays on chip
+      MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, &smX, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b, ws.X1, s_.eps};
+      if (P) prof->begin(st, &ev);
+      SURGE_TRY(launch_mlp(a, st));
+      if (P) prof->end(KK_MLP, st, ev, 4 * M * F * D, 2 * (2 * F * D + 2 * M * D));
+      k += 1;
+      continue;
+    }
     // K7: H = GELU(X1 W1^T + b1)
     g.tmA = &tmX1; g.tmB = &L.tm_w1; g.tmC = &smH; g.tmR = nullptr; g.N = f; g.K = d; g.epi = EPI_BIAS_GELU; g.bias = L.b1; g.res = nullptr;
     g.gamma = g.beta = nullptr; g.C = ws.H;
@@ -344,7 +357,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln2_g, L.ln2_b, s_.eps, ws.X, st));
     }
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += (att_fused ? 4 : 5 + (max_len > 64 ? 1 : 0)) + (fused ? 0 : 2);
+    k += (att_fused ? 3 : 4 + (max_len > 64 ? 1 : 0)) + (fused ? 0 : 2);
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));

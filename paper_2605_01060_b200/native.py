@@ -71,8 +71,9 @@ class surge_kernel_profile(C.Structure):
 
 
 KERNEL_KINDS = ("embed_ln", "gemm_qkv", "attention", "gemm_out_ln", "gemm_ffn1_gelu", "gemm_ffn2_ln",
-                "meanpool_l2", "pack", "gemm_qkv_attn")
+                "meanpool_l2", "pack", "gemm_qkv_attn", "gemm_mlp")
 SURGE_OPT_ATT_FUSED = 1
+SURGE_OPT_MLP_FUSED = 2
 
 
 class surge_superbatch_info(C.Structure):

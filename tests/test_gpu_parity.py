@@ -221,10 +221,11 @@ def test_larger_encoder_classes_sample(N, enc, length_model):
         compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))
 
 
-def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0):
+def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True):
     h = N.surge_create(N.make_config(ecfg, 1000, 5000, chunk_tokens=chunk_tokens), pack_blob(ecfg, w))
     try:
         N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, 1 if fused else 0)
+        N.surge_set_option(h, N.SURGE_OPT_MLP_FUSED, 1 if mlp_fused else 0)
         out = torch.zeros(len(lens), ecfg.hidden, device="cuda")
         N.surge_encode_packed(h, torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(), lens, len(lens), out)
         torch.cuda.synchronize()
@@ -278,4 +279,23 @@ def test_fused_path_falls_back_for_long_texts(N):
     E = oenc.Encoder(ecfg, w)
     T = texts_of(ids, lens)
     rows = [0, 50, 51, 52, 300, 399]
+    compare(fused[rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+@pytest.mark.parametrize("enc,n_texts", [("toy", 300), ("minilm", 2500), ("minilm", 3)])
+def test_fused_mlp_matches_separate_gemms_and_oracle(N, enc, n_texts):
+    """K7+K8 fused (H on chip, ff-chunks through TMEM and shared memory) vs the separate FFN1 GELU
+    GEMM + FFN2 LN GEMM: bit-identical embeddings (same k-block order, shared LN epilogue); sampled
+    rows vs the oracle.  Sizes give ragged last 256-row units (and a single partial unit)."""
+    ecfg = ENCODERS[enc]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(11)
+    lens = rng.integers(1, min(64, ecfg.max_position) + 1, size=n_texts).astype(np.int32)
+    ids = rng.integers(4 if enc == "toy" else 1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    fused = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=16384, mlp_fused=True)
+    sep = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=16384, mlp_fused=False)
+    assert np.array_equal(fused, sep)
+    E = oenc.Encoder(ecfg, w)
+    T = texts_of(ids, lens)
+    rows = sorted({0, len(lens) - 1, *rng.integers(0, len(lens), size=min(10, len(lens))).tolist()})
     compare(fused[rows], np.stack([E.encode_text(T[i]) for i in rows]))

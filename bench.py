@@ -50,6 +50,8 @@ def parse():
                     help="1: K4 QKV GEMM + K5 attention as one kernel (default); 0: separate kernels")
     ap.add_argument("--mlp-fused", type=int, default=1, choices=[0, 1],
                     help="1: K7 FFN1+GELU and K8 FFN2+LN as one kernel (default); 0: separate GEMMs")
+    ap.add_argument("--tail-fused", type=int, default=1, choices=[0, 1],
+                    help="1: K6 out-proj+LN also inside the fused MLP kernel (default); 0: own kernel")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -232,6 +234,7 @@ def main():
     h = N.surge_create(cfg, blob_dev, n_weights=blob_dev.numel() // 2)
     N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, args.att_fused)
     N.surge_set_option(h, N.SURGE_OPT_MLP_FUSED, args.mlp_fused)
+    N.surge_set_option(h, N.SURGE_OPT_TAIL_FUSED, args.tail_fused)
     stream = torch.cuda.Stream(device=dev)
 
     sizes = wl.sizes.astype(np.int64)

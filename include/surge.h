@@ -292,7 +292,7 @@ surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const
  * Per-kernel-class device timing (CUDA events around every launch, on the launching stream).
  * Enable before a timed region, read after synchronising.  Classes: 0 embed_ln, 1 gemm_qkv,
  * 2 attention, 3 gemm_out_ln, 4 gemm_ffn1_gelu, 5 gemm_ffn2_ln, 6 meanpool_l2, 7 pack,
- * 8 gemm_qkv_attn (K4 + K5 fused), 9 gemm_mlp (K7 + K8 fused).
+ * 8 gemm_qkv_attn (K4 + K5 fused), 9 gemm_mlp (K7 + K8 fused), 10 gemm_tail (K6 + K7 + K8 fused).
  *   flops/bytes: ALGORITHMIC work of the launches (2*M*N*K for GEMMs; 4*d*sum(l^2) attention
  *   flops; minimal HBM bytes in+out for every class), summed over launches.
  */
@@ -316,6 +316,9 @@ typedef struct {
 /*   SURGE_OPT_MLP_FUSED (default 1): 1 = K7 FFN1 + GELU and K8 FFN2 + residual + LN run as one kernel
  *     (H kept on chip; hidden size 384 or 64); 0 = two GEMM kernels.  Bit-identical results. */
 #define SURGE_OPT_MLP_FUSED 2
+/*   SURGE_OPT_TAIL_FUSED (default 1; effective with SURGE_OPT_MLP_FUSED): K6 out-projection +
+ *     residual + LN also runs inside the fused MLP kernel (X1 kept on chip).  Bit-identical. */
+#define SURGE_OPT_TAIL_FUSED 3
 surge_status surge_set_option(surge_handle h, int32_t option, int64_t value);
 
 surge_status surge_profile_enable(surge_handle h, int32_t on);   /* on: clears counters */

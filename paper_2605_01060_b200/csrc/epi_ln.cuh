@@ -36,6 +36,27 @@ __device__ long long g_ln_trace[32][4];
 #define LNT(i) do {} while (0)
 #endif
 
+// Coalesced store of a warp's 32 rows x 32 bf16 columns (lane = row, p = its 64 bytes): transposed
+// through a 2 KB per-warp smem buffer (64-byte rows, 16-byte chunks XOR-swizzled by (row / 2) % 4,
+// conflict-free both ways), then each store instruction writes 8 whole 64-byte row segments.
+// Plain st.global: no wait on the TMA unit (whose queue is shared with the producers' loads).
+__device__ __forceinline__ void store_rows_32x32(uint8_t* stg, const uint32_t (&p)[16], int lane, uint16_t* out,
+                                                 int64_t row0, int64_t rows, int ld, int col) {
+  __syncwarp();   // previous use of stg drained
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) =
+        make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+  __syncwarp();
+  const int c = lane & 3;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int r = 8 * t + (lane >> 2);
+    const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+    if (row0 + r < rows) *reinterpret_cast<uint4*>(out + size_t(row0 + r) * ld + col + 8 * c) = v;
+  }
+}
+
 template <int BN, int HALF, typename Res, typename Ready, typename Store>
 __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
                                             const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,

@@ -563,12 +563,15 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       } else {
         // LayerNorm over the full row (BN == N), two warps per row (column halves): epi_ln.cuh
         const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + c_lo};
+        uint8_t* stg = sStg + (warp - 4) * T::STG_BUFS * 2048;
         ln_epilogue<BN, T::HALF>(taddr, c_lo, rg, s_bias, s_gamma, s_beta, stats + (it & 1) * 2 * BM, q, hh, lane,
                                  eps, [&] {
                                    mbar_wait(&tfull[acc], aph);
                                    tc_fence_after();
                                  },
-                                 stage_store);
+                                 [&](const uint32_t (&p)[16], int col) {
+                                   store_rows_32x32(stg, p, lane, C, m0 + q * 32, M, N, col);
+                                 });
       }
       if constexpr (!T::ATT) {
         tc_fence_before();

@@ -79,14 +79,17 @@ inline bool fused_ln(int d) { return d == 64 || d == 384; }
 
 // K7 + K8 fused (mlp_tc.cu): X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1) * gamma + beta, H kept on chip.
 struct MlpArgs {
-  const CUtensorMap* tmX1;   // X1 [M x D] load map, box 128 rows (also the residual prefetch map)
+  const CUtensorMap* tmA;    // A [M x D] load map, box 128 rows: X1, or O when tmWo is set
   const CUtensorMap* tmW1;   // W1 [F x D], box 64 rows
-  const CUtensorMap* tmW2;   // W2 [D x F], box D/4 rows (D = 384) or D/2 (D = 64)
-  const CUtensorMap* tmOut;  // X [M x D] store map (make_tmap_store_bf16)
+  const CUtensorMap* tmW2;   // W2 [D x F], box mlp_w2_box_rows(D)
+  const CUtensorMap* tmWo;   // nullptr, or Wo [D x D] (box mlp_w2_box_rows(D)): K6 fused as a prologue
+  const CUtensorMap* tmX;    // X [M x D] load map (L2 prefetch of the K6 residual rows), when tmWo is set
   int64_t M;
   int D, F;
-  const float *b1, *b2, *gamma, *beta;
-  const uint16_t* res;       // X1 (residual rows)
+  const float *b1, *b2, *gamma, *beta;       // FFN biases, LN_o
+  const float *bo, *gamma1, *beta1;          // K6: out-proj bias, LN_a (when tmWo is set)
+  const uint16_t* x;         // X (K6 residual rows; when tmWo is set)
+  uint16_t* out;             // X [M x D] output (in place over x when tmWo is set)
   float eps;
 };
 bool mlp_fused_supported(int d, int ffn);
@@ -122,7 +125,7 @@ cudaError_t launch_bf16_to_f32(const uint16_t* in, float* out, int64_t n, cudaSt
 // --------------------------------------------------------------------- per-kernel-class timing
 enum KernelKind : int {
   KK_EMBED = 0, KK_QKV = 1, KK_ATTN = 2, KK_OUT_LN = 3, KK_FFN1 = 4, KK_FFN2 = 5, KK_POOL = 6, KK_PACK = 7,
-  KK_QKV_ATTN = 8, KK_MLP = 9, KK_COUNT = 10
+  KK_QKV_ATTN = 8, KK_MLP = 9, KK_TAIL = 10, KK_COUNT = 11
 };
 
 // Records a CUDA event pair around launches of each kind (only when enabled).  Not thread-safe:
@@ -156,7 +159,7 @@ struct LayerW {
   uint16_t *wqkv, *wo, *w1, *w2;      // bf16 [3d x d], [d x d], [ff x d], [d x ff]
   float *bqkv, *bo, *ln1_g, *ln1_b, *b1, *b2, *ln2_g, *ln2_b;
   CUtensorMap tm_wqkv, tm_wo, tm_w1, tm_w2;
-  CUtensorMap tm_w1_mlp, tm_w2_mlp;   // fused MLP (mlp_tc.cu) views of W1 / W2
+  CUtensorMap tm_wo_mlp, tm_w1_mlp, tm_w2_mlp;   // fused tail (mlp_tc.cu) views of Wo / W1 / W2
   uint16_t* wqkv_att = nullptr;       // W_qkv rows permuted into head-complete 192-row slices
   float* bqkv_att = nullptr;
   CUtensorMap tm_wqkv_att;
@@ -204,11 +207,14 @@ class DeviceModel {
   bool att_fused() const { return att_fused_; }
   // fused MLP kernel on/off (on by default; off = separate K7 GELU GEMM + K8 LN GEMM)
   void set_mlp_fused(bool on) { mlp_fused_ = on; }
+  // out-projection + LN fused into the MLP kernel as a prologue (on by default; needs mlp fused)
+  void set_tail_fused(bool on) { tail_fused_ = on; }
 
  private:
   ModelShape s_{};
   bool att_fused_ = true;
   bool mlp_fused_ = true;
+  bool tail_fused_ = true;
   std::vector<void*> allocs_;
   uint16_t *word_ = nullptr, *pos_ = nullptr, *type_ = nullptr;
   float *emb_g_ = nullptr, *emb_b_ = nullptr;

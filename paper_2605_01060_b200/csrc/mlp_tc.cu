@@ -105,13 +105,18 @@ __device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_add
 }
 
 // Persistent CTA-pair kernel; unit u = rows [256 u, 256 u + 256), CTA rank r owns [256 u + 128 r, +128).
-template <int D>
+// OP (out-projection prologue, K6 fused too): A = O, and per unit first Y = O Wo^T (G0), then the
+// LN0 epilogue writes X1 = LN_a(Y + bo + X) as bf16 into the A tile (O is dead by then), and the
+// FFN runs on that X1; X1 never reaches HBM.  The final output overwrites X in place (each CTA reads
+// its LN0 residual rows of X before it writes them).
+template <int D, bool OP>
 __global__ void __launch_bounds__(THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmW1,
-                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmOut,
+                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmWo,
                   const __grid_constant__ CUtensorMap tmR, int M, int F, const float* __restrict__ b1,
                   const float* __restrict__ b2, const float* __restrict__ gamma, const float* __restrict__ beta,
-                  const uint16_t* __restrict__ res, float eps) {
+                  const float* __restrict__ bo, const float* __restrict__ gamma1, const float* __restrict__ beta1,
+                  const uint16_t* __restrict__ xres, uint16_t* __restrict__ out, float eps) {
   using T = MlpCfg<D>;
   constexpr int KB1 = T::KB1;
   constexpr int S1 = KB1 == 1 ? 1 : KB1 / 3;         // ring stages per W1 chunk
@@ -129,7 +134,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* y_full = hs_empty + 1;                           // both
   uint64_t* y_empty = y_full + 1;                            // leader, 2 x EPI_WARPS arrivals
   uint64_t* a_free = y_empty + 1;                            // local: LN read its residual from A
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_free + 1);
+  uint64_t* y0_full = a_free + 1;                            // both (OP): G0 retired
+  uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x1_ready + 1);
   uint8_t* sA = smem + T::HEAD;                              // [KB1][128 x 128 B]
   uint8_t* sHs = sA + T::A_BYTES;                            // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
@@ -162,6 +169,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(y_full, 1);
     mbar_init(y_empty, 2 * EPI_WARPS);
     mbar_init(a_free, EPI_WARPS);
+    mbar_init(y0_full, 1);
+    mbar_init(x1_ready, 2 * EPI_WARPS);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -208,6 +217,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                              j * T::N2 + rank * T::B2_BOX, pol_w);
         }
       };
+      auto ring_wo = [&]() {                             // OP: Wo k-blocks in the W2 stage format
+        for (int kb = 0; kb < KB1; ++kb, ++sc) {
+          const int s = int(sc % RING);
+          const uint32_t ph = (sc / RING) & 1;
+          if (int(sc % 3) != p) continue;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * T::N2_MMAS * T::B2_BOX * 128);
+          for (int j = 0; j < T::N2_MMAS; ++j)
+            tma_load_2d_pair(sW + s * STAGE + j * T::B2_BOX * 128, &tmWo, full_c + uint32_t(s) * 8, kb * 64,
+                             j * T::N2 + rank * T::B2_BOX, pol_w);
+        }
+      };
       for (int u = unit0; u < n_units; u += units, ++ui) {
         const int m0 = u * 2 * MBM + rank * MBM;
         if (p == 0) {                                    // A: this CTA's rows, once per unit
@@ -219,7 +240,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           // warm L2 with the next unit's rows: its A load waits for this unit's LN (residual from A)
           if (MLP_PREFETCH && u + units < n_units)
             for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmX1, kb * 64, m0 + units * 2 * MBM);
+          if constexpr (OP)                              // LN0 residual rows (X), read from L2
+            for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmR, kb * 64, m0);
         }
+        if constexpr (OP) ring_wo();
         for (int c = 0; c < NCH; ++c) {
           ring_w1(c);
           if (c > 0) ring_w2(c - 1);
@@ -243,7 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t gc = 0;        // chunks issued (G2) -> hs_full / hs_empty phases
     int ui = 0;
     auto g2 = [&](int c, int uiu) {
-      if (c == 0) {
+      if (!OP && c == 0) {
         MW(y_empty, (uiu & 1) ^ 1, 0);               // LN of the previous unit drained Y
         tc_fence_after();
       }
@@ -276,6 +300,32 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int u = unit0; u < n_units; u += units, ++ui) {
       MW(a_full, ui & 1, 3);
       tc_fence_after();
+      if constexpr (OP) {
+        // G0: Y = O Wo^T (the previous unit's final LN has drained Y)
+        MW(y_empty, (ui & 1) ^ 1, 0);
+        tc_fence_after();
+        for (int kb = 0; kb < KB1; ++kb, ++sc) {
+          const int s = int(sc % RING);
+          MW(&full[s], (sc / RING) & 1, 2);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = a_desc0 + uint64_t((kb * MBM * 128) >> 4);
+            const uint64_t bd = w_desc0 + uint64_t((s * STAGE) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int j = 0; j < T::N2_MMAS; ++j)
+                tc_mma_bf16_pair(tmem_base + j * T::N2, ad + uint64_t(k * 2),
+                                 bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, (kb | k) != 0);
+            tc_commit_pair_mc(&empty[s], 0x3);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) tc_commit_pair_mc(y0_full, 0x3);
+        __syncwarp();
+        MW(x1_ready, ui & 1, 1);                      // both CTAs' X1 written into A
+        tc_fence_after();
+      }
       for (int c = 0; c < NCH; ++c) {
         MW(h_empty, (hc & 1) ^ 1, 4);                // epilogue drained H(c-1)
         tc_fence_after();
@@ -330,8 +380,47 @@ __global__ void __launch_bounds__(THREADS, 1)
 #else
 #define ETR(i) do {} while (0)
 #endif
+    const uint32_t x1_ready_c = mapa_shared(smem_u32(x1_ready), 0);
     for (int u = unit0; u < n_units; u += units, ++ui) {
       const int m0 = u * 2 * MBM + rank * MBM;
+      if constexpr (OP) {
+        // ---- LN0 epilogue (K6): X1 = LN_a(Y + bo + X) -> bf16 into the A tile (swizzled K-major)
+        {
+          constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
+          float cv[PER];
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+            cv[i] = k < D ? __ldg(bo + k) : k < 2 * D ? __ldg(gamma1 + k - D) : k < 3 * D ? __ldg(beta1 + k - 2 * D) : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {     // Hs idle: the previous unit's LN is done, chunk 0 not yet
+            const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+            if (k < 3 * D) s_b2[k] = cv[i];
+          }
+          asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+        }
+        const int row = m0 + row_l;
+        const ResidualGlobal rg{xres + size_t(row < M ? row : 0) * D + hh * (D / 2)};
+        ln_epilogue<D, D / 2>(t_row, hh * (D / 2), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+                              [&] {
+                                mbar_wait(y0_full, ui & 1);
+                                tc_fence_after();
+                              },
+                              [&](const uint32_t (&p)[16], int col) {   // row row_l, columns col .. col+31
+                                uint8_t* base = sA + (col >> 6) * (MBM * 128) + row_l * 128;
+                                const int j0 = (col & 63) >> 3;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                  *reinterpret_cast<uint4*>(base + (((j0 + i) ^ (row_l & 7)) << 4)) =
+                                      make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                              });
+        tc_fence_before();                     // Y reads done before G2(0) may accumulate into Y
+        fence_proxy_async_smem();              // X1 (generic writes) -> visible to the MMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_release(x1_ready_c);
+        asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");   // LN0 scratch free
+      }
       for (int c = 0; c < NCH; ++c, ++hc) {
         // H(c) columns [64 hh, 64 hh + 64) of this row: TMEM -> registers, then release the accumulator
         const float4* bp = reinterpret_cast<const float4*>(b1 + c * FC + 64 * hh);
@@ -400,34 +489,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       // residual X1 = this unit's A tile, still resident (the next unit's A load waits for a_free)
       const ResidualSmemA ra{sA, row_l, hh * (D / 2)};
       uint8_t* stg0 = sHs + (warp - 4) * (MLP_STG * 2048);
-      int nst = 0;
       ln_epilogue<D, D / 2>(t_row, hh * (D / 2), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();
                             },
-                            [&](const uint32_t (&p)[16], int col) {   // 32 rows x 32 columns per TMA store
-                              uint8_t* stg = stg0 + (nst % MLP_STG) * 2048;
-                              if (lane == 0 && nst >= MLP_STG) bulk_wait_read<MLP_STG - 1>();
-                              __syncwarp();
-#pragma unroll
-                              for (int i = 0; i < 4; ++i)
-                                *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) =
-                                    make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
-                              fence_proxy_async_smem();
-                              __syncwarp();
-                              if (lane == 0) {
-                                tma_store_2d(&tmOut, stg, col, m0 + q * 32);
-                                bulk_commit();
-                              }
-                              ++nst;
+                            [&](const uint32_t (&p)[16], int col) {
+                              store_rows_32x32(stg0, p, lane, out, m0 + q * 32, M, D, col);
                             });
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_cluster(y_empty_c);
         mbar_arrive(a_free);                   // this CTA's A tile no longer read (residual done)
-        bulk_wait_read<0>();                   // staged output read before Hs is overwritten
       }
       // LN constants / stats (in Hs) consumed before the next unit's first chunk overwrites Hs
       ETR(10);
@@ -456,10 +530,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int D>
+template <int D, bool OP>
 cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
   using T = MlpCfg<D>;
-  auto kern = mlp_tc_kernel<D>;
+  auto kern = mlp_tc_kernel<D, OP>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
@@ -483,8 +557,10 @@ cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, *a.tmX1, *a.tmW1, *a.tmW2, *a.tmOut, *a.tmX1, int(a.M), a.F, a.b1, a.b2,
-                            a.gamma, a.beta, a.res, a.eps);
+  const CUtensorMap& tmWo = OP ? *a.tmWo : *a.tmW2;
+  const CUtensorMap& tmR = OP ? *a.tmX : *a.tmA;
+  return cudaLaunchKernelEx(&cfg, kern, *a.tmA, *a.tmW1, *a.tmW2, tmWo, tmR, int(a.M), a.F, a.b1, a.b2, a.gamma,
+                            a.beta, a.bo, a.gamma1, a.beta1, a.x, a.out, a.eps);
 }
 
 }  // namespace
@@ -494,9 +570,10 @@ bool mlp_fused_supported(int d, int ffn) { return (d == 384 || d == 64) && ffn %
 cudaError_t launch_mlp(const MlpArgs& a, cudaStream_t st) {
   if (a.M <= 0) return cudaSuccess;
   if (!mlp_fused_supported(a.D, a.F)) return cudaErrorInvalidValue;
+  const bool op = a.tmWo != nullptr;
   switch (a.D) {
-    case 64: return launch_mlp_t<64>(a, st);
-    case 384: return launch_mlp_t<384>(a, st);
+    case 64: return op ? launch_mlp_t<64, true>(a, st) : launch_mlp_t<64, false>(a, st);
+    case 384: return op ? launch_mlp_t<384, true>(a, st) : launch_mlp_t<384, false>(a, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -162,6 +162,7 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), ln_epi)));
       if (mlp_fused_supported(int(d), int(f))) {
+        SURGE_TRY(make_tmap_bf16(&L.tm_wo_mlp, L.wo, d, d, mlp_w2_box_rows(int(d))));
         SURGE_TRY(make_tmap_bf16(&L.tm_w1_mlp, L.w1, f, d, 64));
         SURGE_TRY(make_tmap_bf16(&L.tm_w2_mlp, L.w2, d, f, mlp_w2_box_rows(int(d))));
       }
@@ -306,6 +307,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_gemm(g, st));
       if (P) prof->end(KK_QKV_ATTN, st, ev, 2 * M * 3 * D * D + 4 * D * sum_l2, 2 * (M * D + 3 * D * D + M * D));
       g.att_rec = nullptr; g.n_att_tiles = 0;
+      k += 1;
     } else {
       // K4: QKV = X Wqkv^T + b
       g.tmA = &tmX; g.tmB = &L.tm_wqkv; g.tmC = &smQKV; g.N = 3 * d; g.K = d; g.epi = EPI_BIAS; g.bias = L.bqkv; g.C = ws.QKV;
@@ -317,6 +319,17 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st,
                                  host_cu ? ws.long_idx : nullptr, int32_t(long_texts.size())));
       if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
+      k += 2 + (max_len > 64 ? 1 : 0);
+    }
+    if (tail_fused_ && mlp_fused_ && mlp_fused_supported(d, f)) {
+      // K6 + K7 + K8 fused: X = LN_o(FFN(X1) + X1), X1 = LN_a(O Wo^T + bo + X) kept on chip
+      MlpArgs a{&tmO, &L.tm_w1_mlp, &L.tm_w2_mlp, &L.tm_wo_mlp, &tmX, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
+                L.bo, L.ln1_g, L.ln1_b, ws.X, ws.X, s_.eps};
+      if (P) prof->begin(st, &ev);
+      SURGE_TRY(launch_mlp(a, st));
+      if (P) prof->end(KK_TAIL, st, ev, 2 * M * D * D + 4 * M * F * D, 2 * (D * D + 2 * F * D + 3 * M * D));
+      k += 1;
+      continue;
     }
     // K6: X1 = LN(O Wo^T + bo + X)
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
@@ -330,9 +343,11 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln1_g, L.ln1_b, s_.eps, ws.X1, st));
     }
     if (P) prof->end(KK_OUT_LN, st, ev, 2 * M * D * D, 2 * (M * D + D * D + 2 * M * D));
+    k += fused ? 1 : 2;
     if (mlp_fused_ && mlp_fused_supported(d, f)) {
       // K7 + K8 fused: X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1), H stays on chip
-      MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, &smX, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b, ws.X1, s_.eps};
+      MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, nullptr, nullptr, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
+                nullptr, nullptr, nullptr, nullptr, ws.X, s_.eps};
       if (P) prof->begin(st, &ev);
       SURGE_TRY(launch_mlp(a, st));
       if (P) prof->end(KK_MLP, st, ev, 4 * M * F * D, 2 * (2 * F * D + 2 * M * D));
@@ -357,7 +372,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln2_g, L.ln2_b, s_.eps, ws.X, st));
     }
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += (att_fused ? 3 : 4 + (max_len > 64 ? 1 : 0)) + (fused ? 0 : 2);
+    k += fused ? 2 : 3;
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));

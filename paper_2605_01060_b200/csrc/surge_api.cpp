@@ -1077,6 +1077,10 @@ surge_status surge_set_option(surge_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
       c->model.set_mlp_fused(value != 0);
       return SURGE_OK;
+    case SURGE_OPT_TAIL_FUSED:
+      if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
+      c->model.set_tail_fused(value != 0);
+      return SURGE_OK;
   }
   return SURGE_E_INVALID_ARG;
 }

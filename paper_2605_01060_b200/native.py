@@ -71,9 +71,10 @@ class surge_kernel_profile(C.Structure):
 
 
 KERNEL_KINDS = ("embed_ln", "gemm_qkv", "attention", "gemm_out_ln", "gemm_ffn1_gelu", "gemm_ffn2_ln",
-                "meanpool_l2", "pack", "gemm_qkv_attn", "gemm_mlp")
+                "meanpool_l2", "pack", "gemm_qkv_attn", "gemm_mlp", "gemm_tail")
 SURGE_OPT_ATT_FUSED = 1
 SURGE_OPT_MLP_FUSED = 2
+SURGE_OPT_TAIL_FUSED = 3
 
 
 class surge_superbatch_info(C.Structure):

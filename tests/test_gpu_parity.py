@@ -221,11 +221,12 @@ def test_larger_encoder_classes_sample(N, enc, length_model):
         compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))
 
 
-def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True):
+def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True, tail_fused=True):
     h = N.surge_create(N.make_config(ecfg, 1000, 5000, chunk_tokens=chunk_tokens), pack_blob(ecfg, w))
     try:
         N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, 1 if fused else 0)
         N.surge_set_option(h, N.SURGE_OPT_MLP_FUSED, 1 if mlp_fused else 0)
+        N.surge_set_option(h, N.SURGE_OPT_TAIL_FUSED, 1 if tail_fused else 0)
         out = torch.zeros(len(lens), ecfg.hidden, device="cuda")
         N.surge_encode_packed(h, torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(), lens, len(lens), out)
         torch.cuda.synchronize()
@@ -284,16 +285,19 @@ def test_fused_path_falls_back_for_long_texts(N):
 
 @pytest.mark.parametrize("enc,n_texts", [("toy", 300), ("minilm", 2500), ("minilm", 3)])
 def test_fused_mlp_matches_separate_gemms_and_oracle(N, enc, n_texts):
-    """K7+K8 fused (H on chip, ff-chunks through TMEM and shared memory) vs the separate FFN1 GELU
-    GEMM + FFN2 LN GEMM: bit-identical embeddings (same k-block order, shared LN epilogue); sampled
-    rows vs the oracle.  Sizes give ragged last 256-row units (and a single partial unit)."""
+    """K7+K8 fused (H on chip, ff-chunks through TMEM and shared memory), and K6+K7+K8 fused (the
+    out-projection + LN as its prologue, X1 on chip) vs the separate K6 LN GEMM, FFN1 GELU GEMM and
+    FFN2 LN GEMM: bit-identical embeddings (same k-block order, shared LN epilogue); sampled rows vs
+    the oracle.  Sizes give ragged last 256-row units (and a single partial unit)."""
     ecfg = ENCODERS[enc]
     w = make_weights(ecfg, seed=1234)
     rng = np.random.default_rng(11)
     lens = rng.integers(1, min(64, ecfg.max_position) + 1, size=n_texts).astype(np.int32)
     ids = rng.integers(4 if enc == "toy" else 1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
     fused = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=16384, mlp_fused=True)
+    mlp_only = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=16384, mlp_fused=True, tail_fused=False)
     sep = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=16384, mlp_fused=False)
+    assert np.array_equal(mlp_only, sep)
     assert np.array_equal(fused, sep)
     E = oenc.Encoder(ecfg, w)
     T = texts_of(ids, lens)

@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
   uint64_t* tfull = empty + T::MAX_STAGES;              // [ACC]
   uint64_t* tempty = tfull + 2;                         // [ACC]
   uint64_t* bfull = tempty + 2;                         // resident B slice landed (WS)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* att_gate = bfull + 1;                       // ATT: the attention phase of a tile is done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(att_gate + 1);
   float4* stats = reinterpret_cast<float4*>(smem + T::HEAD_BYTES);                  // [2][2][BM]
   float* s_bias = reinterpret_cast<float*>(stats + 2 * 2 * BM);                      // LN: [BN] each
   float* s_gamma = s_bias + BN;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       mbar_init(&tempty[a], (PAIR ? 2 : 1) * T::EPI_WARPS);
     }
     mbar_init(bfull, 1);
+    mbar_init(att_gate, (PAIR ? 2 : 1) * T::EPI_WARPS);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -307,6 +309,15 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       const int acc = it % ACC;
       const uint32_t aph = (it / ACC) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
+#ifndef ATT_GATE
+#define ATT_GATE 1
+#endif
+      if constexpr (T::ATT) {
+        // legacy mma.sync (the attention) is starved while tcgen05 MMAs run on the SM
+        // (scripts/microbench/umma_hmma.cu: ~0.01 vs 0.46 HMMA/clk): the next tile's MMAs wait until
+        // the previous tile's attention phase is over, instead of stretching it
+        if (ATT_GATE && it >= 1) mbar_wait(att_gate, (it - 1) & 1);
+      }
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * BN;
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -453,7 +464,10 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
         const int row0 = R[0], nrows = R[1], ntexts = R[2], nunits = R[3];
         const uint8_t* tstart = reinterpret_cast<const uint8_t*>(R + 4);
         const uint16_t* units = reinterpret_cast<const uint16_t*>(R + 36);
-        constexpr int NHU = DH == 16 ? 2 : 1;   // heads per unit (internal.h att_unit_heads)
+#ifndef ATT_NHU32
+#define ATT_NHU32 2
+#endif
+        constexpr int NHU = DH == 16 ? 2 : DH == 32 ? ATT_NHU32 : 1;   // heads per unit (internal.h att_unit_heads)
         constexpr int W = T::EPI_WARPS;
         const int w = warp - 4;
 #pragma unroll 1
@@ -477,6 +491,11 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
           attn_store_tile<DH, NHU>(sQt, LDS, qt, len, lane, o, ia, ib);
         }
         ATT_TR(4);
+        __syncwarp();
+        if (lane == 0) {                          // attention of this tile done (its HMMAs retired)
+          if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(att_gate), 0));
+          else mbar_arrive(att_gate);
+        }
         named_bar_sync(1, T::EPI_WARPS * 32);   // O complete
         ATT_TR(5);
         {

@@ -57,7 +57,9 @@ __device__ __forceinline__ void store_rows_32x32(uint8_t* stg, const uint32_t (&
   }
 }
 
-template <int BN, int HALF, typename Res, typename Ready, typename Store>
+// NP warps share a lane quadrant, each owning HALF = BN / NP columns (part hh).  PIPE: TMEM loads and
+// residual loads one step ahead (2 register buffers); !PIPE: one buffer (for register-limited kernels).
+template <int BN, int HALF, bool PIPE = true, typename Res, typename Ready, typename Store, int NP = BN / HALF>
 __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
                                             const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,
                                             int lane, float eps, Ready&& wait_ready, Store&& store) {
@@ -65,8 +67,9 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   long long _lt = 0;
 #endif
   constexpr int NSTEP = HALF / 32;
-  uint32_t r[2][32];
-  uint32_t rs[2][16];
+  constexpr int NB = PIPE ? 2 : 1;
+  uint32_t r[NB][32];
+  uint32_t rs[NB][16];
   load_res(0, rs[0]);
   wait_ready();
   LNT(0);
@@ -75,10 +78,14 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   f32x2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < NSTEP; ++k) {
-    const int cur = k & 1;
+    const int cur = PIPE ? (k & 1) : 0;
     const int c = c_lo + 32 * k;
+    if (!PIPE && k > 0) {
+      tmem_ld32(taddr + c, r[0]);
+      load_res(k, rs[0]);
+    }
     tmem_ld_wait_regs(r[cur]);
-    if (k + 1 < NSTEP) {
+    if (PIPE && k + 1 < NSTEP) {
       tmem_ld32(taddr + c + 32, r[cur ^ 1]);
       load_res(k + 1, rs[cur ^ 1]);
     }
@@ -103,24 +110,47 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   LNT(1);
   const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
   stats[hh * 128 + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");   // the two warps of this quadrant
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NP) : "memory");   // the NP warps of this quadrant
   LNT(2);
-  const float4 o = stats[(hh ^ 1) * 128 + q * 32 + lane];
   const float nh = float(HALF);
-  const float mean_a = shift + S1 / nh, m2_a = S2 - S1 * S1 / nh;
-  const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
-  const float dm = mean_a - mean_b;
-  const float mean = 0.5f * (mean_a + mean_b);
-  const float var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
+  float mean, var;
+  if constexpr (NP == 2) {
+    const float4 o = stats[(hh ^ 1) * 128 + q * 32 + lane];
+    const float mean_a = shift + S1 / nh, m2_a = S2 - S1 * S1 / nh;
+    const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
+    const float dm = mean_a - mean_b;
+    mean = 0.5f * (mean_a + mean_b);
+    var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
+  } else {
+    // Chan's parallel merge of NP equal-size parts, in part order (identical in every warp)
+    float mp[NP], m2p[NP];
+    float msum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const float4 o = stats[i * 128 + q * 32 + lane];
+      mp[i] = o.x + o.y / nh;
+      m2p[i] = o.z - o.y * o.y / nh;
+      msum += mp[i];
+    }
+    mean = msum * (1.0f / NP);
+    float m2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const float dm = mp[i] - mean;
+      m2 += m2p[i] + nh * dm * dm;
+    }
+    var = fmaxf(m2 / float(BN), 0.f);
+  }
   const float rstd = rsqrtf(var + eps);
   const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);
   tmem_ld32(taddr + c_lo, r[0]);
 #pragma unroll
   for (int k = 0; k < NSTEP; ++k) {
-    const int cur = k & 1;
+    const int cur = PIPE ? (k & 1) : 0;
     const int c = c_lo + 32 * k;
+    if (!PIPE && k > 0) tmem_ld32(taddr + c, r[0]);
     tmem_ld_wait_regs(r[cur]);
-    if (k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+    if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
     uint32_t p[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {

@@ -42,7 +42,12 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 #endif
 constexpr int RING = MLP_RING;      // weight ring stages
 constexpr int STAGE = 24 * 1024;    // 3 W1 k-blocks (64 rows x 128 B each) or 1 W2 k-block (2 x 96 rows)
-constexpr int EPI_WARPS = 8;
+#ifndef MLP_EPI_WARPS
+#define MLP_EPI_WARPS 8   // 16 measured slower (tail 2148 -> 2344 ms/step: 96-register cap)
+#endif
+constexpr int EPI_WARPS = MLP_EPI_WARPS;   // 4 lane quadrants x NP column parts
+constexpr int NP = EPI_WARPS / 4;
+constexpr int HC = FC / NP;                // H-chunk columns per epilogue warp
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr uint32_t H_COL = 384;     // TMEM column of the H chunk
 
@@ -60,7 +65,7 @@ struct MlpCfg {
   // LN scratch (aliases Hs, which is idle during the LN): output staging [8 warps][MLP_STG][2 KB],
   // stats [2 halves][128] float4, b2 / gamma / beta
   static constexpr int LN_STG = EPI_WARPS * MLP_STG * 2048;
-  static constexpr int LN_SCRATCH = ((LN_STG + 2 * MBM * 16 + 3 * D * 4 + 1023) / 1024) * 1024;
+  static constexpr int LN_SCRATCH = ((LN_STG + NP * MBM * 16 + 3 * D * 4 + 1023) / 1024) * 1024;
   static constexpr int SCRATCH = LN_SCRATCH > HS_BYTES ? LN_SCRATCH : HS_BYTES;
   static constexpr int SMEM = 1024 + HEAD + A_BYTES + SCRATCH + RING * STAGE;
   static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sA = smem + T::HEAD;                              // [KB1][128 x 128 B]
   uint8_t* sHs = sA + T::A_BYTES;                            // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
-  float* s_b2 = reinterpret_cast<float*>(stats + 2 * MBM);   // LN only
+  float* s_b2 = reinterpret_cast<float*>(stats + NP * MBM);  // LN only
   float* s_gamma = s_b2 + D;
   float* s_beta = s_gamma + D;
   uint8_t* sW = sHs + T::SCRATCH;                            // [RING][STAGE]
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue (warps 4..11)
     const int q = warp & 3;                    // TMEM lane quadrant
-    const int hh = (warp - 4) >> 2;            // column half
+    const int hh = (warp - 4) >> 2;            // column part (0 .. NP-1)
     const int row_l = q * 32 + lane;           // row within the CTA tile
     const uint32_t hs_full_c = mapa_shared(smem_u32(hs_full), 0);
     const uint32_t h_empty_c = mapa_shared(smem_u32(h_empty), 0);
@@ -401,8 +406,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
         }
         const int row = m0 + row_l;
-        const ResidualGlobal rg{xres + size_t(row < M ? row : 0) * D + hh * (D / 2)};
-        ln_epilogue<D, D / 2>(t_row, hh * (D / 2), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+        const ResidualGlobal rg{xres + size_t(row < M ? row : 0) * D + hh * (D / NP)};
+        ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
                                 tc_fence_after();
@@ -422,31 +427,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");   // LN0 scratch free
       }
       for (int c = 0; c < NCH; ++c, ++hc) {
-        // H(c) columns [64 hh, 64 hh + 64) of this row: TMEM -> registers, then release the accumulator
-        const float4* bp = reinterpret_cast<const float4*>(b1 + c * FC + 64 * hh);
-        float4 bb[16];
+        // H(c) columns [HC hh, HC hh + HC) of this row: TMEM -> registers, then release the accumulator
+        const float4* bp = reinterpret_cast<const float4*>(b1 + c * FC + HC * hh);
+        float4 bb[HC / 4];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) bb[i] = __ldg(bp + i);
-        uint32_t r0[32], r1[32];
+        for (int i = 0; i < HC / 4; ++i) bb[i] = __ldg(bp + i);
+        uint32_t rh[HC];
         ETR(0);
         mbar_wait(h_full, hc & 1);
         ETR(1);
         tc_fence_after();
-        tmem_ld32(t_row + H_COL + 64 * hh, r0);
-        tmem_ld32(t_row + H_COL + 64 * hh + 32, r1);
-        tmem_ld_wait_regs(r0);
-        tmem_ld_wait_regs(r1);
+#pragma unroll
+        for (int s = 0; s < HC / 32; ++s) tmem_ld32(t_row + H_COL + HC * hh + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(rh + 32 * s));
+#pragma unroll
+        for (int s = 0; s < HC / 32; ++s) tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(rh + 32 * s));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(h_empty_c);
         ETR(2);
-        uint32_t pk[32];
+        uint32_t pk[HC / 2];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t* rr = i < 8 ? r0 : r1;
-          const int o = (i & 7) * 4;
-          float v0 = __uint_as_float(rr[o]) + bb[i].x, v1 = __uint_as_float(rr[o + 1]) + bb[i].y;
-          float v2 = __uint_as_float(rr[o + 2]) + bb[i].z, v3 = __uint_as_float(rr[o + 3]) + bb[i].w;
+        for (int i = 0; i < HC / 4; ++i) {
+          float v0 = __uint_as_float(rh[4 * i]) + bb[i].x, v1 = __uint_as_float(rh[4 * i + 1]) + bb[i].y;
+          float v2 = __uint_as_float(rh[4 * i + 2]) + bb[i].z, v3 = __uint_as_float(rh[4 * i + 3]) + bb[i].w;
           gelu2(v0, v1);
           gelu2(v2, v3);
           pk[2 * i] = pack_bf16x2(v0, v1);
@@ -455,12 +458,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         ETR(3);
         mbar_wait(hs_empty, (hc & 1) ^ 1);      // Hs free: G2(c-1) retired
         ETR(4);
-        // k-block hh of Hs, row row_l: 8 chunks of 16 B at (j ^ (row & 7)) (128-byte swizzle)
-        uint8_t* hrow = sHs + hh * MBM * 128 + row_l * 128;
+        // columns [HC hh, +HC) of Hs, row row_l: k-block (HC hh) / 64, 16-byte chunks j at (j ^ (row & 7))
+        {
+          uint8_t* hrow = sHs + ((HC * hh) >> 6) * MBM * 128 + row_l * 128;
+          const int j0 = ((HC * hh) & 63) >> 3;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<uint4*>(hrow + ((j ^ (row_l & 7)) << 4)) =
-              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          for (int j = 0; j < HC / 8; ++j)
+            *reinterpret_cast<uint4*>(hrow + (((j0 + j) ^ (row_l & 7)) << 4)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
         ETR(5);
         fence_proxy_async_smem();              // generic-proxy writes -> visible to the MMA (async proxy)
         __syncwarp();
@@ -487,9 +493,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
       }
       // residual X1 = this unit's A tile, still resident (the next unit's A load waits for a_free)
-      const ResidualSmemA ra{sA, row_l, hh * (D / 2)};
+      const ResidualSmemA ra{sA, row_l, hh * (D / NP)};
       uint8_t* stg0 = sHs + (warp - 4) * (MLP_STG * 2048);
-      ln_epilogue<D, D / 2>(t_row, hh * (D / 2), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+      ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();

@@ -273,7 +273,10 @@ PinnedBuf take_from_pool(std::vector<PinnedBuf>& pool, size_t bytes) {
   for (int i = 0; i < int(pool.size()); ++i) {
     if (pool[i].cap >= bytes && (best < 0 || pool[i].cap < pool[best].cap)) best = i;
   }
-  if (best < 0 && !pool.empty()) best = 0;
+  if (best < 0) {   // none large enough: grow the largest (least growth)
+    for (int i = 0; i < int(pool.size()); ++i)
+      if (best < 0 || pool[i].cap > pool[best].cap) best = i;
+  }
   if (best < 0) return PinnedBuf{};
   PinnedBuf b = pool[best];
   pool.erase(pool.begin() + best);

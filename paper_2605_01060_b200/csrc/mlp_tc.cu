@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* a_free = y_empty + 1;                            // local: LN read its residual from A
   uint64_t* y0_full = a_free + 1;                            // both (OP): G0 retired
   uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x1_ready + 1);
+  uint64_t* xres_full = x1_ready + 1;                         // local (OP): X residual rows landed in A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xres_full + 1);
   uint8_t* sA = smem + T::HEAD;                              // [KB1][128 x 128 B]
   uint8_t* sHs = sA + T::A_BYTES;                            // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(a_free, EPI_WARPS);
     mbar_init(y0_full, 1);
     mbar_init(x1_ready, 2 * EPI_WARPS);
+    mbar_init(xres_full, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -248,7 +250,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           if constexpr (OP)                              // LN0 residual rows (X), read from L2
             for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmR, kb * 64, m0);
         }
-        if constexpr (OP) ring_wo();
+        if constexpr (OP) {
+          ring_wo();
+          if (p == 0) {
+            // once G0 has consumed O, the A tile takes this unit's X rows: the LN0 residual, read from
+            // smem instead of from L2 one step ahead (its latency bounded LN0's first pass)
+            mbar_wait(y0_full, ui & 1);
+            mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
+            for (int kb = 0; kb < KB1; ++kb)
+              tma_load_2d(sA + kb * MBM * 128, &tmR, xres_full, kb * 64, m0);
+          }
+        }
         for (int c = 0; c < NCH; ++c) {
           ring_w1(c);
           if (c > 0) ring_w2(c - 1);
@@ -406,7 +418,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
         }
         const int row = m0 + row_l;
-        const ResidualGlobal rg{xres + size_t(row < M ? row : 0) * D + hh * (D / NP)};
+        (void)row;
+        const ResidualSmemA rg{sA, row_l, hh * (D / NP)};
+        mbar_wait(xres_full, ui & 1);          // X rows in the A tile (G0 is done with O)
         ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);

@@ -59,10 +59,17 @@ __device__ __forceinline__ void store_rows_32x32(uint8_t* stg, const uint32_t (&
 
 // NP warps share a lane quadrant, each owning HALF = BN / NP columns (part hh).  PIPE: TMEM loads and
 // residual loads one step ahead (2 register buffers); !PIPE: one buffer (for register-limited kernels).
-template <int BN, int HALF, bool PIPE = true, typename Res, typename Ready, typename Store, int NP = BN / HALF>
+struct LnNoOp {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// pass1_done() runs once the residual has been read for the last time (after pass 1).
+template <int BN, int HALF, bool PIPE = true, typename Res, typename Ready, typename Store, typename P1 = LnNoOp,
+          int NP = BN / HALF>
 __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
                                             const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,
-                                            int lane, float eps, Ready&& wait_ready, Store&& store) {
+                                            int lane, float eps, Ready&& wait_ready, Store&& store,
+                                            P1&& pass1_done = P1{}) {
 #ifdef LN_TRACE
   long long _lt = 0;
 #endif
@@ -107,6 +114,7 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
     tmem_st32(taddr + c, w);
   }
   tmem_st_wait();
+  pass1_done();
   LNT(1);
   const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
   stats[hh * 128 + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);

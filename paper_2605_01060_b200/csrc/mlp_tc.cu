@@ -516,13 +516,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                             },
                             [&](const uint32_t (&p)[16], int col) {
                               store_rows_32x32(stg0, p, lane, out, m0 + q * 32, M, D, col);
+                            },
+                            [&] {                // residual read for the last time: the A tile may take
+                              __syncwarp();      // the next unit's rows while pass 2 runs
+                              if (lane == 0) mbar_arrive(a_free);
                             });
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(y_empty_c);
-        mbar_arrive(a_free);                   // this CTA's A tile no longer read (residual done)
-      }
+      if (lane == 0) mbar_arrive_cluster(y_empty_c);
       // LN constants / stats (in Hs) consumed before the next unit's first chunk overwrites Hs
       ETR(10);
       asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");

@@ -1,4 +1,4 @@
-# round-1 profile set v7 (fused QKV+attention, fused tail): full bench line, ncu launch list, --set full captures
+# round-1 profile set (current) (fused QKV+attention, fused tail): full bench line, ncu launch list, --set full captures
 set -x
 mkdir -p gpurun_out
 timeout 1200 python bench.py > gpurun_out/bench_full.log 2>&1; tail -1 gpurun_out/bench_full.log | cut -c1-300

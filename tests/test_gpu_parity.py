@@ -303,3 +303,47 @@ def test_fused_mlp_matches_separate_gemms_and_oracle(N, enc, n_texts):
     T = texts_of(ids, lens)
     rows = sorted({0, len(lens) - 1, *rng.integers(0, len(lens), size=min(10, len(lens))).tolist()})
     compare(fused[rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def test_output_side_upload_and_resume(N, tmp_path):
+    """NEXT N4 end to end: polled pieces go to zero-copy Arrow files through the async uploader (the
+    upload releases each piece); a first run whose storage dies after a few partitions leaves a
+    partial prefix; the resumed run skips the completed partitions and the union of both runs
+    equals the direct encoding bit for bit."""
+    from paper_2605_01060_b200 import output as O
+    ecfg = ENCODERS["toy"]
+    wcfg = scaled(WORKLOADS["toy"], n_texts=1500, n_partitions=30, b_min=200, b_max=1000)
+    w = make_weights(ecfg, seed=1234, init="pin")
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=4)
+    direct, _, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+
+    class Dying(O.LocalStorage):
+        def __init__(self, root, budget):
+            super().__init__(root)
+            self.budget = budget
+
+        def write(self, path, data):
+            if self.budget <= 0:
+                raise OSError("storage gone")
+            self.budget -= 1
+            super().write(path, data)
+
+    parts = list(wl)
+    for attempt, storage in enumerate((Dying(str(tmp_path), 12), O.LocalStorage(str(tmp_path)))):
+        h = N.surge_create(N.make_config(ecfg, wcfg.b_min, wcfg.b_max), pack_blob(ecfg, w))
+        try:
+            skip = O.completed(storage, "run")
+            if attempt == 1:
+                assert 0 < len(skip) < len(parts)
+            up = O.AsyncUploader(storage, "run", workers=8, backoff_s=0.001,
+                                 release=lambda r, h=h: N.surge_release(h, r))
+            O.encode_to_storage(N, h, parts, up, skip=skip)
+            up.close()
+        finally:
+            N.surge_destroy(h)
+    st = O.LocalStorage(str(tmp_path))
+    assert O.completed(st, "run") == {int(k) for k in wl.keys}
+    for key, ids, lens in wl:
+        files = [f for f in st.list(f"run/{int(key):020d}") if f.endswith(".arrow")]
+        got = np.concatenate([O.deserialize(st.read(f"run/{int(key):020d}/{f}")) for f in sorted(files)])
+        assert np.array_equal(got, direct[int(key)])

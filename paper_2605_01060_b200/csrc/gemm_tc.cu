@@ -310,13 +310,16 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       const uint32_t aph = (it / ACC) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
 #ifndef ATT_GATE
-#define ATT_GATE 1
+#define ATT_GATE 2
 #endif
       if constexpr (T::ATT) {
         // legacy mma.sync (the attention) is starved while tcgen05 MMAs run on the SM
         // (scripts/microbench/umma_hmma.cu: ~0.01 vs 0.46 HMMA/clk): the next tile's MMAs wait until
         // the previous tile's attention phase is over, instead of stretching it
-        if (ATT_GATE && it >= 1) mbar_wait(att_gate, (it - 1) & 1);
+        // schedule per SM: MMA(t+1) | epilogue: store(t-1), stage(t)  ->  attention(t) alone on the pipe
+        // -> MMA(t+2) | ... : MMA(t) waits for attention(t-2); attention(t) waits for MMA(t+1) to retire.
+        if (ATT_GATE == 1 && it >= 1) mbar_wait(att_gate, (it - 1) & 1);
+        if (ATT_GATE == 2 && it >= 2) mbar_wait(att_gate, (it - 2) & 1);
       }
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * BN;
@@ -459,6 +462,10 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
         }
         ATT_TR(2);
         named_bar_sync(1, T::EPI_WARPS * 32);   // the tile's Q | K | V staged (and its record visible)
+        if (ATT_GATE == 2 && has_next) {          // the next tile's MMAs retire before the attention starts
+          mbar_wait(&tfull[acc ^ (ACC > 1 ? 1 : 0)], ((it + 1) / ACC) & 1);
+          tc_fence_after();
+        }
         ATT_TR(3);
         const int32_t* R = s_rec + slot * ATT_REC_INTS;
         const int row0 = R[0], nrows = R[1], ntexts = R[2], nunits = R[3];

@@ -49,50 +49,52 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// One warp computes the 16 query rows [16 qt, 16 qt + 16) of one text for NH heads at once (the
-// heads' arithmetic is independent and interleaved for instruction-level parallelism; each head's
-// operation sequence is the single-head one, so results do not depend on NH):
-//   sQt : the tile's first query row at head 0's columns; sK / sV : the text's first key row at
-//   head 0's columns; head h is DH columns further right in each; len = text length,
-//   nt = ceil(len / 16) key blocks.
-// Returns the unnormalised accumulators o[h] (mma C-fragment layout: row g = lane / 4 in
-// o[h][n][0..1], row g + 8 in o[h][n][2..3], columns 8 n + 2 (lane % 4) + {0, 1}) and the
-// reciprocal row sums ia[h] (row g), ib[h] (row g + 8): O = o * i.
-// One key block of the online softmax for NH heads (FIRST: block 0, where the running max is -inf,
-// so the rescale factors are exactly 0 and are skipped -- the same values the general step gives).
-template <int DH, int NH, bool FIRST>
+// One step of the online softmax over NS consecutive 16-key sub-blocks (NS = 1 or 2) for NH heads
+// (FIRST: the first step, where the running max is -inf, so the rescale factors are exactly 0 and
+// are skipped -- the same values the general step gives).  Wider steps shorten the dependency chain
+// of texts longer than 16 tokens (one max / exp / rescale round per 32 keys instead of per 16).
+template <int DH, int LDS, int NH, int NS, bool FIRST>
 __device__ __forceinline__ void attn_key_block(uint32_t k_addr, uint32_t v_addr, const uint32_t (&qa)[NH][DH / 16][4],
                                                int j0, int len, float qscale, float (&o)[NH][DH / 8][4],
                                                float (&ma)[NH], float (&mb)[NH], float (&la)[NH], float (&lb)[NH]) {
-  const bool v0 = j0 < len, v1 = j0 + 1 < len, v2 = j0 + 8 < len, v3 = j0 + 9 < len;
-  float s0[NH][4], s1[NH][4];
+  constexpr uint32_t SB = 16 * LDS * 2;          // bytes between 16-row sub-blocks
+  float s[NH][NS][2][4];
 #pragma unroll
-  for (int h = 0; h < NH; ++h) {
+  for (int h = 0; h < NH; ++h)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) s0[h][i] = s1[h][i] = 0.f;
+    for (int sb = 0; sb < NS; ++sb) {
 #pragma unroll
-    for (int kk = 0; kk < DH / 16; ++kk) {
-      uint32_t b00, b01, b10, b11;
-      ldsm_x4(k_addr + h * DH * 2 + kk * 32, b00, b01, b10, b11);
-      mma_bf16_16816(s0[h], qa[h][kk], b00, b01);
-      mma_bf16_16816(s1[h], qa[h][kk], b10, b11);
+      for (int i = 0; i < 4; ++i) s[h][sb][0][i] = s[h][sb][1][i] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < DH / 16; ++kk) {
+        uint32_t b00, b01, b10, b11;
+        ldsm_x4(k_addr + sb * SB + h * DH * 2 + kk * 32, b00, b01, b10, b11);
+        mma_bf16_16816(s[h][sb][0], qa[h][kk], b00, b01);
+        mma_bf16_16816(s[h][sb][1], qa[h][kk], b10, b11);
+      }
     }
-  }
 #pragma unroll
   for (int h = 0; h < NH; ++h) {
     // raw scores; the scale (log2(e) / sqrt(d_h) > 0) is applied inside the exponent:
-    // p = 2^(s q - m q), m = running row max of the raw scores
-    float pa[4], pb[4];
-    pa[0] = v0 ? s0[h][0] : -INFINITY;
-    pa[1] = v1 ? s0[h][1] : -INFINITY;
-    pa[2] = v2 ? s1[h][0] : -INFINITY;
-    pa[3] = v3 ? s1[h][1] : -INFINITY;
-    pb[0] = v0 ? s0[h][2] : -INFINITY;
-    pb[1] = v1 ? s0[h][3] : -INFINITY;
-    pb[2] = v2 ? s1[h][2] : -INFINITY;
-    pb[3] = v3 ? s1[h][3] : -INFINITY;
-    float xa = fmaxf(fmaxf(pa[0], pa[1]), fmaxf(pa[2], pa[3]));
-    float xb = fmaxf(fmaxf(pb[0], pb[1]), fmaxf(pb[2], pb[3]));
+    // p = 2^(s q - m q), m = running row max of the raw scores.  pa: row g, pb: row g + 8;
+    // element 4 sb + 2 t + e = key j0 + 16 sb + 8 t + e.
+    float pa[4 * NS], pb[4 * NS];
+#pragma unroll
+    for (int sb = 0; sb < NS; ++sb)
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool v = j0 + 16 * sb + 8 * t + e < len;
+          pa[4 * sb + 2 * t + e] = v ? s[h][sb][t][e] : -INFINITY;
+          pb[4 * sb + 2 * t + e] = v ? s[h][sb][t][2 + e] : -INFINITY;
+        }
+    float xa = pa[0], xb = pb[0];
+#pragma unroll
+    for (int i = 1; i < 4 * NS; ++i) {
+      xa = fmaxf(xa, pa[i]);
+      xb = fmaxf(xb, pb[i]);
+    }
     xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 1));
     xa = fmaxf(xa, __shfl_xor_sync(0xffffffffu, xa, 2));
     xb = fmaxf(xb, __shfl_xor_sync(0xffffffffu, xb, 1));
@@ -100,17 +102,22 @@ __device__ __forceinline__ void attn_key_block(uint32_t k_addr, uint32_t v_addr,
     const float na = FIRST ? xa : fmaxf(ma[h], xa), nb = FIRST ? xb : fmaxf(mb[h], xb);   // finite
     const float nqa = na * qscale, nqb = nb * qscale;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 4 * NS; ++i) {
       pa[i] = ex2_approx(fmaf(pa[i], qscale, -nqa));   // masked: 2^-inf = 0
       pb[i] = ex2_approx(fmaf(pb[i], qscale, -nqb));
     }
+    float sa = (pa[0] + pa[1]) + (pa[2] + pa[3]), sbb = (pb[0] + pb[1]) + (pb[2] + pb[3]);
+    if (NS == 2) {
+      sa += (pa[4] + pa[5]) + (pa[6] + pa[7]);
+      sbb += (pb[4] + pb[5]) + (pb[6] + pb[7]);
+    }
     if (FIRST) {
-      la[h] = (pa[0] + pa[1]) + (pa[2] + pa[3]);
-      lb[h] = (pb[0] + pb[1]) + (pb[2] + pb[3]);
+      la[h] = sa;
+      lb[h] = sbb;
     } else {
       const float ca = ex2_approx(fmaf(ma[h], qscale, -nqa)), cb = ex2_approx(fmaf(mb[h], qscale, -nqb));
-      la[h] = fmaf(la[h], ca, (pa[0] + pa[1]) + (pa[2] + pa[3]));
-      lb[h] = fmaf(lb[h], cb, (pb[0] + pb[1]) + (pb[2] + pb[3]));
+      la[h] = fmaf(la[h], ca, sa);
+      lb[h] = fmaf(lb[h], cb, sbb);
 #pragma unroll
       for (int n = 0; n < DH / 8; ++n) {
         o[h][n][0] *= ca; o[h][n][1] *= ca;
@@ -119,29 +126,32 @@ __device__ __forceinline__ void attn_key_block(uint32_t k_addr, uint32_t v_addr,
     }
     ma[h] = na;
     mb[h] = nb;
-    const uint32_t pf[4] = {pack_bf16x2(pa[0], pa[1]), pack_bf16x2(pb[0], pb[1]), pack_bf16x2(pa[2], pa[3]),
-                            pack_bf16x2(pb[2], pb[3])};
+#pragma unroll
+    for (int sb = 0; sb < NS; ++sb) {
+      const uint32_t pf[4] = {pack_bf16x2(pa[4 * sb], pa[4 * sb + 1]), pack_bf16x2(pb[4 * sb], pb[4 * sb + 1]),
+                              pack_bf16x2(pa[4 * sb + 2], pa[4 * sb + 3]), pack_bf16x2(pb[4 * sb + 2], pb[4 * sb + 3])};
 #if ATT_P_SPLIT
-    // P = P_hi + P_lo, both bf16 (two MMAs): P V keeps ~16 mantissa bits of P
-    const uint32_t pl[4] = {pack_bf16x2(pa[0] - bf16lo(pf[0]), pa[1] - bf16hi(pf[0])),
-                            pack_bf16x2(pb[0] - bf16lo(pf[1]), pb[1] - bf16hi(pf[1])),
-                            pack_bf16x2(pa[2] - bf16lo(pf[2]), pa[3] - bf16hi(pf[2])),
-                            pack_bf16x2(pb[2] - bf16lo(pf[3]), pb[3] - bf16hi(pf[3]))};
+      // P = P_hi + P_lo, both bf16 (two MMAs): P V keeps ~16 mantissa bits of P
+      const uint32_t pl[4] = {pack_bf16x2(pa[4 * sb] - bf16lo(pf[0]), pa[4 * sb + 1] - bf16hi(pf[0])),
+                              pack_bf16x2(pb[4 * sb] - bf16lo(pf[1]), pb[4 * sb + 1] - bf16hi(pf[1])),
+                              pack_bf16x2(pa[4 * sb + 2] - bf16lo(pf[2]), pa[4 * sb + 3] - bf16hi(pf[2])),
+                              pack_bf16x2(pb[4 * sb + 2] - bf16lo(pf[3]), pb[4 * sb + 3] - bf16hi(pf[3]))};
 #endif
 #pragma unroll
-    for (int n = 0; n < DH / 16; ++n) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(v_addr + h * DH * 2 + n * 32, b0, b1, b2, b3);
-      if (FIRST) {   // o = 0 + P V: start the accumulators from zero inside the MMA
-        o[h][2 * n][0] = o[h][2 * n][1] = o[h][2 * n][2] = o[h][2 * n][3] = 0.f;
-        o[h][2 * n + 1][0] = o[h][2 * n + 1][1] = o[h][2 * n + 1][2] = o[h][2 * n + 1][3] = 0.f;
-      }
-      mma_bf16_16816(o[h][2 * n], pf, b0, b1);
-      mma_bf16_16816(o[h][2 * n + 1], pf, b2, b3);
+      for (int n = 0; n < DH / 16; ++n) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(v_addr + sb * SB + h * DH * 2 + n * 32, b0, b1, b2, b3);
+        if (FIRST && sb == 0) {   // o = 0 + P V: start the accumulators from zero inside the MMA
+          o[h][2 * n][0] = o[h][2 * n][1] = o[h][2 * n][2] = o[h][2 * n][3] = 0.f;
+          o[h][2 * n + 1][0] = o[h][2 * n + 1][1] = o[h][2 * n + 1][2] = o[h][2 * n + 1][3] = 0.f;
+        }
+        mma_bf16_16816(o[h][2 * n], pf, b0, b1);
+        mma_bf16_16816(o[h][2 * n + 1], pf, b2, b3);
 #if ATT_P_SPLIT
-      mma_bf16_16816(o[h][2 * n], pl, b0, b1);
-      mma_bf16_16816(o[h][2 * n + 1], pl, b2, b3);
+        mma_bf16_16816(o[h][2 * n], pl, b0, b1);
+        mma_bf16_16816(o[h][2 * n + 1], pl, b2, b3);
 #endif
+      }
     }
   }
 }
@@ -170,12 +180,24 @@ __device__ __forceinline__ void attn_query_tile(const uint16_t* sQt, const uint1
   float ma[NH], mb[NH], la[NH], lb[NH];
   const uint32_t k_base = smem_u32(sK + ((lane & 7) + ((lane >> 4) & 1) * 8) * LDS + ((lane >> 3) & 1) * 8);
   const uint32_t v_base = smem_u32(sV + ((lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
-  // key index within the text: 16 kb + 2 c4 + {0, 1} (s0), + 8 (s1); valid iff < len
-  attn_key_block<DH, NH, true>(k_base, v_base, qa, 2 * c4, len, qscale, o, ma, mb, la, lb);
+  // key index within the text of a thread's score element: 16 sub-block + 8 t + 2 c4 + e; valid iff < len.
+  // Steps of 32 keys while more than 16 keys remain, a final step of 16 (reads stay within
+  // 16 * ceil(len / 16) rows of the text, as with 16-key steps).
+  if (nt >= 2) {
+    attn_key_block<DH, LDS, NH, 2, true>(k_base, v_base, qa, 2 * c4, len, qscale, o, ma, mb, la, lb);
+  } else {
+    attn_key_block<DH, LDS, NH, 1, true>(k_base, v_base, qa, 2 * c4, len, qscale, o, ma, mb, la, lb);
+  }
 #pragma unroll 1
-  for (int kb = 1; kb < nt; ++kb)
-    attn_key_block<DH, NH, false>(k_base + uint32_t(kb * 16 * LDS * 2), v_base + uint32_t(kb * 16 * LDS * 2), qa,
-                                  16 * kb + 2 * c4, len, qscale, o, ma, mb, la, lb);
+  for (int kb = 2; kb < nt; kb += 2) {
+    const uint32_t off = uint32_t(kb * 16 * LDS * 2);
+    if (kb + 1 < nt)
+      attn_key_block<DH, LDS, NH, 2, false>(k_base + off, v_base + off, qa, 16 * kb + 2 * c4, len, qscale, o, ma, mb,
+                                            la, lb);
+    else
+      attn_key_block<DH, LDS, NH, 1, false>(k_base + off, v_base + off, qa, 16 * kb + 2 * c4, len, qscale, o, ma, mb,
+                                            la, lb);
+  }
 #pragma unroll
   for (int h = 0; h < NH; ++h) {
     la[h] += __shfl_xor_sync(0xffffffffu, la[h], 1);

@@ -95,6 +95,13 @@ __device__ __forceinline__ void gelu2(float& x0, float& x1) {
   x1 = f2hi(g);
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream serialization may
+// start while the previous kernel in the stream drains; griddep_wait() blocks until that kernel has
+// completed and its memory is visible (no-op without PDL); griddep_launch_dependents() lets the next
+// PDL kernel be scheduled (its CTAs take SMs as ours retire).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // One lane of the (fully active) warp returns true.
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "attn_tile.cuh"
 #include "common.cuh"
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
           }
         }
       }
+      griddep_wait();                         // A / residual come from the previous kernel
       uint32_t c = 0;
       for (int t = sc.t0; t < sc.tend; t += sc.dt) {
         const int m0 = sc.m0(t), n0 = sc.n0(t) * BN;
@@ -293,6 +295,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       }
     }
   } else if (warp == 1 && leader) {
+    griddep_launch_dependents();
     // -------------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (warp-uniform control flow and operands, so descriptors live
     // in uniform registers); one elected lane issues the tcgen05.mma / commit instructions.
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {
+    griddep_wait();                           // records / residual rows / outputs of the previous kernel
     // ------------------------------------------------------------------ epilogue (warps 4..11)
     if constexpr (EPI == EPI_BIAS_LN) {       // LN tiles span all N columns: constants once
       for (int i = threadIdx.x - 128; i < BN; i += T::EPI_WARPS * 32) {
@@ -650,11 +654,11 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   const int smem = T::smem_bytes(g.K, WS, g.N);
   const int stages = T::stages(g.K, WS, g.N);
   if (stages < 2 || smem > T::MAX_SMEM) return cudaErrorInvalidValue;
-  static int attr = 0;
-  if (attr < smem) {
+  static int smem_attr = 0;
+  if (smem_attr < smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::MAX_SMEM);
     if (e != cudaSuccess) return e;
-    attr = T::MAX_SMEM;
+    smem_attr = T::MAX_SMEM;
   }
   const bool att = EPI == EPI_QKV_ATTN;
   const int64_t m_tiles = att ? g.n_att_tiles : (g.M + BM - 1) / BM, n_tiles = g.N / BN;
@@ -674,25 +678,29 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     grid = int(std::min<int64_t>(m_tiles * n_tiles, num_sms()));
   }
   const CUtensorMap tmR = g.tmR ? *g.tmR : *g.tmC;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(T::THREADS);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   if (PAIR) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(T::THREADS);
-    cfg.dynamicSmemBytes = size_t(smem);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
-                              g.beta, g.C, g.eps, stages, at);
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
-  kern<<<grid, T::THREADS, smem, st>>>(*g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K,
-                                         g.bias, g.res, g.gamma, g.beta, g.C, g.eps, stages, at);
-  return cudaGetLastError();
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *g.tmC, tmR, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
+                            g.beta, g.C, g.eps, stages, at);
 }
 
 // Weight-stationary when the B slice fits next to >= 4 A stages and there are enough M tiles to
@@ -722,6 +730,14 @@ cudaError_t launch_gemm_bn(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SURGE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 cudaError_t init_tma_encoder() {
   if (g_encode_tiled) return cudaSuccess;

@@ -69,6 +69,8 @@ inline bool qkv_att_supported(int d, int heads) {
 }
 
 cudaError_t init_tma_encoder();
+// Programmatic dependent launch for the GEMM-class kernels (env SURGE_PDL=0 disables).
+bool pdl_enabled();
 cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 // Output map for the GEMM epilogue's TMA stores: box 32 rows x 32 columns, 64-byte swizzle.
 cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols);

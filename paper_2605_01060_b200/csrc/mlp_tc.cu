@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0 || warp == 2 || warp == 3) {
+    griddep_wait();                            // A (O or X1) and the residual rows come from the previous kernel
     if (lane == 0) {
       // ------------------------------------------------------------------ TMA producers
       // Box sequence per unit: A (KB1 boxes, after the previous unit's last G1 freed it), then per
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1 && leader) {
+    griddep_launch_dependents();
     // -------------------------------------------------------------------- MMA issuer (leader)
     constexpr uint32_t idesc1 = umma_idesc_bf16(2 * MBM, FC);
     constexpr uint32_t idesc2 = umma_idesc_bf16(2 * MBM, T::N2);
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
 
   } else if (warp >= 4) {
+    griddep_wait();
     // ------------------------------------------------------------------ epilogue (warps 4..11)
     const int q = warp & 3;                    // TMEM lane quadrant
     const int hh = (warp - 4) >> 2;            // column part (0 .. NP-1)
@@ -571,13 +574,15 @@ cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = size_t(T::SMEM);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   const CUtensorMap& tmWo = OP ? *a.tmWo : *a.tmW2;
   const CUtensorMap& tmR = OP ? *a.tmX : *a.tmA;
   return cudaLaunchKernelEx(&cfg, kern, *a.tmA, *a.tmW1, *a.tmW2, tmWo, tmR, int(a.M), a.F, a.b1, a.b2, a.gamma,

@@ -401,8 +401,11 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
 // 16-row query tiles and 16-key blocks aligned to the text start, mma.sync m16n8k16 with P split
 // hi+lo, online softmax over the key blocks in order (so long and short texts follow one rule).
 template <int DH>
+#ifndef ATT_LONG_WARPS
+#define ATT_LONG_WARPS 16
+#endif
 struct LongAtt {
-  static constexpr int WARPS = 8;
+  static constexpr int WARPS = ATT_LONG_WARPS;   // one 16-row query tile per warp
   static constexpr int QROWS = 16 * WARPS;
   static constexpr int LDS = DH + 8;
   static constexpr int CH = DH / 8;

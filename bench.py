@@ -328,7 +328,7 @@ def main():
                                    f"B_min={wcfg.b_min}, B_max={wcfg.b_max}",
                        "superbatches_per_step": F, "parallelism": f"lpt{world}",
                        "l2": "inputs (ids 565 MB) and outputs (15.4 GB) larger than L2; no explicit flush",
-                       "chunk_tokens": cfg.chunk_tokens or 262144},
+                       "chunk_tokens": cfg.chunk_tokens or 524288},
             "tokens_per_s": wl.n_tokens * args.steps / (ms_max / 1e3),
             "tc_fraction_of_sustained": all_flops / (ms_max / 1e3) / 1e12 / tc_peak,   # this rank's share
             "gemm_tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,

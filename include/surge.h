@@ -72,7 +72,7 @@ typedef struct {
   int64_t b_min, b_max;         /* two-threshold policy, texts                                  */
   int32_t rank, world_size;     /* LPT shard owned by this process; 0, 1 for single GPU         */
   int32_t device;               /* CUDA device ordinal                                          */
-  int32_t chunk_tokens;         /* tokens per encode chunk; 0 = auto (262144)                   */
+  int32_t chunk_tokens;         /* tokens per encode chunk; 0 = auto (524288)                   */
   int32_t max_inflight;         /* SuperBatches queued/encoding before submit blocks; 0 = 2      */
   int32_t nonblocking_submit;   /* 1: submit returns SURGE_E_AGAIN instead of blocking           */
   int32_t weights_on_device;    /* 1: `weights` passed to surge_create is a device pointer       */

@@ -31,7 +31,7 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
 // PAIR: a cluster of two CTAs runs cta_group::2 MMAs on 256 x BN tiles; each CTA holds its 128
 // rows of A and of the accumulator, and half of every MMA's N rows of B (so B traffic per CTA
 // halves).
-template <int BN, int EPI, bool PAIR = false>
+template <int BN, int EPI, bool PAIR = false, int DH = 0>
 struct TileCfg {
   static constexpr int MMA_N = (BN <= 256) ? BN : BN / 2;       // <= 256, multiple of 16
   static constexpr int N_MMA = BN / MMA_N;
@@ -49,7 +49,9 @@ struct TileCfg {
   // The attention epilogue (EPI_QKV_ATTN) runs 12 warps: the (text, head) units of a tile are its
   // critical path.
   static constexpr bool ATT = EPI == EPI_QKV_ATTN;
-  static constexpr int SPLIT = ATT ? (BN % 96 == 0 ? 3 : 2)
+  // attention epilogue: 16 warps at d_h = 32 (MiniLM; 12 -> 16 warps: QKV+attention 1138 -> 1128
+  // ms/step), 12 elsewhere (their attention registers spill at the 96-register cap of 16 warps)
+  static constexpr int SPLIT = ATT ? (DH == 32 ? 4 : 3)
                                : EPI != EPI_BIAS_GELU ? 2 : BN % 128 == 0 ? 4 : BN % 96 == 0 ? 3 : 2;
   static constexpr int EPI_WARPS = 4 * SPLIT;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -72,7 +74,7 @@ struct TileCfg {
   static constexpr int HALF = BN / SPLIT;                         // columns per epilogue warp
   static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "invalid UMMA N");
   static_assert(B_BOX * N_LOADS * (PAIR ? 2 : 1) == BN, "B box split");
-  static_assert(HALF % 32 == 0, "epilogue column split");
+  static_assert(HALF % 32 == 0 || (ATT && HALF % 16 == 0), "epilogue column split");
   // Weight-stationary (ws): the CTA's whole B slice [BN x K] stays resident; only A streams.
   __host__ __device__ static int b_res_bytes(int K, bool ws) { return ws ? (PAIR ? BN / 2 : BN) * K * 2 : 0; }
   __host__ __device__ static int stage_bytes(bool ws) { return A_STAGE_BYTES + (ws ? 0 : B_STAGE_BYTES); }
@@ -155,13 +157,13 @@ struct Sched {
 #endif
 
 template <int BN, int EPI, bool WS, bool PAIR, int DH = 0>
-__global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
+__global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
                    float eps, int stages, const AttTiles att) {
-  using T = TileCfg<BN, EPI, PAIR>;
+  using T = TileCfg<BN, EPI, PAIR, DH>;
   constexpr int ACC = T::ACC;
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the __shared__ array (an integer round trip would turn every
@@ -425,38 +427,41 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
         const bool has_next = t + sc.dt < sc.tend;
         int32_t nxt = 0;
         if (e < ATT_REC_INTS && has_next) nxt = att.rec[size_t(sc.att_tile(t + sc.dt)) * ATT_REC_INTS + e];
+        // phase 1 in 16-column steps (HALF = 64 with 12 epilogue warps, 48 with 16)
+        constexpr int NS16 = T::HALF / 16;
         const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c_lo);
-        float4 b4[2][8];
+        float4 b4[2][4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) b4[0][i] = __ldg(bp + i);
-        uint32_t r[2][32];
+        for (int i = 0; i < 4; ++i) b4[0][i] = __ldg(bp + i);
+        uint32_t r[2][16];
         ATT_TR(0);
         mbar_wait(&tfull[acc], aph);
         ATT_TR(1);
         tc_fence_after();
-        tmem_ld32(taddr + c_lo, r[0]);
+        tmem_ld16(taddr + c_lo, r[0]);
         uint16_t* srow = sAtt + (q * 32 + lane) * LDS + c_lo;
 #pragma unroll
-        for (int k = 0; k < NSTEP; ++k) {
+        for (int k = 0; k < NS16; ++k) {
           const int cur = k & 1;
-          tmem_ld_wait_regs(r[cur]);
-          if (k + 1 < NSTEP) {
-            tmem_ld32(taddr + c_lo + 32 * (k + 1), r[cur ^ 1]);
+          tmem_ld_wait_regs16(r[cur]);
+          const uint32_t (&rc)[16] = r[cur];
+          if (k + 1 < NS16) {
+            tmem_ld16(taddr + c_lo + 16 * (k + 1), r[cur ^ 1]);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) b4[cur ^ 1][i] = __ldg(bp + 8 * (k + 1) + i);
+            for (int i = 0; i < 4; ++i) b4[cur ^ 1][i] = __ldg(bp + 4 * (k + 1) + i);
           }
-          uint32_t p[16];
+          uint32_t p[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 4; ++i) {
             const float4 bb = b4[cur][i];
-            const f32x2 v01 = fadd2(f2(__uint_as_float(r[cur][4 * i]), __uint_as_float(r[cur][4 * i + 1])), f2(bb.x, bb.y));
-            const f32x2 v23 = fadd2(f2(__uint_as_float(r[cur][4 * i + 2]), __uint_as_float(r[cur][4 * i + 3])), f2(bb.z, bb.w));
+            const f32x2 v01 = fadd2(f2(__uint_as_float(rc[4 * i]), __uint_as_float(rc[4 * i + 1])), f2(bb.x, bb.y));
+            const f32x2 v23 = fadd2(f2(__uint_as_float(rc[4 * i + 2]), __uint_as_float(rc[4 * i + 3])), f2(bb.z, bb.w));
             p[2 * i] = pack_bf16x2(f2lo(v01), f2hi(v01));
             p[2 * i + 1] = pack_bf16x2(f2lo(v23), f2hi(v23));
           }
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            *reinterpret_cast<uint4*>(srow + 32 * k + 8 * i) = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+          for (int i = 0; i < 2; ++i)
+            *reinterpret_cast<uint4*>(srow + 16 * k + 8 * i) = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
         }
         tc_fence_before();
         __syncwarp();
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR>::THREADS, 1)
         const uint8_t* tstart = reinterpret_cast<const uint8_t*>(R + 4);
         const uint16_t* units = reinterpret_cast<const uint16_t*>(R + 36);
 #ifndef ATT_NHU32
-#define ATT_NHU32 2
+#define ATT_NHU32 1
 #endif
         constexpr int NHU = DH == 16 ? 2 : DH == 32 ? ATT_NHU32 : 1;   // heads per unit (internal.h att_unit_heads)
         constexpr int W = T::EPI_WARPS;
@@ -649,7 +654,7 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 
 template <int BN, int EPI, bool WS, bool PAIR = false, int DH = 0>
 cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
-  using T = TileCfg<BN, EPI, PAIR>;
+  using T = TileCfg<BN, EPI, PAIR, DH>;
   auto kern = gemm_tc_kernel<BN, EPI, WS, PAIR, DH>;
   const int smem = T::smem_bytes(g.K, WS, g.N);
   const int stages = T::stages(g.K, WS, g.N);
@@ -705,9 +710,9 @@ cudaError_t launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
 
 // Weight-stationary when the B slice fits next to >= 4 A stages and there are enough M tiles to
 // give every slice's CTAs work.
-template <int BN, int EPI, bool PAIR = false>
+template <int BN, int EPI, bool PAIR = false, int DH = 0>
 bool use_ws(const GemmArgs& g) {
-  using T = TileCfg<BN, EPI, PAIR>;
+  using T = TileCfg<BN, EPI, PAIR, DH>;
   const int64_t m_units = g.epi == EPI_QKV_ATTN ? (PAIR ? g.n_att_tiles / 2 : g.n_att_tiles)
                          : PAIR ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM - 1) / BM;
   const int units = PAIR ? num_sms() / 2 : num_sms();
@@ -820,7 +825,7 @@ uint32_t gemm_b_box_rows(int N, int K, int epi) {
 
 template <int DH>
 cudaError_t launch_qkv_att(const GemmArgs& g, cudaStream_t st) {
-  if (use_ws<ATT_SLICE, EPI_QKV_ATTN, true>(g)) return launch_gemm_t<ATT_SLICE, EPI_QKV_ATTN, true, true, DH>(g, st);
+  if (use_ws<ATT_SLICE, EPI_QKV_ATTN, true, DH>(g)) return launch_gemm_t<ATT_SLICE, EPI_QKV_ATTN, true, true, DH>(g, st);
   return launch_gemm_t<ATT_SLICE, EPI_QKV_ATTN, false, true, DH>(g, st);
 }
 

@@ -53,7 +53,7 @@ constexpr int ATT_REC_INTS = 172;
 constexpr int ATT_REC_MAX_UNITS = 272;   // (128 / 16 + ntexts <= 136 query tiles) x <= 2 head groups
 // heads per work unit: 1 (head groups = heads of the slice) except d_h = 16 (4 heads per slice) -> 2
 #ifndef ATT_NHU32
-#define ATT_NHU32 2
+#define ATT_NHU32 1
 #endif
 inline int att_unit_heads(int dh) { return dh == 16 ? 2 : dh == 32 ? ATT_NHU32 : 1; }
 // Upper bound on the tiles of a chunk of ntok tokens (two consecutive greedy tiles hold > 128 rows).

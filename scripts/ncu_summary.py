@@ -54,6 +54,8 @@ def main():
                 x = None
             if x is not None and k.endswith("_MB"):
                 x = x * SCALE.get(unit, 1.0) / 1e6
+            if x is not None and k == "time_us":
+                x = x * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
             row[k] = x
         name = d.get("Kernel Name", ("", ""))[1]
         traffic = (row["dram_read_MB"] + row["dram_write_MB"]) * 1e6

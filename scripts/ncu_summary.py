@@ -55,7 +55,7 @@ def main():
             if x is not None and k.endswith("_MB"):
                 x = x * SCALE.get(unit, 1.0) / 1e6
             if x is not None and k == "time_us":
-                x = x * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+                x = x * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(unit, 1.0)
             row[k] = x
         name = d.get("Kernel Name", ("", ""))[1]
         traffic = (row["dram_read_MB"] + row["dram_write_MB"]) * 1e6

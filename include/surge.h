@@ -319,6 +319,13 @@ typedef struct {
 /*   SURGE_OPT_TAIL_FUSED (default 1; effective with SURGE_OPT_MLP_FUSED): K6 out-projection +
  *     residual + LN also runs inside the fused MLP kernel (X1 kept on chip).  Bit-identical. */
 #define SURGE_OPT_TAIL_FUSED 3
+/*   SURGE_OPT_POOLING (default SURGE_POOL_MEAN): SURGE_POOL_MEAN = masked mean over all tokens of
+ *     the text incl. [CLS]/[SEP] (all-MiniLM-L6-v2 convention, reading R6);
+ *     SURGE_POOL_CLS = the [CLS] token's hidden state (bge's native pooling).
+ *     Either is followed by L2 normalisation.  Changes the embeddings, not the schedule. */
+#define SURGE_OPT_POOLING 4
+#define SURGE_POOL_MEAN 0
+#define SURGE_POOL_CLS 1
 surge_status surge_set_option(surge_handle h, int32_t option, int64_t value);
 
 surge_status surge_profile_enable(surge_handle h, int32_t on);   /* on: clears counters */

@@ -94,9 +94,11 @@ class Encoder:
             h = self.layer(h, i)
         return h
 
-    def encode_text(self, ids: np.ndarray) -> np.ndarray:
-        """One text -> its d-dim unit embedding."""
-        return mean_pool_l2(self.hidden_states(ids))
+    def encode_text(self, ids: np.ndarray, pooling: str = "mean") -> np.ndarray:
+        """One text -> its d-dim unit embedding (pooling "mean": reading #6; "cls": bge's native
+        [CLS] pooling)."""
+        h = self.hidden_states(ids)
+        return cls_pool_l2(h) if pooling == "cls" else mean_pool_l2(h)
 
     def encode_texts(self, texts) -> np.ndarray:
         """Each text independently (PBP order, P:167 -- no batching, no padding)."""
@@ -109,4 +111,10 @@ def mean_pool_l2(h: np.ndarray) -> np.ndarray:
     """v = (1/l) sum_t h_t over ALL l tokens incl. [CLS]/[SEP] (reading #6);
     e = v / max(||v||_2, 1e-12) (reading #7, torch F.normalize)."""
     v = h.sum(axis=0) / h.shape[0]
+    return v / max(float(np.sqrt((v * v).sum())), 1e-12)
+
+
+def cls_pool_l2(h: np.ndarray) -> np.ndarray:
+    """[CLS] pooling (bge): e = h_0 / max(||h_0||_2, 1e-12)."""
+    v = h[0]
     return v / max(float(np.sqrt((v * v).sum())), 1e-12)

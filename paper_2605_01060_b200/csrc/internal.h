@@ -123,7 +123,7 @@ cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* g
                              uint16_t* y, cudaStream_t st);
 // K9
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
-                               float* out, cudaStream_t st);
+                               float* out, cudaStream_t st, int pooling = 0);   // pooling: 0 mean, 1 [CLS]
 
 cudaError_t launch_bf16_to_f32(const uint16_t* in, float* out, int64_t n, cudaStream_t st);
 
@@ -214,12 +214,15 @@ class DeviceModel {
   void set_mlp_fused(bool on) { mlp_fused_ = on; }
   // out-projection + LN fused into the MLP kernel as a prologue (on by default; needs mlp fused)
   void set_tail_fused(bool on) { tail_fused_ = on; }
+  // pooling: 0 = masked mean over all tokens (reading R6, default), 1 = [CLS] (bge's native)
+  void set_pooling(int p) { pooling_ = p; }
 
  private:
   ModelShape s_{};
   bool att_fused_ = true;
   bool mlp_fused_ = true;
   bool tail_fused_ = true;
+  int pooling_ = 0;
   std::vector<void*> allocs_;
   uint16_t *word_ = nullptr, *pos_ = nullptr, *type_ = nullptr;
   float *emb_g_ = nullptr, *emb_b_ = nullptr;

@@ -505,7 +505,8 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
 }
 
 // ----------------------------------------------------------------------------- K9 meanpool + L2
-template <int D>
+// CLS: [CLS] pooling (the text's first row only; bge's native pooling, execution option).
+template <int D, bool CLS = false>
 __global__ void __launch_bounds__(256) meanpool_l2_kernel(const uint16_t* __restrict__ x,
                                                           const int32_t* __restrict__ cu, int64_t n_texts,
                                                           int32_t tok0, float* __restrict__ out) {
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(256) meanpool_l2_kernel(const uint16_t* __rest
   const int64_t text = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (text >= n_texts) return;
-  const int32_t a = cu[text] - tok0, b = cu[text + 1] - tok0;
+  const int32_t a = cu[text] - tok0, b = CLS ? a + 1 : cu[text + 1] - tok0;
   float acc[PER][4];
 #pragma unroll
   for (int i = 0; i < PER; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
@@ -716,16 +717,22 @@ cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* g
 }
 
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
-                               float* out, cudaStream_t st) {
+                               float* out, cudaStream_t st, int pooling) {
   if (n_texts <= 0) return cudaSuccess;
   const unsigned grid = blocks_for_warps(n_texts, 8);
+#define SURGE_POOL(DD)                                                                                   \
+  case DD:                                                                                               \
+    if (pooling == 1) meanpool_l2_kernel<DD, true><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);     \
+    else meanpool_l2_kernel<DD, false><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);                 \
+    break;
   switch (d) {
-    case 64: meanpool_l2_kernel<64><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out); break;
-    case 384: meanpool_l2_kernel<384><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out); break;
-    case 768: meanpool_l2_kernel<768><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out); break;
-    case 1024: meanpool_l2_kernel<1024><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out); break;
+    SURGE_POOL(64)
+    SURGE_POOL(384)
+    SURGE_POOL(768)
+    SURGE_POOL(1024)
     default: return cudaErrorInvalidValue;
   }
+#undef SURGE_POOL
   return cudaGetLastError();
 }
 

@@ -375,7 +375,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     k += fused ? 2 : 3;
   }
   if (P) prof->begin(st, &ev);
-  SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st));
+  SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st, pooling_));
   if (P) prof->end(KK_POOL, st, ev, 0.0, M * 2 * D + double(n) * 4 * D);
   ++k;
   if (launches) *launches += k;

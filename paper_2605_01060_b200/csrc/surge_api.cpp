@@ -1084,6 +1084,10 @@ surge_status surge_set_option(surge_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
       c->model.set_tail_fused(value != 0);
       return SURGE_OK;
+    case SURGE_OPT_POOLING:
+      if (value != SURGE_POOL_MEAN && value != SURGE_POOL_CLS) return SURGE_E_INVALID_ARG;
+      c->model.set_pooling(int(value));
+      return SURGE_OK;
   }
   return SURGE_E_INVALID_ARG;
 }

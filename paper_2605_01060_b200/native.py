@@ -75,6 +75,8 @@ KERNEL_KINDS = ("embed_ln", "gemm_qkv", "attention", "gemm_out_ln", "gemm_ffn1_g
 SURGE_OPT_ATT_FUSED = 1
 SURGE_OPT_MLP_FUSED = 2
 SURGE_OPT_TAIL_FUSED = 3
+SURGE_OPT_POOLING = 4
+SURGE_POOL_MEAN, SURGE_POOL_CLS = 0, 1
 
 
 class surge_superbatch_info(C.Structure):

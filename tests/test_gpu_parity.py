@@ -347,3 +347,30 @@ def test_output_side_upload_and_resume(N, tmp_path):
         files = [f for f in st.list(f"run/{int(key):020d}") if f.endswith(".arrow")]
         got = np.concatenate([O.deserialize(st.read(f"run/{int(key):020d}/{f}")) for f in sorted(files)])
         assert np.array_equal(got, direct[int(key)])
+
+
+@pytest.mark.parametrize("enc", ["toy", "bgebase"])
+def test_cls_pooling_option(N, enc):
+    """SURGE_OPT_POOLING = CLS (bge's native pooling, NEXT N1) vs the oracle's [CLS] pooling; mean
+    pooling stays the default."""
+    ecfg = ENCODERS[enc]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(21)
+    lens = rng.integers(1, min(40, ecfg.max_position) + 1, size=300).astype(np.int32)
+    ids = rng.integers(4 if enc == "toy" else 1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    outs = {}
+    for pool in (N.SURGE_POOL_MEAN, N.SURGE_POOL_CLS):
+        h = N.surge_create(N.make_config(ecfg, 1000, 5000), pack_blob(ecfg, w))
+        try:
+            N.surge_set_option(h, N.SURGE_OPT_POOLING, pool)
+            out = torch.zeros(len(lens), ecfg.hidden, device="cuda")
+            N.surge_encode_packed(h, torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(), lens, len(lens), out)
+            torch.cuda.synchronize()
+            outs[pool] = out.cpu().numpy()
+        finally:
+            N.surge_destroy(h)
+    E = oenc.Encoder(ecfg, w)
+    T = texts_of(ids, lens)
+    rows = sorted({0, len(lens) - 1, *rng.integers(0, len(lens), size=6).tolist()})
+    compare(outs[N.SURGE_POOL_CLS][rows], np.stack([E.encode_text(T[i], pooling="cls") for i in rows]))
+    compare(outs[N.SURGE_POOL_MEAN][rows], np.stack([E.encode_text(T[i]) for i in rows]))

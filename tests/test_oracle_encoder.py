@@ -21,8 +21,9 @@ from synth.workload import make_workload, random_texts
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
 
 
-def hf_reference(cfg, weights, texts):
-    """transformers BertModel in fp64 (eager attention, erf GELU, eps 1e-12), then mean-pool+normalize."""
+def hf_reference(cfg, weights, texts, pooling="mean"):
+    """transformers BertModel in fp64 (eager attention, erf GELU, eps 1e-12), then mean (or [CLS])
+    pooling + normalize."""
     from transformers import BertConfig, BertModel
     hc = BertConfig(vocab_size=cfg.vocab_size, hidden_size=cfg.hidden, num_hidden_layers=cfg.layers,
                     num_attention_heads=cfg.heads, intermediate_size=cfg.ffn, hidden_act="gelu",
@@ -37,7 +38,7 @@ def hf_reference(cfg, weights, texts):
     with torch.no_grad():
         for t in texts:
             h = m(input_ids=torch.from_numpy(np.asarray(t, dtype=np.int64))[None]).last_hidden_state[0]
-            v = h.mean(0)
+            v = h[0] if pooling == "cls" else h.mean(0)
             out.append(torch.nn.functional.normalize(v, dim=0, eps=1e-12).numpy())
     return np.stack(out)
 
@@ -141,3 +142,19 @@ def test_discriminating_power_minilm():
     C = X @ X.T
     off = C[~np.eye(len(X), dtype=bool)]
     assert off.mean() <= 0.6 and off.max() <= 0.9, (off.mean(), off.max())
+
+
+def test_cls_pooling_pin():
+    """[CLS] pooling (bge's native): closed form e = h_0 / ||h_0|| on a known
+    matrix, equal to mean pooling for one-token texts, and the full encoder vs transformers' CLS
+    hidden state (independent library)."""
+    h = np.array([[3.0, 4.0], [10.0, -1.0], [0.5, 0.5]])
+    assert np.allclose(enc.cls_pool_l2(h), [0.6, 0.8])
+    assert np.allclose(enc.cls_pool_l2(h[:1]), enc.mean_pool_l2(h[:1]))
+    cfg = ENCODERS["toy"]
+    w = make_weights(cfg, seed=99, init="pin")
+    texts = random_texts(12, cfg.vocab_size, cfg.max_position, seed=3, lo=1, cls_id=1, sep_id=2, id_lo=4)
+    E = enc.Encoder(cfg, w)
+    ours = np.stack([E.encode_text(t, pooling="cls") for t in texts])
+    assert np.max(np.abs(ours - hf_reference(cfg, w, texts, pooling="cls"))) <= 1e-10
+    assert not np.allclose(ours, E.encode_texts(texts))

@@ -310,10 +310,20 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
+#ifdef ATT_TRACE
+    long long mt_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const long long mt_start = clock64();
+#endif
     for (int t = sc.t0; t < sc.tend; t += sc.dt, ++it) {
       const int acc = it % ACC;
       const uint32_t aph = (it / ACC) & 1;
+#ifdef ATT_TRACE
+      long long _e0 = clock64();
+      mbar_wait(&tempty[acc], aph ^ 1);
+      mt_acc[8] += clock64() - _e0;
+#else
       mbar_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
+#endif
 #ifndef ATT_GATE
 #define ATT_GATE 2
 #endif
@@ -323,13 +333,25 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
         // the previous tile's attention phase is over, instead of stretching it
         // schedule per SM: MMA(t+1) | epilogue: store(t-1), stage(t)  ->  attention(t) alone on the pipe
         // -> MMA(t+2) | ... : MMA(t) waits for attention(t-2); attention(t) waits for MMA(t+1) to retire.
+#ifdef ATT_TRACE
+        long long _g0 = clock64();
+#endif
         if (ATT_GATE == 1 && it >= 1) mbar_wait(att_gate, (it - 1) & 1);
         if (ATT_GATE == 2 && it >= 2) mbar_wait(att_gate, (it - 2) & 1);
+#ifdef ATT_TRACE
+        mt_acc[0] += clock64() - _g0;
+#endif
       }
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * BN;
       for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef ATT_TRACE
+        long long _f0 = clock64();
         mbar_wait(&full[s], ph);
+        if (kb < 7) mt_acc[1 + kb] += clock64() - _f0;
+#else
+        mbar_wait(&full[s], ph);
+#endif
         tc_fence_after();
         if (elect_one()) {
           const uint64_t a_desc = a_desc0 + uint64_t((s * A_STAGE_BYTES) >> 4);
@@ -355,6 +377,15 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
       }
       __syncwarp();
     }
+#ifdef ATT_TRACE
+    if constexpr (T::ATT) {
+      const long long n = it > 0 ? it : 1;
+      if (lane == 0 && blockIdx.x < 8)
+        printf("MMA_TRACE cta %d tiles %d total %lld | gate %lld tempty %lld full kb0..5 %lld %lld %lld %lld %lld %lld (cycles/tile)\n",
+               int(blockIdx.x), it, (clock64() - mt_start) / n, mt_acc[0] / n, mt_acc[8] / n, mt_acc[1] / n,
+               mt_acc[2] / n, mt_acc[3] / n, mt_acc[4] / n, mt_acc[5] / n, mt_acc[6] / n);
+    }
+#endif
   } else if (warp >= 4) {
     griddep_wait();                           // records / residual rows / outputs of the previous kernel
     // ------------------------------------------------------------------ epilogue (warps 4..11)

@@ -101,7 +101,9 @@ bool mlp_fused_supported(int d, int ffn);
 inline uint32_t mlp_w2_box_rows(int d) { return uint32_t(d <= 256 ? d / 2 : d / 4); }
 cudaError_t launch_mlp(const MlpArgs& a, cudaStream_t st);
 
-// K1: cu[0..n], row_off[0..m], tok_off[0..m] (single CTA)
+// K1: cu[0..n], row_off[0..m], tok_off[0..m] (one CTA up to one 8K-element tile; beyond, one CTA per
+// tile for cu, then a one-CTA kernel for the partition offsets)
+int pack_launch_count(int64_t n, int64_t m);   // kernels launch_pack issues
 cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes, int64_t m, int32_t* cu,
                         int32_t* row_off, int32_t* tok_off, cudaStream_t st);
 // K3: tokens of texts [0, n_texts) described by cu (absolute offsets), activations indexed cu[i]-tok0

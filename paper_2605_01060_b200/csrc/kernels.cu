@@ -80,6 +80,87 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_kernel(const int32_t* __res
   }
 }
 
+// K1 for SuperBatches of more than one tile (S up to ~5.7e5 texts at a Safety flush): CTA b scans
+// tile b after adding the sum of all lengths before it (read directly, coalesced: no scratch buffer,
+// no inter-CTA protocol; the last CTA reads n - TILE values, a few microseconds), so the one-CTA tile
+// loop (7.7 us per 8K-element tile, ~0.1 ms per C2 SuperBatch) becomes one wave of CTAs.  The
+// partition offsets (m values) follow in a one-CTA kernel once cu is complete.
+constexpr int PACK_TILE = PACK_THREADS * PACK_PER_THREAD;
+
+__global__ void __launch_bounds__(PACK_THREADS) pack_scan_tiles_kernel(const int32_t* __restrict__ lengths,
+                                                                       int64_t n, int32_t* __restrict__ cu) {
+  __shared__ int32_t s_warp[32];
+  __shared__ int32_t s_carry;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t base = int64_t(blockIdx.x) * PACK_TILE;
+  int32_t acc[4] = {0, 0, 0, 0};
+  int64_t i = t;
+  for (; i + 3 * PACK_THREADS < base; i += 4 * PACK_THREADS) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] += __ldg(lengths + i + k * PACK_THREADS);
+  }
+  for (; i < base; i += PACK_THREADS) acc[0] += __ldg(lengths + i);
+  int32_t part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) s_warp[w] = part;
+  __syncthreads();
+  if (w == 0) {
+    int32_t x = s_warp[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_carry = x;
+  }
+  __syncthreads();
+  // the one-tile body of block_exclusive_scan, starting from the carry
+  const int64_t i0 = base + int64_t(t) * PACK_PER_THREAD;
+  int32_t v[PACK_PER_THREAD];
+  int32_t local = 0;
+#pragma unroll
+  for (int k = 0; k < PACK_PER_THREAD; ++k) {
+    v[k] = (i0 + k < n) ? lengths[i0 + k] : 0;
+    local += v[k];
+  }
+  int32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();   // s_warp reused
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int32_t x = s_warp[lane];
+    int32_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    s_warp[lane] = xi - x;
+  }
+  __syncthreads();
+  int32_t run = s_carry + s_warp[w] + (incl - local);
+#pragma unroll
+  for (int k = 0; k < PACK_PER_THREAD; ++k) {
+    if (i0 + k < n) cu[i0 + k] = run;
+    run += v[k];
+  }
+  if (blockIdx.x == gridDim.x - 1 && t == PACK_THREADS - 1) cu[n] = run;   // the total
+}
+
+__global__ void __launch_bounds__(PACK_THREADS) pack_offsets_kernel(const int32_t* __restrict__ sizes, int64_t m,
+                                                                    const int32_t* __restrict__ cu,
+                                                                    int32_t* __restrict__ row_off,
+                                                                    int32_t* __restrict__ tok_off) {
+  __shared__ int32_t s_warp[32];
+  __shared__ int32_t s_carry;
+  block_exclusive_scan(sizes, m, row_off, s_warp, &s_carry);
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j <= m; j += PACK_THREADS) tok_off[j] = cu[row_off[j]];
+}
+
 // ------------------------------------------------------------------------------- K3 embed + LN
 // One warp per text; lane owns columns {4*(lane + 32*i) .. +3}.
 template <int D>
@@ -614,9 +695,16 @@ cudaError_t launch_bf16_to_f32(const uint16_t* in, float* out, int64_t n, cudaSt
   return cudaGetLastError();
 }
 
+int pack_launch_count(int64_t n, int64_t m) { return n <= PACK_TILE ? 1 : (m > 0 ? 2 : 1); }
+
 cudaError_t launch_pack(const int32_t* lengths, int64_t n, const int32_t* sizes, int64_t m, int32_t* cu,
                         int32_t* row_off, int32_t* tok_off, cudaStream_t st) {
-  pack_kernel<<<1, PACK_THREADS, 0, st>>>(lengths, n, sizes, m, cu, row_off, tok_off);
+  if (n <= PACK_TILE) {       // one tile: the one-CTA kernel does cu and the partition offsets
+    pack_kernel<<<1, PACK_THREADS, 0, st>>>(lengths, n, sizes, m, cu, row_off, tok_off);
+    return cudaGetLastError();
+  }
+  pack_scan_tiles_kernel<<<unsigned((n + PACK_TILE - 1) / PACK_TILE), PACK_THREADS, 0, st>>>(lengths, n, cu);
+  if (m > 0) pack_offsets_kernel<<<1, PACK_THREADS, 0, st>>>(sizes, m, cu, row_off, tok_off);
   return cudaGetLastError();
 }
 

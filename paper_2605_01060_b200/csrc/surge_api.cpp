@@ -401,7 +401,7 @@ int process_superbatch(Ctx* c, SuperBatch* sb) {
                                 c->d_tokoff[slot], c->s_comp));
     c->prof.end(KK_PACK, c->s_comp, ev, 0.0, 8.0 * double(LS) + 12.0 * double(NP));
   }
-  c->launches += 1;
+  c->launches += pack_launch_count(LS, NP);
   // chunks
   int64_t s0 = 0;
   const int64_t cap = c->ws.cap;
@@ -923,7 +923,7 @@ surge_status surge_encode_packed(surge_handle h, const int32_t* d_ids, const int
   c->prof_api.begin(st, &ev);
   CUDA_OR_FAIL(c, launch_pack(d_lengths, n_texts, nullptr, 0, c->api_cu, nullptr, nullptr, st));
   c->prof_api.end(KK_PACK, st, ev, 0.0, 8.0 * double(n_texts));
-  int64_t nl = 1;
+  int64_t nl = pack_launch_count(n_texts, 0);
   CUDA_OR_FAIL(c, c->model.encode(c->ws_api, d_ids, c->api_cu, c->api_host_cu.data(), n_texts, d_out, st, &nl,
                                   &c->prof_api));
   c->launches += nl;
@@ -1015,7 +1015,7 @@ surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const
   c->prof_api.begin(st, &ev);
   CUDA_OR_FAIL(c, launch_pack(lens, LS, c->api_sizes, NP, c->api_cu, c->api_ro, c->api_to, st));
   c->prof_api.end(KK_PACK, st, ev, 0.0, 8.0 * double(LS) + 12.0 * double(NP));
-  int64_t nl = 1;
+  int64_t nl = pack_launch_count(LS, NP);
   CUDA_OR_FAIL(c, c->model.encode(c->ws_api, ids, c->api_cu, host_cu.data(), LS, out, st, &nl, &c->prof_api));
   c->launches += nl;
   if (!direct) {

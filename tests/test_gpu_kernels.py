@@ -37,7 +37,10 @@ def from_bits(t: torch.Tensor) -> torch.Tensor:
     return t.view(torch.bfloat16).float()
 
 
-@pytest.mark.parametrize("n,m", [(1, 1), (5, 2), (8191, 3), (8192, 7), (8193, 11), (300_000, 45), (10, 0)])
+# n > 8192 runs the multi-CTA scan (one CTA per 8K tile, then the partition offsets); 16384: exact
+# tile multiple; 600,000 x 1,000 members: a Safety-flush-sized SuperBatch (sigma = 2.5)
+@pytest.mark.parametrize("n,m", [(1, 1), (5, 2), (8191, 3), (8192, 7), (8193, 11), (16384, 0), (16385, 2),
+                                 (300_000, 45), (600_000, 1000), (10, 0)])
 def test_pack_bit_exact(N, n, m):
     rng = np.random.default_rng(n + m)
     lengths = rng.integers(1, 513, size=n).astype(np.int32)

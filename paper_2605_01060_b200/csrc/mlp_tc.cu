@@ -37,6 +37,9 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 #ifndef MLP_STG
 #define MLP_STG 1                   // LN output staging buffers per epilogue warp
 #endif
+#ifndef MLP_A_SPLIT
+#define MLP_A_SPLIT 1               // A-tile boxes issued by all three producers (0: producer 0 alone)
+#endif
 #ifndef MLP_PREFETCH
 #define MLP_PREFETCH 0              // L2 prefetch of the next unit's A rows (measured: no effect)
 #endif
@@ -225,8 +228,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                              j * T::N2 + rank * T::B2_BOX, pol_w);
         }
       };
-      auto ring_wo = [&]() {                             // OP: Wo k-blocks in the W2 stage format
-        for (int kb = 0; kb < KB1; ++kb, ++sc) {
+      auto ring_wo = [&](int kb0, int kb1) {             // OP: Wo k-blocks in the W2 stage format
+        for (int kb = kb0; kb < kb1; ++kb, ++sc) {
           const int s = int(sc % RING);
           const uint32_t ph = (sc / RING) & 1;
           if (int(sc % 3) != p) continue;
@@ -237,22 +240,36 @@ __global__ void __launch_bounds__(THREADS, 1)
                              j * T::N2 + rank * T::B2_BOX, pol_w);
         }
       };
-      for (int u = unit0; u < n_units; u += units, ++ui) {
-        const int m0 = u * 2 * MBM + rank * MBM;
-        if (p == 0) {                                    // A: this CTA's rows, once per unit
-          mbar_wait(a_empty, (ui & 1) ^ 1);     // MMAs done with the previous unit's A
-          mbar_wait(a_free, (ui & 1) ^ 1);      // its LN has read the residual rows
-          if (leader) mbar_arrive_expect_tx(a_full, 2u * T::A_BYTES);
-          for (int kb = 0; kb < KB1; ++kb)
-            tma_load_2d_pair(sA + kb * MBM * 128, &tmX1, afull_c, kb * 64, m0, l2_policy_evict_first());
+      // A: this CTA's rows, once per unit.  Its k-blocks are split over the three producers (one
+      // issuing thread completes ~one box per 500 cycles, and the load sits between the previous
+      // unit's final-LN pass 1 and this unit's G0).  Box completions of producers 1 and 2 may reach
+      // the leader's a_full before producer 0's arrive.expect_tx: the transiently negative tx-count
+      // cannot complete the phase while that arrival is pending.
+      auto load_a = [&](int u, int m0) {
+        mbar_wait(a_empty, (ui & 1) ^ 1);       // MMAs done with the previous unit's A
+        mbar_wait(a_free, (ui & 1) ^ 1);        // its LN has read the residual rows
+        if (leader && p == 0) mbar_arrive_expect_tx(a_full, 2u * T::A_BYTES);
+        for (int kb = (OP && MLP_A_SPLIT) ? p : 0; kb < KB1; kb += (OP && MLP_A_SPLIT) ? 3 : 1)
+          tma_load_2d_pair(sA + kb * MBM * 128, &tmX1, afull_c, kb * 64, m0, l2_policy_evict_first());
+        if (p == 0) {
           // warm L2 with the next unit's rows: its A load waits for this unit's LN (residual from A)
           if (MLP_PREFETCH && u + units < n_units)
             for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmX1, kb * 64, m0 + units * 2 * MBM);
           if constexpr (OP)                              // LN0 residual rows (X), read from L2
             for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmR, kb * 64, m0);
         }
+      };
+      for (int u = unit0; u < n_units; u += units, ++ui) {
+        const int m0 = u * 2 * MBM + rank * MBM;
+        // OP: the first RING Wo stages need only ring slots freed by the previous unit's G2, so
+        // every producer issues its share of them before it waits for the A tile to be released;
+        // the remaining Wo stages need slots that G0 frees, i.e. after A has landed (issuing them
+        // before A would deadlock: G0 waits for A).
+        constexpr int WO_EARLY = (OP && MLP_A_SPLIT) ? (RING < KB1 ? RING : KB1) : 0;
+        if constexpr (OP) ring_wo(0, WO_EARLY);
+        if ((OP && MLP_A_SPLIT) || p == 0) load_a(u, m0);   // !OP: producer 0 alone (unchanged)
         if constexpr (OP) {
-          ring_wo();
+          ring_wo(WO_EARLY, KB1);
           if (p == 0) {
             // once G0 has consumed O, the A tile takes this unit's X rows: the LN0 residual, read from
             // smem instead of from L2 one step ahead (its latency bounded LN0's first pass)

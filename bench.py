@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-texts", type=int, default=256, help="--impl reference: texts encoded per step")
+    ap.add_argument("--ref-texts", type=int, default=512, help="--impl reference: texts encoded per step")
+    ap.add_argument("--host-only", action="store_true",
+                    help="no GPU: the multi-rank host plan (Alg.1 + LPT) over gloo (CPU tests of --gpus N)")
     ap.add_argument("--profile-run", action="store_true",
                     help="for ncu: one SuperBatch, no e2e/baseline/JSON timing")
     return ap.parse_args()
@@ -120,37 +121,100 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(ecfg, w, wl, seconds: float, one_step: bool = False):
-    """The oracle (fp64 numpy, as it stands) on host cores over a bounded sample of the workload."""
-    from threadpoolctl import threadpool_limits
-    from oracle import aggregator as oagg
-    from oracle import encoder as oenc
-    E = oenc.Encoder(ecfg, w)
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: launch the N ranks ourselves, exactly as the driver does
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1); returns its exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_host_only(args, world, rank):
+    """--host-only: the multi-rank host plumbing without a GPU (gloo): every rank runs Alg.1 and the
+    LPT plan through libsurge's pure host functions over the whole stream and keeps its share; the
+    shares are reduced over the process group and rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_01060_b200 import native as N
+    ecfg = ENCODERS[args.encoder]
+    wcfg = WORKLOADS[args.workload]
+    if args.n_texts:
+        wcfg = scaled(wcfg, n_texts=args.n_texts)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
     t0 = time.perf_counter()
-    oagg.run_aggregator(range(len(wl.sizes)), wl.sizes, wl.cfg.b_min, wl.cfg.b_max)   # full-stream Alg.1
-    t_agg = time.perf_counter() - t0
-    n = 0
-    tok = 0
-    with threadpool_limits(limits=1):
-        t0 = time.perf_counter()
-        off = 0
-        while True:
-            l = int(wl.lengths[n])
-            E.encode_text(wl.ids[off:off + l])
-            off += l
-            tok += l
-            n += 1
-            if time.perf_counter() - t0 >= seconds or n >= wl.n_texts:
-                break
-        dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {n} texts ({tok} tokens) of the stream, fp64 per-text encode, 1 thread; "
-                      f"plus Alg.1 over all {len(wl.sizes)} partitions in {t_agg:.3f}s",
-            "texts": n, "seconds": dt}
+    sbs, peak = N.surge_aggregate(wl.sizes.astype(np.int64), wcfg.b_min, wcfg.b_max)
+    texts = tokens = 0
+    for a, b, _ in sbs:
+        t_a, t_b = int(wl.text_off[a]), int(wl.text_off[b])
+        plan = N.surge_lpt_plan(wl.lengths[t_a:t_b], wl.sizes[a:b], world)
+        mine = plan["rank"] == rank
+        texts += int(plan["n_rows"][mine].sum())
+        tokens += int(plan["tokens"][mine].sum())
+    dt = time.perf_counter() - t0
+    t = torch.tensor([texts, tokens], dtype=torch.int64)
+    per_rank = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(per_rank, t)
+    if rank == 0:
+        print(json.dumps({"host_only": True, "n_ranks": world, "backend": dist.get_backend(),
+                          "superbatches": len(sbs), "peak_buffered_texts": peak, "plan_s": dt,
+                          "texts_per_rank": [int(x[0]) for x in per_rank],
+                          "tokens_per_rank": [int(x[1]) for x in per_rank],
+                          "n_texts": wl.n_texts, "n_tokens": wl.n_tokens}), flush=True)
+
+
+def _oracle_flops_per_text(ecfg, l: int) -> float:
+    """SURVEY §8(d) FLOP model of one text of l tokens: L [2d(3d) + 2d^2 + 4 d ff] l + L 4 d l^2."""
+    d, f, L = ecfg.hidden, ecfg.ffn, ecfg.layers
+    return L * (2 * d * 3 * d + 2 * d * d + 4 * d * f) * l + L * 4 * d * l * l
+
+
+def integer_oracle(wl, world: int):
+    """the integer oracle (Alg.1 + packing + LPT plan) over the FULL stream,
+    single-threaded.  Returns (seconds, SuperBatches)."""
+    from oracle import aggregator as oagg
+    t0 = time.perf_counter()
+    A = oagg.run_aggregator(range(len(wl.sizes)), wl.sizes, wl.cfg.b_min, wl.cfg.b_max)
+    for sb in A.flushes:
+        parts = [int(i) for i in sb.refs]
+        a, b = int(wl.text_off[parts[0]]), int(wl.text_off[parts[-1] + 1])
+        oagg.pack(wl.lengths[a:b], sb.sizes)
+        oagg.lpt_plan(wl.lengths[a:b], sb.sizes, world)
+    return time.perf_counter() - t0, len(A.flushes)
+
+
+def cpu_baseline(ecfg, w, wl, world: int = 8, n_rows: int = 16_384):
+    """the oracle as it stands on the box's host cores.
+    (1) the integer oracle over the whole stream, one thread (LPT plan at G = `world`);
+    (2) the fp64 encoder oracle over the SURVEY §8(c) 16,384-row parity sample, one process per host
+        core: texts/s, tokens/s, GFLOP/s (the §8(d) FLOP model of the sampled texts), 10M extrapolation."""
+    from oracle import pool as opool
+    from synth.workload import parity_sample
+    t_int, F = integer_oracle(wl, world)
+    rows = parity_sample(wl, n_rows)
+    ends = np.cumsum(wl.lengths, dtype=np.int64)
+    starts = ends - wl.lengths
+    _, secs, procs = opool.encode_rows(ecfg, w, wl.ids, starts, ends, rows)
+    lens = wl.lengths[rows].astype(np.int64)
+    flops = float(sum(_oracle_flops_per_text(ecfg, int(l)) for l in lens))
+    tps = len(rows) / secs
+    return {"value": tps, "unit": UNIT, "cores": procs, "kind": "oracle",
+            "sample": f"SURVEY 8(c) parity sample: {len(rows)} texts ({int(lens.sum())} tokens), fp64 numpy "
+                      f"per-text encode, {procs} processes (one per host core); plus the integer oracle "
+                      f"(Alg.1 + pack + LPT G={world}) over all {len(wl.sizes)} partitions / {wl.n_texts} texts",
+            "host_cores": opool.host_cores(), "cpu_model": opool.cpu_model(),
+            "tokens_per_s": float(lens.sum()) / secs, "gflops": flops / secs / 1e9,
+            "texts": len(rows), "seconds": secs, "extrapolated_10M_s": 1e7 / tps,
+            "integer_oracle_full_stream_s": t_int, "integer_oracle_superbatches": F}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the oracle timed on host cores (rank 0 only)."""
+    """--impl reference: the oracle timed on the host cores (rank 0 only).  One step = the integer
+    oracle over the whole stream + the fp64 encoder oracle over a bounded sample of the stream (the
+    next --ref-texts texts, one process per host core)."""
     if rank != 0:
         return
     ecfg = ENCODERS[args.encoder]
@@ -159,42 +223,63 @@ def run_reference(args, world, rank):
         wcfg = scaled(wcfg, n_texts=args.n_texts)
     w = make_weights(ecfg, seed=1234)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
-    from threadpoolctl import threadpool_limits
-    from oracle import aggregator as oagg
-    from oracle import encoder as oenc
-    E = oenc.Encoder(ecfg, w)
+    from oracle import pool as opool
+    ends = np.cumsum(wl.lengths, dtype=np.int64)
+    starts = ends - wl.lengths
     per_step = args.ref_texts
-    times = []
-    with threadpool_limits(limits=1):
-        off_t = 0
+    times, t_int = [], []
+    with opool.OraclePool(ecfg, w, wl.ids, starts, ends) as P:
         pos = 0
         for step in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            oagg.run_aggregator(range(len(wl.sizes)), wl.sizes, wcfg.b_min, wcfg.b_max)
-            for _ in range(per_step):
-                l = int(wl.lengths[pos])
-                E.encode_text(wl.ids[off_t:off_t + l])
-                off_t += l
-                pos += 1
+            ti, _ = integer_oracle(wl, max(args.gpus, 1))
+            P.encode(range(pos, pos + per_step))
+            pos += per_step
             if step >= args.warmup:
                 times.append(time.perf_counter() - t0)
+                t_int.append(ti)
     v = per_step * len(times) / sum(times)
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    line = {"metric": metric_name(args, ecfg, wcfg), "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.workload}: N={wcfg.n_texts}, P={wcfg.n_partitions}, sigma={wcfg.sigma}, "
                                    f"{enc_desc(ecfg)}, B_min={wcfg.b_min}, B_max={wcfg.b_max}",
-                       "step": f"Alg.1 over all partitions + oracle encode of {per_step} texts"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{per_step} texts per step, consecutive in stream order"},
+                       "step": f"integer oracle (Alg.1 + pack + LPT) over the whole stream + fp64 oracle encode "
+                               f"of {per_step} consecutive texts on {P.procs} processes"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": P.procs, "kind": "oracle",
+                             "cpu_model": opool.cpu_model(),
+                             "sample": f"{per_step} texts per step, consecutive in stream order, one process per "
+                                       f"host core; integer oracle on the full stream "
+                                       f"({1e3 * float(np.mean(t_int)):.0f} ms of each step)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def metric_name(args, ecfg, wcfg) -> str:
+    """BASELINE.json's metric for the headline (10M, P=4000, MiniLM-L6); otherwise the same template
+    with the encoder class and workload actually run."""
+    if args.encoder == "minilm" and wcfg.n_texts == 10_000_000 and wcfg.n_partitions == 4000 and wcfg.sigma == 1.72:
+        return METRIC
+    n = wcfg.n_texts
+    ns = f"{n // 1_000_000}M" if n % 1_000_000 == 0 else f"{n // 1000}K" if n % 1000 == 0 else str(n)
+    return (f"texts/sec ({ns} texts, P={wcfg.n_partitions}, sigma={wcfg.sigma}, "
+            f"{enc_desc(ecfg).split(' (')[0]}) at 1/2/4/8 B200; TTFO; % TC peak")
 
 
 def main():
     args = parse()
     world, rank, local = dist_setup(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
+    if args.impl == "ours" and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but {world} rank(s) were launched")
+    if args.host_only:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        run_host_only(args, world, rank)
+        dist.destroy_process_group()
+        return
     if world > 1:
         import torch.distributed as dist
         if args.impl == "ours":
@@ -219,19 +304,19 @@ def main():
     if args.n_texts:
         wcfg = scaled(wcfg, n_texts=args.n_texts)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
-    # weights: rank 0 draws them; one NCCL broadcast over NVLink replicates them (K11)
+    # weights: rank 0 draws them; libsurge replicates them with one NCCL broadcast (K11)
     w = make_weights(ecfg, seed=1234) if rank == 0 or world == 1 else None
     n_w = sum(int(np.prod(s)) for s in [v.shape for v in (w or make_weights_shapes(ecfg)).values()])
-    if rank == 0 or world == 1:
-        blob_dev = torch.from_numpy(pack_blob(ecfg, w).view(np.uint8)).to(dev)
-    else:
-        blob_dev = torch.empty(2 * n_w, dtype=torch.uint8, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.broadcast(blob_dev, src=0)     # bf16 bits as bytes (NCCL has no int16 type)
     cfg = N.make_config(ecfg, wcfg.b_min, wcfg.b_max, rank=rank, world_size=world, device=local,
                         chunk_tokens=args.chunk_tokens, weights_on_device=1)
-    h = N.surge_create(cfg, blob_dev, n_weights=blob_dev.numel() // 2)
+    blob_dev = torch.from_numpy(pack_blob(ecfg, w).view(np.uint16)).to(dev) if w is not None else None
+    if world > 1:
+        import torch.distributed as dist
+        nid = [N.surge_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        h = N.surge_create_replicated(cfg, nid[0], blob_dev, n_weights=n_w)
+    else:
+        h = N.surge_create(cfg, blob_dev, n_weights=n_w)
     N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, args.att_fused)
     N.surge_set_option(h, N.SURGE_OPT_MLP_FUSED, args.mlp_fused)
     N.surge_set_option(h, N.SURGE_OPT_TAIL_FUSED, args.tail_fused)
@@ -319,7 +404,7 @@ def main():
     gemm_ms = sum(v["ms"] for k, v in prof.items() if k.startswith("gemm"))
     all_flops = sum(v["flops"] for v in prof.values())
 
-    metric = METRIC if args.encoder == "minilm" else METRIC.replace("MiniLM-L6", enc_desc(ecfg).split(" (")[0])
+    metric = metric_name(args, ecfg, wcfg)
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
@@ -342,7 +427,7 @@ def main():
     if not args.no_e2e:
         line["e2e"] = run_e2e(N, h, wl, args, world, rank, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(ecfg, w, wl, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(ecfg, w, wl)
     line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -43,12 +43,16 @@ typedef enum {
   SURGE_E_TOO_LONG = -4,      /* a text length outside [1, max_position] (no silent truncation) */
   SURGE_E_OOM = -5,           /* device or pinned-host allocation failed                        */
   SURGE_E_CUDA = -6,          /* CUDA runtime/driver error, or no sm_100 device (poisons)       */
-  SURGE_E_NCCL = -7,          /* reserved                                                       */
+  SURGE_E_NCCL = -7,          /* NCCL unavailable or an NCCL call failed (surge_create_replicated) */
   SURGE_E_AGAIN = -8,         /* non-blocking submit would block (backpressure)                 */
   SURGE_E_TOKEN_ID = -9       /* a token id outside [0, vocab_size)                             */
 } surge_status;
 
 typedef struct surge_ctx* surge_handle;
+
+/* Output element types (surge_config.out_dtype, surge_flushed.dtype). */
+#define SURGE_F32 0    /* float32 unit vectors: the paper's output (pa.float32()), default */
+#define SURGE_BF16 1   /* bf16 bit patterns (uint16): half the D2H / host bytes per text           */
 
 /*
  * Encoder configuration (BERT class) + aggregation policy.
@@ -63,7 +67,9 @@ typedef struct surge_ctx* surge_handle;
  *   0 < b_min < b_max.
  *   Sharding: the process encodes only the LPT pieces of every SuperBatch assigned to `rank`
  *   out of `world_size` (north star).  Every rank must be fed the
- *   same partition stream; world_size = 1 encodes everything.
+ *   same partition stream; world_size = 1 encodes everything.  (SURVEY.md §8(b) sketches a
+ *   single-process `num_gpus`; this library runs one process per GPU, so each handle names its
+ *   own rank and device instead, and world_size plays the role of num_gpus.)
  */
 typedef struct {
   int32_t vocab_size, max_position, type_vocab_size;
@@ -76,6 +82,8 @@ typedef struct {
   int32_t max_inflight;         /* SuperBatches queued/encoding before submit blocks; 0 = 2      */
   int32_t nonblocking_submit;   /* 1: submit returns SURGE_E_AGAIN instead of blocking           */
   int32_t weights_on_device;    /* 1: `weights` passed to surge_create is a device pointer       */
+  int32_t out_dtype;            /* SURGE_F32 (default) or SURGE_BF16: element type of every output
+                                   row (streaming pieces and the device-level d_out buffers)      */
 } surge_config;
 
 /*
@@ -96,6 +104,22 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
                           surge_handle* out);
 
 /*
+ * Multi-GPU creation (north star: "weights are replicated once via an NCCL broadcast"; SURVEY.md
+ * §8(e) K11).  One process per GPU; all cfg.world_size ranks call surge_create_replicated
+ * concurrently with the same 128-byte NCCL unique id (obtained once by rank 0 through
+ * surge_nccl_unique_id and handed to the other ranks by the caller, e.g. over its process group).
+ * The library opens an NCCL communicator over the world, broadcasts the weight blob from rank 0
+ * (one ncclBroadcast over NVLink / NVSwitch; `weights` is read on rank 0 only and may be NULL
+ * elsewhere; host or device per cfg.weights_on_device), then builds the handle as surge_create.
+ * The communicator lives until surge_destroy.  No per-SuperBatch collective follows: every rank
+ * encodes its own LPT pieces and returns them itself.
+ * Errors: SURGE_E_NCCL (libnccl.so.2 unavailable, or an NCCL call failed), else as surge_create.
+ */
+surge_status surge_nccl_unique_id(uint8_t* id /* [128] out */);
+surge_status surge_create_replicated(const surge_config* cfg, const uint8_t* nccl_id, const uint16_t* weights,
+                                     size_t n_weights, surge_handle* out);
+
+/*
  * AddPartition (Alg.1).  token_ids: host, sum(lengths) int32 ids in [0, vocab),
  * the n_texts texts concatenated; lengths: host, n_texts int32 values in [1, max_position],
  * each INCLUDING [CLS]/[SEP].  Both are copied before return (Alg.1 `copy(texts)`).
@@ -104,7 +128,8 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
  * n_texts == 0 is accepted: the partition completes immediately with 0 rows (rank 0 only).
  * Errors: SURGE_E_DUPLICATE_ID (id seen before), SURGE_E_TOO_LONG, SURGE_E_TOKEN_ID,
  * SURGE_E_STATE (after finish), SURGE_E_AGAIN (nonblocking_submit and the pipeline is full;
- * nothing was consumed), SURGE_E_INVALID_ARG.
+ * nothing was consumed), SURGE_E_INVALID_ARG (also when the open SuperBatch would reach 2^31
+ * tokens: device token offsets are int32; nothing was consumed).
  */
 surge_status surge_submit_partition(surge_handle h, uint64_t partition_id,
                                     const int32_t* token_ids, const int32_t* lengths,
@@ -118,9 +143,9 @@ surge_status surge_finish(surge_handle h);
  * with row_begin = 0 and n_rows = partition_rows.  For world_size > 1 a partition may be split
  * into LPT pieces encoded on different ranks; each rank returns its own pieces, and the union
  * over ranks covers every row of every partition exactly once.
- *   data: host, pinned, library-owned, row-major n_rows x d float32 unit vectors (P:406 float32;
- *         rows in submission order).  Read-only; valid until surge_release(h, rec) (the buffer
- *         lifetime rule of P:413) or surge_destroy.
+ *   data: host, pinned, library-owned, row-major n_rows x d unit vectors of element type `dtype`
+ *         (SURGE_F32 float32 per P:406, or SURGE_BF16; rows in submission order).  Read-only; valid
+ *         until surge_release(h, rec) (the buffer lifetime rule of P:413) or surge_destroy.
  */
 typedef struct {
   uint64_t partition_id;
@@ -128,8 +153,8 @@ typedef struct {
   int64_t n_rows;           /* rows in this piece                                   */
   int64_t partition_rows;   /* n_k of the whole partition                           */
   int32_t d;                /* embedding dimension (= hidden)                        */
-  int32_t dtype;            /* 0 = float32                                          */
-  const float* data;
+  int32_t dtype;            /* SURGE_F32 or SURGE_BF16 (the handle's out_dtype)      */
+  const void* data;
   int64_t superbatch;       /* index of the SuperBatch that encoded it (-1: n_k = 0) */
   uint64_t token;           /* opaque, for surge_release                            */
 } surge_flushed;
@@ -142,13 +167,16 @@ typedef struct {
 surge_status surge_poll_flushed(surge_handle h, surge_flushed* out, int64_t max_items,
                                 int32_t timeout_ms, int64_t* n_out);
 
-/* Return a polled piece's buffer to the library's pinned pool. */
+/* Return a polled piece's buffer to the library's pinned pool.  Each polled record is released
+ * exactly once: a record that was not polled from the current stream (before the last
+ * surge_reset), or one released twice, returns SURGE_E_INVALID_ARG and changes nothing. */
 surge_status surge_release(surge_handle h, const surge_flushed* rec);
 
 /* Pieces sealed into SuperBatches but not yet returned by poll (0 => everything delivered). */
 surge_status surge_pending(surge_handle h, int64_t* n_pending);
 
-/* After finish and once every piece was polled: start a new stream (keeps weights and pools). */
+/* After finish, once every piece was polled AND released: start a new stream (keeps weights and
+ * pools; the released buffers are reused).  SURGE_E_STATE otherwise. */
 surge_status surge_reset(surge_handle h);
 
 typedef struct {
@@ -199,12 +227,13 @@ void surge_destroy(surge_handle h);             /* drains the pipeline and frees
  *   d_ids     device int32[sum(lengths)]  token ids, texts concatenated (varlen, no padding)
  *   d_lengths device int32[n_texts]        text lengths
  *   h_lengths host   int32[n_texts]        the same lengths (host copy, used to cut chunks)
- *   d_out     device float32[n_texts * d]  unit-norm embeddings, row i = text i
+ *   d_out     device [n_texts * d]         unit-norm embeddings, row i = text i, element type
+ *                                          cfg.out_dtype (float32, or bf16 bits)
  * Runs K1 pack -> per chunk: K3 embed+LN -> L x (QKV GEMM, varlen attention, out-proj+res+LN,
  * FFN1+GELU, FFN2+res+LN) -> K9 mean-pool+L2, enqueued on `stream`; returns without syncing.
  */
 surge_status surge_encode_packed(surge_handle h, const int32_t* d_ids, const int32_t* d_lengths,
-                                 const int32_t* h_lengths, int64_t n_texts, float* d_out,
+                                 const int32_t* h_lengths, int64_t n_texts, void* d_out,
                                  void* stream);
 
 /*
@@ -279,14 +308,14 @@ surge_status surge_aggregate(const int64_t* sizes, int64_t n_partitions, int64_t
  *   d_ids     device int32[sum(lengths)], the SuperBatch's texts concatenated (Flush allTexts)
  *   d_lengths device int32[n_texts];  h_lengths host int32[n_texts] (same values, cuts chunks)
  *   h_sizes   host int64[n_members], n_k of each member in arrival order (bounds)
- *   d_out     device float32[n_texts * d]: rows of THIS rank's LPT pieces are written at their
+ *   d_out     device [n_texts * d] (cfg.out_dtype): rows of THIS rank's LPT pieces are written at their
  *             SuperBatch row positions (all rows when world_size == 1); other rows are untouched.
  * K2 LPT plan (world_size > 1) -> gather of the rank's pieces -> K1 pack -> encoder chunks ->
  * K9 pool -> scatter of the rank's rows into d_out (device-to-device), on `stream`.
  */
 surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const int32_t* d_lengths,
                                      const int32_t* h_lengths, int64_t n_texts, const int64_t* h_sizes,
-                                     int64_t n_members, float* d_out, void* stream);
+                                     int64_t n_members, void* d_out, void* stream);
 
 /*
  * Per-kernel-class device timing (CUDA events around every launch, on the launching stream).

@@ -170,8 +170,11 @@ def lpt_plan(lengths: np.ndarray, sizes, world: int):
     3. Assign each to the rank with minimum (load, rank).
     4. Rank-local order = first_row asc.
     Returns (pieces in global-row order with .rank set, per-rank lists of pieces).
-    parity unpinned (our design, not the paper's): pinned only by brute-force re-check
-    of its stated rule and the LPT makespan bound (tests/test_oracle_aggregator.py).
+    Pinned (tests/test_oracle_aggregator.py) independently of this code: Graham's LPT bound
+    makespan <= (4/3 - 1/(3G)) * OPT against a brute-forced OPT on <= 10-piece instances (an
+    ascending or arrival-order schedule breaks it), and Graham's tight instance family reaches
+    the ratio exactly.  The tie-breaks (equal tokens -> lower first_row; equal load -> lower
+    rank) are this design's reading R16: any tie-break is a valid LPT schedule.
     """
     lengths = np.asarray(lengths, dtype=np.int64)
     T = int(lengths.sum())

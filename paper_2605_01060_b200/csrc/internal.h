@@ -124,8 +124,9 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
 cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* gamma, const float* beta, float eps,
                              uint16_t* y, cudaStream_t st);
 // K9
+// pooling: 0 mean, 1 [CLS]; out: float [n x d], or bf16 bits [n x d] when out_bf16
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
-                               float* out, cudaStream_t st, int pooling = 0);   // pooling: 0 mean, 1 [CLS]
+                               void* out, cudaStream_t st, int pooling = 0, bool out_bf16 = false);
 
 cudaError_t launch_bf16_to_f32(const uint16_t* in, float* out, int64_t n, cudaStream_t st);
 
@@ -172,8 +173,29 @@ struct LayerW {
   CUtensorMap tm_wqkv_att;
 };
 
+// Small host tables (tile starts, text indices, piece sizes) copied to the device per chunk or per
+// SuperBatch.  A cudaMemcpyAsync from pageable memory synchronises the stream before it starts, which
+// would stall the launching thread until the queued kernels finish; these tables are staged in a ring
+// of pinned buffers instead, each slot guarded by an event recorded after its copy.
+struct PinnedRing {
+  static constexpr int NS = 8;
+  int32_t* buf[NS] = {};
+  size_t cap[NS] = {};
+  cudaEvent_t ev[NS] = {};
+  int next = 0;
+  // A pinned slot of >= n int32 whose previous copy has completed; nullptr on allocation failure.
+  int32_t* acquire(size_t n, int* slot);
+  // Copy n int32 from slot to dst on st and guard the slot until the copy has run.
+  cudaError_t copy(int slot, int32_t* dst, size_t n, cudaStream_t st);
+  // acquire + memcpy from src + copy
+  cudaError_t upload(int32_t* dst, const int32_t* src, size_t n, cudaStream_t st);
+  void release();
+  ~PinnedRing() { release(); }
+};
+
 // Activation workspace for one chunk of <= cap tokens (bf16): X, QKV, O, X1, H.
 struct Workspace {
+  PinnedRing tables;        // host -> device staging of the per-chunk tables
   int64_t cap = 0;
   uint16_t *X = nullptr, *QKV = nullptr, *O = nullptr, *X1 = nullptr, *H = nullptr;
   float* V = nullptr;       // fp32 pre-LayerNorm rows (hidden sizes without the fused LN epilogue)
@@ -197,11 +219,11 @@ class DeviceModel {
   // activations chunk-local (token t at row t - tok0); writes d_out rows [s0, s1) (fp32 [n x d]).
   // host_cu (optional, absolute, indexed like d_cu) is only read when prof is enabled.
   cudaError_t encode_chunk(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, int64_t s0, int64_t s1,
-                           int32_t tok0, int32_t ntok, float* d_out, cudaStream_t st, int64_t* launches,
+                           int32_t tok0, int32_t ntok, void* d_out, cudaStream_t st, int64_t* launches,
                            Profiler* prof = nullptr, const int32_t* host_cu = nullptr) const;
   // All texts [0, n): cuts chunks of <= ws.cap tokens at text boundaries using host_cu.
   cudaError_t encode(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, const int32_t* host_cu,
-                     int64_t n_texts, float* d_out, cudaStream_t st, int64_t* launches,
+                     int64_t n_texts, void* d_out, cudaStream_t st, int64_t* launches,
                      Profiler* prof = nullptr) const;
   const ModelShape& shape() const { return s_; }
   const uint16_t* word() const { return word_; }
@@ -218,6 +240,9 @@ class DeviceModel {
   void set_tail_fused(bool on) { tail_fused_ = on; }
   // pooling: 0 = masked mean over all tokens (reading R6, default), 1 = [CLS] (bge's native)
   void set_pooling(int p) { pooling_ = p; }
+  // output element type: false = float32 (default), true = bf16
+  void set_out_bf16(bool b) { out_bf16_ = b; }
+  size_t out_elem_bytes() const { return out_bf16_ ? 2 : 4; }
 
  private:
   ModelShape s_{};
@@ -225,6 +250,7 @@ class DeviceModel {
   bool mlp_fused_ = true;
   bool tail_fused_ = true;
   int pooling_ = 0;
+  bool out_bf16_ = false;
   std::vector<void*> allocs_;
   uint16_t *word_ = nullptr, *pos_ = nullptr, *type_ = nullptr;
   float *emb_g_ = nullptr, *emb_b_ = nullptr;

@@ -587,10 +587,11 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict_
 
 // ----------------------------------------------------------------------------- K9 meanpool + L2
 // CLS: [CLS] pooling (the text's first row only; bge's native pooling, execution option).
-template <int D, bool CLS = false>
+// OUTB: the unit vector is stored as bf16 (out_dtype SURGE_BF16) instead of fp32.
+template <int D, bool CLS = false, bool OUTB = false>
 __global__ void __launch_bounds__(256) meanpool_l2_kernel(const uint16_t* __restrict__ x,
                                                           const int32_t* __restrict__ cu, int64_t n_texts,
-                                                          int32_t tok0, float* __restrict__ out) {
+                                                          int32_t tok0, void* __restrict__ out) {
   constexpr int G = D / 4;
   constexpr int PER = (G + 31) / 32;
   const int64_t text = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -625,11 +626,21 @@ __global__ void __launch_bounds__(256) meanpool_l2_kernel(const uint16_t* __rest
     }
   }
   const float inv = 1.0f / fmaxf(sqrtf(warp_sum(ss)), 1e-12f);
-  float4* orow = reinterpret_cast<float4*>(out + size_t(text) * D);
+  if constexpr (OUTB) {
+    uint2* orow = reinterpret_cast<uint2*>(static_cast<uint16_t*>(out) + size_t(text) * D);
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int g = lane + 32 * i;
-    if (g < G) orow[g] = make_float4(acc[i][0] * inv, acc[i][1] * inv, acc[i][2] * inv, acc[i][3] * inv);
+    for (int i = 0; i < PER; ++i) {
+      const int g = lane + 32 * i;
+      if (g < G)
+        orow[g] = make_uint2(pack_bf16x2(acc[i][0] * inv, acc[i][1] * inv), pack_bf16x2(acc[i][2] * inv, acc[i][3] * inv));
+    }
+  } else {
+    float4* orow = reinterpret_cast<float4*>(static_cast<float*>(out) + size_t(text) * D);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int g = lane + 32 * i;
+      if (g < G) orow[g] = make_float4(acc[i][0] * inv, acc[i][1] * inv, acc[i][2] * inv, acc[i][3] * inv);
+    }
   }
 }
 
@@ -805,13 +816,18 @@ cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* g
 }
 
 cudaError_t launch_meanpool_l2(const uint16_t* x, const int32_t* cu, int64_t n_texts, int32_t tok0, int d,
-                               float* out, cudaStream_t st, int pooling) {
+                               void* out, cudaStream_t st, int pooling, bool out_bf16) {
   if (n_texts <= 0) return cudaSuccess;
   const unsigned grid = blocks_for_warps(n_texts, 8);
-#define SURGE_POOL(DD)                                                                                   \
-  case DD:                                                                                               \
-    if (pooling == 1) meanpool_l2_kernel<DD, true><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);     \
-    else meanpool_l2_kernel<DD, false><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);                 \
+#define SURGE_POOL(DD)                                                                                          \
+  case DD:                                                                                                      \
+    if (out_bf16) {                                                                                             \
+      if (pooling == 1) meanpool_l2_kernel<DD, true, true><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);    \
+      else meanpool_l2_kernel<DD, false, true><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);                \
+    } else {                                                                                                    \
+      if (pooling == 1) meanpool_l2_kernel<DD, true><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);          \
+      else meanpool_l2_kernel<DD, false><<<grid, 256, 0, st>>>(x, cu, n_texts, tok0, out);                      \
+    }                                                                                                           \
     break;
   switch (d) {
     SURGE_POOL(64)

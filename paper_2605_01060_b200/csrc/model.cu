@@ -37,6 +37,53 @@ cudaError_t Workspace::alloc(const ModelShape& s, int64_t cap_tokens) {
   return cudaSuccess;
 }
 
+int32_t* PinnedRing::acquire(size_t n, int* slot) {
+  const int j = next;
+  next = (next + 1) % NS;
+  if (ev[j]) cudaEventSynchronize(ev[j]);   // the slot's previous copy has run
+  else if (cudaEventCreateWithFlags(&ev[j], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  if (cap[j] < n) {
+    if (buf[j]) cudaFreeHost(buf[j]);
+    buf[j] = nullptr;
+    const size_t c = n < 4096 ? 4096 : 2 * n;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&buf[j]), c * sizeof(int32_t), cudaHostAllocPortable) != cudaSuccess) {
+      cap[j] = 0;
+      return nullptr;
+    }
+    cap[j] = c;
+  }
+  *slot = j;
+  return buf[j];
+}
+
+cudaError_t PinnedRing::copy(int slot, int32_t* dst, size_t n, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(dst, buf[slot], n * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  return cudaEventRecord(ev[slot], st);
+}
+
+cudaError_t PinnedRing::upload(int32_t* dst, const int32_t* src, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  int slot = 0;
+  int32_t* h = acquire(n, &slot);
+  if (!h) return cudaErrorMemoryAllocation;
+  std::memcpy(h, src, n * sizeof(int32_t));
+  return copy(slot, dst, n, st);
+}
+
+void PinnedRing::release() {
+  for (int j = 0; j < NS; ++j) {
+    if (ev[j]) {
+      cudaEventSynchronize(ev[j]);
+      cudaEventDestroy(ev[j]);
+    }
+    if (buf[j]) cudaFreeHost(buf[j]);
+    ev[j] = nullptr;
+    buf[j] = nullptr;
+    cap[j] = 0;
+  }
+}
+
 void Workspace::release() {
   for (uint16_t** p : {&X, &QKV, &O, &X1, &H}) {
     if (*p) cudaFree(*p);
@@ -236,7 +283,7 @@ Profiler::~Profiler() {
 }
 
 cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, int64_t s0,
-                                      int64_t s1, int32_t tok0, int32_t ntok, float* d_out, cudaStream_t st,
+                                      int64_t s1, int32_t tok0, int32_t ntok, void* d_out, cudaStream_t st,
                                       int64_t* launches, Profiler* prof, const int32_t* host_cu) const {
   const int64_t n = s1 - s0;
   if (n <= 0) return cudaSuccess;
@@ -264,8 +311,8 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     tiles.reserve(size_t(s1 - s0) + 4);
     n_tiles = att_tiles_for(host_cu, s0, s1, tiles);
     if (n_tiles > att_max_tiles(ntok)) return cudaErrorInvalidValue;
-    if (n_tiles > 0) {   // pageable source: staged by the runtime before the call returns
-      SURGE_TRY(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, st));
+    if (n_tiles > 0) {
+      SURGE_TRY(ws.tables.upload(ws.tiles, tiles.data(), tiles.size(), st));
       const int dh = d / s_.heads;
       SURGE_TRY(launch_att_records(ws.tiles, n_tiles, d_cu, tok0, ATT_SLICE / (3 * dh) / att_unit_heads(dh),
                                    ws.att_rec, st));
@@ -280,8 +327,8 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       sum_l2 += double(li) * double(li);
       if (li > 64) long_texts.push_back(int32_t(i - s0));
     }
-    if (!long_texts.empty() && !att_fused)   // pageable source: staged by the runtime before the call returns
-      SURGE_TRY(cudaMemcpyAsync(ws.long_idx, long_texts.data(), long_texts.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!long_texts.empty() && !att_fused)
+      SURGE_TRY(ws.tables.upload(ws.long_idx, long_texts.data(), long_texts.size(), st));
   }
   const double M = ntok, D = d, F = f;
   cudaEvent_t ev = nullptr;
@@ -375,15 +422,16 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     k += fused ? 2 : 3;
   }
   if (P) prof->begin(st, &ev);
-  SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, d_out + s0 * d, st, pooling_));
-  if (P) prof->end(KK_POOL, st, ev, 0.0, M * 2 * D + double(n) * 4 * D);
+  SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, static_cast<uint8_t*>(d_out) + size_t(s0) * d * out_elem_bytes(),
+                               st, pooling_, out_bf16_));
+  if (P) prof->end(KK_POOL, st, ev, 0.0, M * 2 * D + double(n) * double(out_elem_bytes()) * D);
   ++k;
   if (launches) *launches += k;
   return cudaSuccess;
 }
 
 cudaError_t DeviceModel::encode(Workspace& ws, const int32_t* d_ids, const int32_t* d_cu, const int32_t* host_cu,
-                                int64_t n_texts, float* d_out, cudaStream_t st, int64_t* launches,
+                                int64_t n_texts, void* d_out, cudaStream_t st, int64_t* launches,
                                 Profiler* prof) const {
   int64_t s0 = 0;
   while (s0 < n_texts) {

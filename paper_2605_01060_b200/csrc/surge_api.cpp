@@ -9,6 +9,8 @@
 //        -> host callback: pieces whose last row landed become pollable (TTFO)
 //   poll / release (any thread): zero-copy views E[start:end] into the pinned output
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types and prototypes only: libnccl.so.2 is opened at run time (nccl_api())
 
 #include <algorithm>
 #include <atomic>
@@ -119,6 +121,7 @@ struct SuperBatch {
   PinnedBuf out;                             // float [local_texts x d]
   int64_t delivered_pieces = 0;              // pushed to the ready queue
   int64_t released_pieces = 0;
+  std::vector<uint8_t> piece_state;          // per piece: 0 in flight/ready, 1 polled, 2 released
   bool done = false;                         // all local rows on the host
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   double encode_ms = -1.0;
@@ -129,6 +132,40 @@ struct Ready {
   int64_t piece;        // index into sb->pieces
   uint64_t key;
 };
+
+// NCCL, resolved with dlopen on first use (K11: the one-time weight broadcast).  In a process that
+// already loaded NCCL (e.g. through torch.distributed) dlopen returns that library; libsurge itself
+// has no link-time NCCL dependency, so it loads and runs single-GPU without it.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      a.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+      return a;
+    }
+    a.get_unique_id = reinterpret_cast<decltype(&ncclGetUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(lib, "ncclCommInitRank"));
+    a.broadcast = reinterpret_cast<decltype(&ncclBroadcast)>(dlsym(lib, "ncclBroadcast"));
+    a.comm_destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(lib, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(lib, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.broadcast && a.comm_destroy && a.error_string;
+    if (!a.ok) a.why = "libnccl.so.2 lacks an expected symbol";
+    return a;
+  }();
+  return api;
+}
 
 struct ChunkDone {
   Ctx* ctx;
@@ -157,7 +194,7 @@ struct Ctx {
   size_t cap_ids[2] = {0, 0}, cap_texts[2] = {0, 0}, cap_pieces[2] = {0, 0};
   size_t cap_cu[2] = {0, 0}, cap_ro[2] = {0, 0}, cap_to[2] = {0, 0};
   cudaEvent_t slot_free[2] = {nullptr, nullptr};   // compute finished with input slot
-  float* d_E[2] = {nullptr, nullptr};
+  uint8_t* d_E[2] = {nullptr, nullptr};           // pooled rows of a chunk (out_dtype elements)
   cudaEvent_t e_free[2] = {nullptr, nullptr};      // D2H finished reading chunk buffer
   cudaEvent_t e_ready[2] = {nullptr, nullptr};     // chunk rows written
   int64_t chunk_counter = 0;
@@ -169,7 +206,7 @@ struct Ctx {
   std::mutex api_mu;
   // api-path gather scratch (world_size > 1)
   int32_t *api_ids = nullptr, *api_len = nullptr, *api_sizes = nullptr, *api_ro = nullptr, *api_to = nullptr;
-  float* api_out = nullptr;
+  uint8_t* api_out = nullptr;
   size_t api_ids_cap = 0, api_len_cap = 0, api_sizes_cap = 0, api_ro_cap = 0, api_to_cap = 0, api_out_cap = 0;
   // per-kernel-class timing
   std::mutex prof_mu;
@@ -195,8 +232,10 @@ struct Ctx {
   int64_t inflight_sbs = 0, inflight_texts = 0, pending_pieces = 0;
   bool shutdown = false;
   int poisoned = 0;
+  uint64_t generation = 0;           // incremented by surge_reset: tokens of an older stream are rejected
   std::string err;
   std::thread worker;
+  ncclComm_t nccl = nullptr;         // surge_create_replicated: the world's communicator (K11)
 
   // ---- stats
   surge_stats st{};
@@ -383,9 +422,8 @@ int process_superbatch(Ctx* c, SuperBatch* sb) {
       p = q;
     }
   }
-  // piece sizes: pageable source -> the runtime stages it before returning, so the vector may die
-  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->d_sizes[slot], piece_sizes.data(), size_t(NP) * 4, cudaMemcpyHostToDevice,
-                                  c->s_h2d));
+  // piece sizes through the pinned ring (a pageable source would synchronise s_h2d)
+  CUDA_OR_FAIL(c, c->ws.tables.upload(c->d_sizes[slot], piece_sizes.data(), size_t(NP), c->s_h2d));
   cudaEvent_t h2d_done;
   CUDA_OR_FAIL(c, cudaEventCreateWithFlags(&h2d_done, cudaEventDisableTiming));
   CUDA_OR_FAIL(c, cudaEventRecord(h2d_done, c->s_h2d));
@@ -412,7 +450,8 @@ int process_superbatch(Ctx* c, SuperBatch* sb) {
     CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->s_comp, c->e_free[b], 0));
     int64_t nl = 0;
     // encode into d_E[b] rows [0, s1-s0): pass d_out shifted so that row s0 maps to d_E[b][0]
-    float* dout = c->d_E[b] - s0 * d;
+    const size_t eb = c->model.out_elem_bytes();
+    uint8_t* dout = c->d_E[b] - size_t(s0) * d * eb;
     cudaError_t e;
     {
       std::lock_guard<std::mutex> pg(c->prof_mu);
@@ -431,7 +470,7 @@ int process_superbatch(Ctx* c, SuperBatch* sb) {
       CUDA_OR_FAIL(c, cudaEventRecord(c->slot_free[slot], c->s_comp));
     }
     CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->s_d2h, c->e_ready[b], 0));
-    CUDA_OR_FAIL(c, cudaMemcpyAsync(static_cast<float*>(sb->out.p) + s0 * d, c->d_E[b], size_t(s1 - s0) * d * 4,
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(static_cast<uint8_t*>(sb->out.p) + size_t(s0) * d * eb, c->d_E[b], size_t(s1 - s0) * d * eb,
                                     cudaMemcpyDeviceToHost, c->s_d2h));
     CUDA_OR_FAIL(c, cudaEventRecord(c->e_free[b], c->s_d2h));
     ChunkDone* cd = new ChunkDone{c, sb, s1, last};
@@ -500,14 +539,15 @@ int seal(Ctx* c, int reason) {
     sb->local_tokens += p.tokens;
   }
   sb->local_texts = lrow;
+  sb->piece_state.assign(sb->pieces.size(), 0);
   cudaEventCreate(&sb->ev_begin);
   cudaEventCreate(&sb->ev_end);
   {
     std::lock_guard<std::mutex> g(c->mu);
     sb->index = int64_t(c->sbs.size());
-    sb->out = take_from_pool(c->out_pool, size_t(sb->local_texts) * c->shape.d * 4);
+    sb->out = take_from_pool(c->out_pool, size_t(sb->local_texts) * c->shape.d * c->model.out_elem_bytes());
   }
-  if (!ensure_pinned(sb->out, size_t(std::max<int64_t>(sb->local_texts, 1)) * c->shape.d * 4)) {
+  if (!ensure_pinned(sb->out, size_t(std::max<int64_t>(sb->local_texts, 1)) * c->shape.d * c->model.out_elem_bytes())) {
     c->set_error(SURGE_E_OOM, "pinned output allocation failed");
     return SURGE_E_OOM;
   }
@@ -565,12 +605,14 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
       !(dh == 16 || dh == 32 || dh == 64) || k.ffn % 64 != 0 || k.heads % 2 != 0)
     return SURGE_E_INVALID_ARG;
   if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return SURGE_E_INVALID_ARG;
+  if (k.out_dtype != SURGE_F32 && k.out_dtype != SURGE_BF16) return SURGE_E_INVALID_ARG;
   ModelShape s{k.vocab_size, k.max_position, k.type_vocab_size, k.hidden, k.layers, k.heads, k.ffn, k.ln_eps};
   if (n_weights != blob_elems(s)) return SURGE_E_INVALID_ARG;
 
   auto c = std::make_unique<surge_ctx>();
   c->cfg = k;
   c->shape = s;
+  c->model.set_out_bf16(k.out_dtype == SURGE_BF16);
   c->device = k.device;
   if (c->cfg.chunk_tokens <= 0) c->cfg.chunk_tokens = 524288;   // sweep: 131K 2.91M, 262K 3.00M, 524K 3.04M, 1M 3.06M texts/s (TTFO 7 / 9 / 16 / 28 ms)
   c->cfg.chunk_tokens = std::max(c->cfg.chunk_tokens, k.max_position);
@@ -595,7 +637,8 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
   if ((e = C->model.init(s, weights, k.weights_on_device != 0, C->s_comp)) != cudaSuccess) return fail(e);
   if ((e = C->ws.alloc(s, C->cfg.chunk_tokens)) != cudaSuccess) return SURGE_E_OOM;
   for (int b = 0; b < 2; ++b) {
-    if ((e = cudaMalloc(&C->d_E[b], size_t(C->cfg.chunk_tokens) * s.d * 4)) != cudaSuccess) return SURGE_E_OOM;
+    if ((e = cudaMalloc(&C->d_E[b], size_t(C->cfg.chunk_tokens) * s.d * C->model.out_elem_bytes())) != cudaSuccess)
+      return SURGE_E_OOM;
     if ((e = cudaEventCreateWithFlags(&C->e_free[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
     if ((e = cudaEventCreateWithFlags(&C->e_ready[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
     if ((e = cudaEventCreateWithFlags(&C->slot_free[b], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
@@ -606,6 +649,67 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
   C->worker = std::thread(surge::worker_main, C);
   C->st.init_s = secs(t0, Clock::now());
   *out = c.release();
+  return SURGE_OK;
+}
+
+surge_status surge_nccl_unique_id(uint8_t* id) {
+  using namespace surge;
+  if (!id) return SURGE_E_INVALID_ARG;
+  const NcclApi& a = nccl_api();
+  if (!a.ok) return SURGE_E_NCCL;
+  ncclUniqueId u;
+  if (a.get_unique_id(&u) != ncclSuccess) return SURGE_E_NCCL;
+  std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  return SURGE_OK;
+}
+
+surge_status surge_create_replicated(const surge_config* cfg, const uint8_t* nccl_id, const uint16_t* weights,
+                                     size_t n_weights, surge_handle* out) {
+  using namespace surge;
+  if (!cfg || !nccl_id || !out || (cfg->rank == 0 && !weights)) return SURGE_E_INVALID_ARG;
+  *out = nullptr;
+  const surge_config& k = *cfg;
+  if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return SURGE_E_INVALID_ARG;
+  ModelShape s{k.vocab_size, k.max_position, k.type_vocab_size, k.hidden, k.layers, k.heads, k.ffn, k.ln_eps};
+  if (k.hidden <= 0 || k.ffn <= 0 || k.layers <= 0 || k.vocab_size <= 0 || n_weights != blob_elems(s))
+    return SURGE_E_INVALID_ARG;
+  const NcclApi& a = nccl_api();
+  if (!a.ok) return SURGE_E_NCCL;
+  const auto t0 = Clock::now();
+  if (cudaSetDevice(k.device) != cudaSuccess) return SURGE_E_CUDA;
+  ncclUniqueId u;
+  std::memcpy(u.internal, nccl_id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t comm = nullptr;
+  if (a.comm_init_rank(&comm, k.world_size, u, k.rank) != ncclSuccess) return SURGE_E_NCCL;
+  uint16_t* blob = nullptr;
+  cudaStream_t st = nullptr;
+  surge_status rc = SURGE_OK;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&blob, n_weights * 2) != cudaSuccess) {
+    rc = SURGE_E_OOM;
+  } else {
+    if (k.rank == 0 &&
+        cudaMemcpyAsync(blob, weights, n_weights * 2, k.weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        st) != cudaSuccess)
+      rc = SURGE_E_CUDA;
+    // K11: one broadcast of the bf16 blob from rank 0 over NVLink / NVSwitch (bytes: NCCL has no 16-bit int type)
+    if (rc == SURGE_OK && a.broadcast(blob, blob, n_weights * 2, ncclUint8, 0, comm, st) != ncclSuccess) rc = SURGE_E_NCCL;
+    if (rc == SURGE_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = SURGE_E_CUDA;
+  }
+  if (rc == SURGE_OK) {
+    surge_config c2 = k;
+    c2.weights_on_device = 1;
+    rc = surge_create(&c2, blob, n_weights, out);
+  }
+  if (blob) cudaFree(blob);
+  if (st) cudaStreamDestroy(st);
+  if (rc != SURGE_OK) {
+    a.comm_destroy(comm);
+    return rc;
+  }
+  (*out)->nccl = comm;
+  (*out)->cfg.weights_on_device = k.weights_on_device;
+  (*out)->st.init_s = secs(t0, Clock::now());
   return SURGE_OK;
 }
 
@@ -624,6 +728,11 @@ surge_status surge_submit_partition(surge_handle h, uint64_t partition_id, const
     const int32_t l = lengths[i];
     if (l < 1 || l > maxp) return SURGE_E_TOO_LONG;
     ntok += l;
+  }
+  if (c->total_tokens + ntok >= (int64_t(1) << 31)) {   // int32 token offsets of one SuperBatch
+    std::lock_guard<std::mutex> g(c->mu);
+    c->err = "surge_submit_partition: the open SuperBatch would reach 2^31 tokens";
+    return SURGE_E_INVALID_ARG;
   }
   {
     const uint32_t V = uint32_t(c->cfg.vocab_size);
@@ -720,7 +829,7 @@ surge_status surge_poll_flushed(surge_handle h, surge_flushed* out, int64_t max_
     surge_flushed& f = out[n++];
     f.partition_id = r.key;
     f.d = c->shape.d;
-    f.dtype = 0;
+    f.dtype = c->cfg.out_dtype;
     if (!r.sb) {
       f.row_begin = 0;
       f.n_rows = 0;
@@ -734,9 +843,12 @@ surge_status surge_poll_flushed(surge_handle h, surge_flushed* out, int64_t max_
     f.row_begin = p.first_row - r.sb->text_off[p.member];
     f.n_rows = p.n_rows;
     f.partition_rows = r.sb->sizes[p.member];
-    f.data = static_cast<const float*>(r.sb->out.p) + r.sb->piece_local_row[r.piece] * c->shape.d;
+    f.data = static_cast<const uint8_t*>(r.sb->out.p) +
+             size_t(r.sb->piece_local_row[r.piece]) * c->shape.d * c->model.out_elem_bytes();
     f.superbatch = r.sb->index;
-    f.token = (uint64_t(r.sb->index) << 24) | uint64_t(r.piece);
+    // token: stream generation (16 bits) | SuperBatch index (28 bits) | piece (20 bits)
+    f.token = ((c->generation & 0xffff) << 48) | (uint64_t(r.sb->index) << 20) | uint64_t(r.piece);
+    r.sb->piece_state[r.piece] = 1;
     c->pending_pieces -= 1;
   }
   *n_out = n;
@@ -749,8 +861,19 @@ surge_status surge_release(surge_handle h, const surge_flushed* rec) {
   if (!c || !rec) return SURGE_E_INVALID_ARG;
   if (rec->superbatch < 0) return SURGE_OK;
   std::lock_guard<std::mutex> g(c->mu);
-  if (rec->superbatch >= int64_t(c->sbs.size())) return SURGE_E_INVALID_ARG;
+  const uint64_t gen = rec->token >> 48, sbi = (rec->token >> 20) & ((uint64_t(1) << 28) - 1),
+                 piece = rec->token & ((uint64_t(1) << 20) - 1);
+  if (gen != (c->generation & 0xffff) || int64_t(sbi) != rec->superbatch || rec->superbatch >= int64_t(c->sbs.size())) {
+    c->err = "surge_release: record is not from the current stream";
+    return SURGE_E_INVALID_ARG;
+  }
   SuperBatch* sb = c->sbs[rec->superbatch].get();
+  if (piece >= sb->piece_state.size() || sb->piece_state[piece] != 1) {
+    c->err = sb && piece < sb->piece_state.size() && sb->piece_state[piece] == 2 ? "surge_release: piece released twice"
+                                                                                   : "surge_release: piece not polled";
+    return SURGE_E_INVALID_ARG;
+  }
+  sb->piece_state[piece] = 2;
   sb->released_pieces += 1;
   if (sb->done && sb->released_pieces == int64_t(sb->pieces.size()) && sb->out.p) {
     c->out_pool.push_back(sb->out);
@@ -774,6 +897,11 @@ surge_status surge_reset(surge_handle h) {
   if (int r = check_handle(c)) return surge_status(r);
   std::lock_guard<std::mutex> g(c->mu);
   if (!c->finished || c->inflight_sbs != 0 || c->pending_pieces != 0 || !c->ready.empty()) return SURGE_E_STATE;
+  for (auto& sbp : c->sbs)   // every polled view must have been released: the buffers are reused
+    if (sbp->released_pieces != int64_t(sbp->pieces.size())) {
+      c->err = "surge_reset: polled pieces not yet released";
+      return SURGE_E_STATE;
+    }
   for (auto& sbp : c->sbs) {
     if (sbp->out.p) c->out_pool.push_back(sbp->out);
     if (sbp->stage.p) c->stage_pool.push_back(sbp->stage);
@@ -782,6 +910,7 @@ surge_status surge_reset(surge_handle h) {
   }
   c->sbs.clear();
   c->seen.clear();
+  c->generation += 1;
   c->finished = false;
   c->total = c->total_tokens = 0;
   c->have_first_submit = false;
@@ -892,12 +1021,13 @@ void surge_destroy(surge_handle h) {
     if (p) cudaFree(p);
   for (cudaStream_t s : {c->s_comp, c->s_h2d, c->s_d2h})
     if (s) cudaStreamDestroy(s);
+  if (c->nccl) nccl_api().comm_destroy(c->nccl);
   delete static_cast<surge_ctx*>(c);
 }
 
 // ------------------------------------------------------------------------------- device-level
 surge_status surge_encode_packed(surge_handle h, const int32_t* d_ids, const int32_t* d_lengths,
-                                 const int32_t* h_lengths, int64_t n_texts, float* d_out, void* stream) {
+                                 const int32_t* h_lengths, int64_t n_texts, void* d_out, void* stream) {
   using namespace surge;
   Ctx* c = h;
   if (int r = check_handle(c)) return surge_status(r);
@@ -932,7 +1062,7 @@ surge_status surge_encode_packed(surge_handle h, const int32_t* d_ids, const int
 
 surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const int32_t* d_lengths,
                                      const int32_t* h_lengths, int64_t n_texts, const int64_t* h_sizes,
-                                     int64_t n_members, float* d_out, void* stream) {
+                                     int64_t n_members, void* d_out, void* stream) {
   using namespace surge;
   Ctx* c = h;
   if (int r = check_handle(c)) return surge_status(r);
@@ -985,18 +1115,18 @@ surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const
   }
   const int32_t* ids = d_ids;
   const int32_t* lens = d_lengths;
-  float* out = d_out;
+  void* out = d_out;
+  const size_t eb = c->model.out_elem_bytes();
   CUDA_OR_FAIL(c, ensure_dev(&c->api_cu, c->api_cu_cap, size_t(LS + 1)));
   CUDA_OR_FAIL(c, ensure_dev(&c->api_sizes, c->api_sizes_cap, size_t(NP + 1)));
   CUDA_OR_FAIL(c, ensure_dev(&c->api_ro, c->api_ro_cap, size_t(NP + 1)));
   CUDA_OR_FAIL(c, ensure_dev(&c->api_to, c->api_to_cap, size_t(NP + 1)));
-  // pageable source: the runtime stages it before returning
-  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->api_sizes, psz.data(), size_t(NP) * 4, cudaMemcpyHostToDevice, st));
+  CUDA_OR_FAIL(c, c->ws_api.tables.upload(c->api_sizes, psz.data(), size_t(NP), st));
   if (!direct) {
     // gather this rank's pieces into contiguous local buffers (device-to-device)
     CUDA_OR_FAIL(c, ensure_dev(&c->api_ids, c->api_ids_cap, size_t(host_cu[LS])));
     CUDA_OR_FAIL(c, ensure_dev(&c->api_len, c->api_len_cap, size_t(LS)));
-    CUDA_OR_FAIL(c, ensure_dev(&c->api_out, c->api_out_cap, size_t(LS) * d));
+    CUDA_OR_FAIL(c, ensure_dev(&c->api_out, c->api_out_cap, size_t(LS) * d * eb));
     int64_t r = 0;
     for (const LptPiece& p : mine) {
       const int64_t t0 = gtok[p.first_row], t1 = gtok[p.first_row + p.n_rows];
@@ -1021,7 +1151,8 @@ surge_status surge_encode_superbatch(surge_handle h, const int32_t* d_ids, const
   if (!direct) {
     int64_t r = 0;
     for (const LptPiece& p : mine) {   // scatter rows to their SuperBatch positions
-      CUDA_OR_FAIL(c, cudaMemcpyAsync(d_out + p.first_row * d, c->api_out + r * d, size_t(p.n_rows) * d * 4,
+      CUDA_OR_FAIL(c, cudaMemcpyAsync(static_cast<uint8_t*>(d_out) + size_t(p.first_row) * d * eb,
+                                      c->api_out + size_t(r) * d * eb, size_t(p.n_rows) * d * eb,
                                       cudaMemcpyDeviceToDevice, st));
       r += p.n_rows;
     }

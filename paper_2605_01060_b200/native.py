@@ -44,13 +44,13 @@ class surge_config(C.Structure):
                 ("ln_eps", C.c_float), ("b_min", C.c_int64), ("b_max", C.c_int64),
                 ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
                 ("chunk_tokens", C.c_int32), ("max_inflight", C.c_int32), ("nonblocking_submit", C.c_int32),
-                ("weights_on_device", C.c_int32)]
+                ("weights_on_device", C.c_int32), ("out_dtype", C.c_int32)]
 
 
 class surge_flushed(C.Structure):
     _fields_ = [("partition_id", C.c_uint64), ("row_begin", C.c_int64), ("n_rows", C.c_int64),
                 ("partition_rows", C.c_int64), ("d", C.c_int32), ("dtype", C.c_int32),
-                ("data", C.POINTER(C.c_float)), ("superbatch", C.c_int64), ("token", C.c_uint64)]
+                ("data", C.c_void_p), ("superbatch", C.c_int64), ("token", C.c_uint64)]
 
 
 class surge_stats(C.Structure):
@@ -77,6 +77,7 @@ SURGE_OPT_MLP_FUSED = 2
 SURGE_OPT_TAIL_FUSED = 3
 SURGE_OPT_POOLING = 4
 SURGE_POOL_MEAN, SURGE_POOL_CLS = 0, 1
+SURGE_F32, SURGE_BF16 = 0, 1
 
 
 class surge_superbatch_info(C.Structure):
@@ -91,6 +92,8 @@ _i32p, _i64p, _u16p, _f32p, _u64p = (C.POINTER(C.c_int32), C.POINTER(C.c_int64),
 _SIGS = {
     "surge_version": (C.c_char_p, []),
     "surge_create": (C.c_int, [C.POINTER(surge_config), _p, C.c_size_t, C.POINTER(_p)]),
+    "surge_nccl_unique_id": (C.c_int, [_p]),
+    "surge_create_replicated": (C.c_int, [C.POINTER(surge_config), _p, _p, C.c_size_t, C.POINTER(_p)]),
     "surge_submit_partition": (C.c_int, [_p, C.c_uint64, _p, _p, C.c_int64]),
     "surge_finish": (C.c_int, [_p]),
     "surge_poll_flushed": (C.c_int, [_p, C.POINTER(surge_flushed), C.c_int64, C.c_int32, _i64p]),
@@ -160,11 +163,11 @@ def surge_version() -> str:
 
 def make_config(enc, b_min: int, b_max: int, rank: int = 0, world_size: int = 1, device: int = 0,
                 chunk_tokens: int = 0, max_inflight: int = 0, nonblocking_submit: int = 0,
-                weights_on_device: int = 0) -> surge_config:
+                weights_on_device: int = 0, out_dtype: int = 0) -> surge_config:
     """surge_config from a synth.configs.EncoderConfig-like object."""
     return surge_config(enc.vocab_size, enc.max_position, enc.type_vocab_size, enc.hidden, enc.layers, enc.heads,
                         enc.ffn, enc.ln_eps, b_min, b_max, rank, world_size, device, chunk_tokens, max_inflight,
-                        nonblocking_submit, weights_on_device)
+                        nonblocking_submit, weights_on_device, out_dtype)
 
 
 def surge_create(cfg: surge_config, weights, n_weights: int | None = None):
@@ -178,6 +181,31 @@ def surge_create(cfg: surge_config, weights, n_weights: int | None = None):
         n = n_weights if n_weights is not None else weights.numel()
     h = C.c_void_p()
     _check(None, lib.surge_create(C.byref(cfg), ptr, n, C.byref(h)), "surge_create")
+    return h
+
+
+def surge_nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be handed to every rank of surge_create_replicated."""
+    buf = (C.c_uint8 * 128)()
+    _check(None, lib.surge_nccl_unique_id(buf), "surge_nccl_unique_id")
+    return bytes(buf)
+
+
+def surge_create_replicated(cfg: surge_config, nccl_id: bytes, weights=None, n_weights: int | None = None):
+    """Every rank calls this concurrently: NCCL communicator over cfg.world_size ranks, one broadcast
+    of the weight blob from rank 0 (weights: read on rank 0 only; host numpy blob or device tensor
+    when cfg.weights_on_device), then the handle as surge_create."""
+    idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+    ptr = None
+    if isinstance(weights, np.ndarray):
+        w = np.ascontiguousarray(weights, dtype=np.uint16)
+        ptr, n = w.ctypes.data, w.size
+    elif weights is not None:
+        ptr, n = _ptr(weights), (n_weights if n_weights is not None else weights.numel())
+    else:
+        n = n_weights
+    h = C.c_void_p()
+    _check(None, lib.surge_create_replicated(C.byref(cfg), idb, ptr, n, C.byref(h)), "surge_create_replicated")
     return h
 
 
@@ -204,10 +232,17 @@ def surge_poll_flushed(h, max_items: int = 4096, timeout_ms: int = 0):
 
 
 def flushed_array(rec: surge_flushed) -> np.ndarray:
-    """Zero-copy numpy view [n_rows, d] of a polled piece (valid until surge_release)."""
+    """Zero-copy numpy view [n_rows, d] of a polled piece (valid until surge_release): float32, or
+    uint16 bf16 bit patterns when the handle's out_dtype is SURGE_BF16 (see bf16_to_f32)."""
+    ct, nt = (C.c_uint16, np.uint16) if rec.dtype == SURGE_BF16 else (C.c_float, np.float32)
     if rec.n_rows == 0:
-        return np.zeros((0, rec.d), np.float32)
-    return np.ctypeslib.as_array(rec.data, shape=(rec.n_rows, rec.d))
+        return np.zeros((0, rec.d), nt)
+    return np.ctypeslib.as_array(C.cast(rec.data, C.POINTER(ct)), shape=(rec.n_rows, rec.d))
+
+
+def bf16_to_f32(a: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> float32 values (exact widening)."""
+    return (np.asarray(a, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
 
 
 def surge_release(h, rec: surge_flushed):

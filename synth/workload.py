@@ -119,3 +119,17 @@ def random_texts(n: int, vocab_size: int, max_position: int, seed: int,
             t[0], t[-1] = cls_id, sep_id
         out.append(t)
     return out
+
+
+def parity_sample(wl: "Workload", n_rows: int = 16_384, head: int = 4096, seed: int = 0) -> list:
+    """Rows of the SURVEY.md §8(c) C2 parity sample: the first `head` rows in stream order, the first
+    and last row of every partition, then seeded uniform rows up to `n_rows` distinct rows (sorted)."""
+    rows = set(range(min(head, wl.n_texts)))
+    for k in range(len(wl.sizes)):
+        if wl.sizes[k] > 0:
+            rows |= {int(wl.text_off[k]), int(wl.text_off[k + 1]) - 1}
+    rng = np.random.default_rng(seed)
+    n_rows = min(n_rows, wl.n_texts)
+    while len(rows) < n_rows:
+        rows |= set(rng.integers(0, wl.n_texts, size=n_rows - len(rows)).tolist())
+    return sorted(rows)

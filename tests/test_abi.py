@@ -105,3 +105,11 @@ def test_native_aggregate_equals_oracle():
         assert [r for _, _, r in sbs] == [s.reason for s in A.flushes]
         got = [[k for k in range(a, b) if sizes[k] > 0] for a, b, _ in sbs]
         assert got == [list(s.keys) for s in A.flushes]
+
+
+def test_nccl_unique_id_without_gpu():
+    """K11 plumbing: libsurge resolves NCCL at run time (dlopen) and hands out the 128-byte unique id
+    every rank of surge_create_replicated needs; the id is fresh per call."""
+    from paper_2605_01060_b200 import native as N
+    a, b = N.surge_nccl_unique_id(), N.surge_nccl_unique_id()
+    assert len(a) == len(b) == 128 and a != b

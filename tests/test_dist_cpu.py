@@ -129,3 +129,33 @@ def test_reference_arm_under_torchrun():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "texts/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_bench_gpus_n_spawns_ranks(gpus):
+    """`bench.py --gpus N` outside torchrun launches the N ranks itself (torch.distributed.run on
+    127.0.0.1); --host-only runs each rank's host plan (Alg.1 + LPT through libsurge) over gloo and
+    rank 0 reports every rank's share: together they cover the stream exactly, within one LPT piece
+    of each other per SuperBatch."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--host-only",
+           "--n-texts", "300000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_ranks"] == gpus and d["backend"] == "gloo"
+    assert sum(d["texts_per_rank"]) == d["n_texts"] == 300_000
+    assert sum(d["tokens_per_rank"]) == d["n_tokens"]
+    assert max(d["tokens_per_rank"]) - min(d["tokens_per_rank"]) <= d["superbatches"] * d["n_tokens"] / (8 * gpus)
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    """Under a launcher, --gpus must equal the number of ranks (a SCALE run never silently measures
+    fewer GPUs than it reports)."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--host-only"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode != 0 and "--gpus 2" in r.stderr

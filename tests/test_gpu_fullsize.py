@@ -3,8 +3,8 @@ launch configuration bench.py times (device-resident SuperBatches through surge_
 the streaming ABI from host memory as bench.py's e2e):
   * integer parity: Alg. 1 flush decisions (membership, order, reasons) == the oracle's, bit-exact;
   * every one of the 10M rows: finite and unit-norm (|norm - 1| <= 1e-5);
-  * sampled rows (first rows of the stream, first/last row of random partitions, uniform random rows)
-    vs the fp64 oracle, one text at a time, under the north-star gate;
+  * the SURVEY §8(c) 16,384-row sample (first 4,096 rows, first and last row of every partition, seeded
+    uniform rows) vs the fp64 oracle, one text at a time over all host cores, under the north-star gate;
   * the streaming path returns the same rows bit for bit (sampled partitions) with the right counts.
 """
 import numpy as np
@@ -12,14 +12,21 @@ import pytest
 import torch
 
 from oracle import aggregator as oagg
-from oracle import encoder as oenc
+from oracle import pool as opool
 from synth.configs import ENCODERS, WORKLOADS
 from synth.weights import make_weights, pack_blob
-from synth.workload import make_workload
+from synth.workload import make_workload, parity_sample
 
 pytestmark = pytest.mark.gpu
 
 COS_MIN, ABS_MAX, NORM_TOL = 0.999, 1e-2, 1e-5
+SAMPLE_ROWS = 16_384
+
+
+def c2_parity_sample(wl, seed: int = 0):
+    """SURVEY.md §8(c) "C2: a 16,384-row sample = the first 4,096 rows in stream order + the first and
+    last row of every partition (<= 8,000) + the rest uniformly random (seeded)"."""
+    return parity_sample(wl, SAMPLE_ROWS, 4096, seed)
 
 
 @pytest.fixture(scope="module")
@@ -59,22 +66,20 @@ def test_full_c2_device_path_and_streaming(setup):
         assert bool(torch.isfinite(out).all())
         norms = out.norm(dim=1)
         assert float((norms - 1).abs().max()) <= NORM_TOL
-        # sampled rows vs the oracle
-        rng = np.random.default_rng(0)
-        parts = rng.choice(len(wl.sizes), size=8, replace=False)
-        rows = set(range(16))
-        for k in parts:
-            rows |= {int(wl.text_off[k]), int(wl.text_off[k + 1]) - 1}
-        rows |= set(rng.integers(0, wl.n_texts, size=16).tolist())
-        rows = sorted(rows)
+        # the SURVEY §8(c) C2 parity sample vs the fp64 oracle (all host cores)
+        rows = c2_parity_sample(wl)
+        assert len(rows) == SAMPLE_ROWS
         ends = np.cumsum(wl.lengths, dtype=np.int64)
         starts = ends - wl.lengths
-        E = oenc.Encoder(ecfg, w)
-        ref = np.stack([E.encode_text(wl.ids[starts[i]:ends[i]]) for i in rows])
+        ref, secs, procs = opool.encode_rows(ecfg, w, wl.ids, starts, ends, rows)
+        print(f"oracle: {len(rows)} rows on {procs} processes in {secs:.1f}s")
         got = out[torch.tensor(rows, device="cuda")].cpu().numpy().astype(np.float64)
         cos = (got * ref).sum(1) / (np.linalg.norm(got, axis=1) * np.linalg.norm(ref, axis=1))
         assert cos.min() >= COS_MIN, cos.min()
         assert np.abs(got - ref).max() <= ABS_MAX
+        rng = np.random.default_rng(0)
+        parts = rng.choice(len(wl.sizes), size=8, replace=False)
+        rows = sorted(set(rows[:16]) | {int(wl.text_off[k]) for k in parts} | {int(wl.text_off[k + 1]) - 1 for k in parts})
         dev_rows = {i: out[i].cpu().numpy() for i in rows}
         del out
         torch.cuda.empty_cache()
@@ -109,5 +114,84 @@ def test_full_c2_device_path_and_streaming(setup):
         assert len(seen) >= 8
         for g, v in seen.items():
             assert np.array_equal(v, dev_rows[g])
+    finally:
+        N.surge_destroy(h)
+
+
+def test_sigma25_safety_superbatch(setup):
+    """C2 at sigma = 2.5 (tab:sigma-sweep P:764-785): the Safety branch fires once and carries a
+    567,878-text SuperBatch (reading R2/R3: literal Alg. 1, never split).  Integer parity of the whole
+    aggregation vs the oracle; that SuperBatch encoded on the device in bench.py's launch configuration:
+    every row unit-norm, a 4,096-row sample vs the fp64 oracle (first rows, first/last row of every
+    member, seeded uniform rows); the streaming ABI reports the same F, Safety count and Lemma-bounded
+    peak, and returns the sampled rows bit for bit."""
+    N, ecfg, _, w, _, blob = setup
+    wcfg = WORKLOADS["minilm_s2.5"]
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=0)
+    sizes = wl.sizes.astype(np.int64)
+    A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, wcfg.b_min, wcfg.b_max)
+    sbs, peak = N.surge_aggregate(sizes, wcfg.b_min, wcfg.b_max)
+    assert [r for _, _, r in sbs] == [f.reason for f in A.flushes]
+    safety = [j for j, f in enumerate(A.flushes) if f.reason == oagg.SAFETY]
+    assert len(safety) == 1 and A.flushes[safety[0]].total == 567_878
+    assert peak == A.peak_buffered == 567_878 <= wcfg.b_min - 1 + A.nmax_seen
+    a, b, _ = sbs[safety[0]]
+    t0, t1, k0, k1 = int(wl.text_off[a]), int(wl.text_off[b]), int(wl.tok_off[a]), int(wl.tok_off[b])
+    h = N.surge_create(N.make_config(ecfg, wcfg.b_min, wcfg.b_max, weights_on_device=1), blob,
+                       n_weights=blob.numel() // 2)
+    try:
+        d_ids = torch.from_numpy(wl.ids[k0:k1]).cuda()
+        d_len = torch.from_numpy(wl.lengths[t0:t1]).cuda()
+        out = torch.empty(t1 - t0, ecfg.hidden, dtype=torch.float32, device="cuda")
+        N.surge_encode_superbatch(h, d_ids, d_len, wl.lengths[t0:t1], sizes[a:b], out, torch.cuda.Stream())
+        torch.cuda.synchronize()
+        assert float((out.norm(dim=1) - 1).abs().max()) <= NORM_TOL
+        rows = set(range(1024))
+        for k in range(a, b):
+            rows |= {int(wl.text_off[k]) - t0, int(wl.text_off[k + 1]) - 1 - t0}
+        rng = np.random.default_rng(25)
+        while len(rows) < 4096:
+            rows |= set(rng.integers(0, t1 - t0, size=4096 - len(rows)).tolist())
+        rows = sorted(rows)
+        ends = np.cumsum(wl.lengths, dtype=np.int64)
+        starts = ends - wl.lengths
+        ref, _, _ = opool.encode_rows(ecfg, w, wl.ids, starts, ends, [t0 + r for r in rows])
+        got = out[torch.tensor(rows, device="cuda")].cpu().numpy().astype(np.float64)
+        cos = (got * ref).sum(1) / (np.linalg.norm(got, axis=1) * np.linalg.norm(ref, axis=1))
+        assert cos.min() >= COS_MIN, cos.min()
+        assert np.abs(got - ref).max() <= ABS_MAX
+        dev = {t0 + r: got[i] for i, r in enumerate(rows[:64])}
+        del out
+        # streaming ABI over the whole sigma = 2.5 stream
+        key_to_k = {int(wl.keys[k]): k for k in range(a, b)}
+        seen, n_rows = {}, 0
+
+        def drain(timeout):
+            nonlocal n_rows
+            for r in N.surge_poll_flushed(h, 4096, timeout):
+                n_rows += r.n_rows
+                k = key_to_k.get(int(r.partition_id))
+                if k is not None:
+                    arr, base = N.flushed_array(r), int(wl.text_off[k]) + int(r.row_begin)
+                    for g in dev:
+                        if base <= g < base + r.n_rows:
+                            seen[g] = arr[g - base].astype(np.float64)
+                N.surge_release(h, r)
+
+        for k in range(len(wl.sizes)):
+            key, ids, lens = wl.partition(k)
+            N.surge_submit_partition(h, key, ids, lens)
+            drain(0)
+        N.surge_finish(h)
+        while N.surge_pending(h) > 0:
+            drain(20)
+        drain(0)
+        st = N.surge_get_stats(h)
+        assert n_rows == wl.n_texts
+        assert st["superbatches"] == len(A.flushes) and st["safety_flushes"] == 1
+        assert st["peak_buffered_texts"] == 567_878
+        assert len(seen) == len(dev)
+        for g, v in seen.items():
+            assert np.array_equal(v, dev[g])
     finally:
         N.surge_destroy(h)

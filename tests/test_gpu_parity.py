@@ -176,17 +176,45 @@ def test_self_invariance_bit_exact(N):
         N.surge_destroy(h)
 
 
-def test_two_ranks_on_one_gpu_cover_exactly(N):
-    """world_size=2: two handles (rank 0, rank 1) fed the same stream encode disjoint LPT pieces whose
-    union equals the world_size=1 result bit-exactly, with the oracle's LPT assignment."""
-    ecfg, wcfg = ENCODERS["toy"], scaled(WORKLOADS["toy"], n_texts=2000, n_partitions=20, b_min=300, b_max=1500)
-    w = make_weights(ecfg, seed=1234, init="pin")
+def oracle_rank_pieces(wl, b_min, b_max, world):
+    """Per rank, the set of (partition key, row_begin, n_rows) pieces the oracle's LPT plan assigns it
+    (oracle.aggregator.lpt_plan on every SuperBatch of oracle.aggregator.run_aggregator)."""
+    A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, b_min, b_max)
+    want = [set() for _ in range(world)]
+    for sb in A.flushes:
+        parts = [int(i) for i in sb.refs]
+        lengths = np.concatenate([wl.lengths[wl.text_off[k]:wl.text_off[k + 1]] for k in parts])
+        member_row = np.concatenate([[0], np.cumsum(sb.sizes)])
+        pieces, _ = oagg.lpt_plan(lengths, sb.sizes, world)
+        for p in pieces:
+            want[p.rank].add((int(sb.keys[p.member]), int(p.first_row - member_row[p.member]), int(p.n_rows)))
+    return A, want
+
+
+@pytest.mark.parametrize("enc,world", [("toy", 2), ("minilm", 2), ("minilm", 4), ("minilm", 8)])
+def test_rank_splits_cover_exactly_and_match_oracle_lpt(N, enc, world):
+    """world_size G on one GPU: G handles (rank 0..G-1) fed the same stream encode disjoint LPT pieces.
+    Each rank's pieces are exactly the oracle's LPT assignment for that rank (bit-exact integer
+    parity), and the union of all ranks' rows equals the world_size = 1 result bit for bit."""
+    ecfg = ENCODERS[enc]
+    if enc == "toy":
+        wcfg = scaled(WORKLOADS["toy"], n_texts=2000, n_partitions=20, b_min=300, b_max=1500)
+        w = make_weights(ecfg, seed=1234, init="pin")
+    else:
+        wcfg = scaled(WORKLOADS["minilm"], n_texts=24_000, n_partitions=24, b_min=5000, b_max=25_000)
+        w = make_weights(ecfg, seed=1234)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=3)
     full, sbs1, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+    A, want = oracle_rank_pieces(wl, wcfg.b_min, wcfg.b_max, world)
+    assert [s["members"] for s in sbs1] == [[int(k) for k in f.keys] for f in A.flushes]
     rows = {}
-    for rank in (0, 1):
-        _, sbs, stats, pieces = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max, rank=rank, world_size=2)
+    for rank in range(world):
+        _, sbs, stats, pieces = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max, rank=rank, world_size=world)
         assert [s["members"] for s in sbs] == [s["members"] for s in sbs1]
+        got = {(key, rb, arr.shape[0]) for key, (n, parts) in pieces.items() for rb, arr in parts.items()
+               if arr.shape[0] > 0}
+        assert got == want[rank], rank
+        assert stats["local_texts"] == sum(n for _, _, n in want[rank])
         for key, (n, parts) in pieces.items():
             for rb, arr in parts.items():
                 for i in range(arr.shape[0]):
@@ -196,9 +224,6 @@ def test_two_ranks_on_one_gpu_cover_exactly(N):
     for key, M in full.items():
         for i in range(M.shape[0]):
             assert np.array_equal(rows[(key, i)], M[i])
-    # oracle LPT: per SuperBatch, the rank-owned rows match
-    A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, wcfg.b_min, wcfg.b_max)
-    assert len(A.flushes) == len(sbs1)
 
 
 @pytest.mark.parametrize("enc,length_model", [("bgebase", "bytes47"), ("bgelarge", "long")])
@@ -374,3 +399,134 @@ def test_cls_pooling_option(N, enc):
     rows = sorted({0, len(lens) - 1, *rng.integers(0, len(lens), size=6).tolist()})
     compare(outs[N.SURGE_POOL_CLS][rows], np.stack([E.encode_text(T[i], pooling="cls") for i in rows]))
     compare(outs[N.SURGE_POOL_MEAN][rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def test_minilm_long_texts_129_to_512(N):
+    """MiniLM class (d_h = 32) with texts of 129..512 tokens: chunks holding such texts take the
+    separate QKV GEMM + long-text attention path (K/V of a text resident in smem), mixed with short
+    texts; every long row and sampled short rows vs the oracle, and the device path vs the streaming
+    path bit for bit."""
+    from oracle import pool as opool
+    ecfg = ENCODERS["minilm"]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(17)
+    edge = [129, 130, 143, 144, 145, 200, 255, 256, 257, 300, 383, 384, 385, 447, 448, 511, 512]
+    long_ = np.concatenate([edge, rng.integers(129, 513, size=23)])
+    short = rng.integers(1, 129, size=200)
+    lens = np.concatenate([short[:60], long_[:20], short[60:140], long_[20:], short[140:]]).astype(np.int32)
+    ids = rng.integers(1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    packed = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096)
+    ends = np.cumsum(lens, dtype=np.int64)
+    starts = ends - lens
+    rows = sorted(set(np.nonzero(lens > 128)[0].tolist()) | {0, 59, 60, 79, 80, len(lens) - 1}
+                  | set(rng.integers(0, len(lens), size=10).tolist()))
+    ref, _, _ = opool.encode_rows(ecfg, w, ids, starts, ends, rows)
+    compare(packed[rows], ref)
+    # the same texts through the streaming ABI as partitions (3 SuperBatches)
+    parts, off = [], 0
+    for k, n in enumerate((70, 90, 80)):
+        parts.append((1000 + k, ids[starts[off]:ends[off + n - 1]], lens[off:off + n]))
+        off += n
+    from paper_2605_01060_b200 import SurgeEncoder
+    with SurgeEncoder(ecfg, pack_blob(ecfg, w), 60, 400, chunk_tokens=4096) as enc:
+        got = enc.run(parts)
+    assert np.array_equal(np.concatenate([got[1000], got[1001], got[1002]]), packed)
+
+
+@pytest.mark.parametrize("enc", ["toy", "minilm"])
+def test_bf16_output_dtype(N, enc):
+    """surge_config.out_dtype = SURGE_BF16: every streamed piece carries dtype BF16 and
+    holds the RNE bf16 rounding of the float32 path's unit vectors (same kernels up to the final
+    store), so it also meets the oracle gate; the device-level path writes the same bits."""
+    ecfg = ENCODERS[enc]
+    if enc == "toy":
+        wcfg, w = WORKLOADS["toy"], make_weights(ecfg, seed=1234, init="pin")
+    else:
+        wcfg, w = scaled(WORKLOADS["minilm"], n_texts=6000, n_partitions=16, b_min=1500, b_max=7500), make_weights(ecfg, seed=1234)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=2)
+    f32, _, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+    b16, _, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max, out_dtype=N.SURGE_BF16)
+    want = torch.from_numpy(np.concatenate([f32[int(k)] for k in wl.keys])).to(torch.bfloat16).view(torch.int16)
+    got = np.concatenate([b16[int(k)] for k in wl.keys])
+    assert got.dtype == np.uint16
+    assert np.array_equal(got.view(np.int16), want.numpy())
+    E = oenc.Encoder(ecfg, w)
+    key, ids, lens = wl.partition(0)
+    rows = list(range(min(8, len(lens))))
+    g = N.bf16_to_f32(b16[key][rows]).astype(np.float64)
+    ref = np.stack([E.encode_text(t) for t in texts_of(ids, lens)[:len(rows)]])
+    cos = (g * ref).sum(1) / (np.linalg.norm(g, axis=1) * np.linalg.norm(ref, axis=1))
+    assert cos.min() >= COS_MIN and np.abs(g - ref).max() <= ABS_MAX
+    h = N.surge_create(N.make_config(ecfg, 1000, 5000, out_dtype=N.SURGE_BF16), pack_blob(ecfg, w))
+    try:
+        out = torch.zeros(len(lens), ecfg.hidden, dtype=torch.int16, device="cuda")
+        N.surge_encode_packed(h, torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(), lens, len(lens), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint16), b16[key])
+    finally:
+        N.surge_destroy(h)
+
+
+def test_release_and_reset_lifetime_rules(N):
+    """P:413 buffer lifetime: a polled view stays valid until it is released; every polled record is
+    released exactly once (a second release, or a record from before a reset, is rejected); reset is
+    refused while a polled piece is unreleased."""
+    ecfg = ENCODERS["toy"]
+    w = make_weights(ecfg, seed=7, init="pin")
+    h = N.surge_create(N.make_config(ecfg, 5, 8), pack_blob(ecfg, w))
+    try:
+        ids = np.arange(4, 4 + 12, dtype=np.int32)
+        N.surge_submit_partition(h, 1, ids, np.array([4, 4, 4], np.int32))
+        N.surge_submit_partition(h, 2, ids, np.array([6, 6], np.int32))
+        N.surge_finish(h)
+        recs = []
+        while N.surge_pending(h) > 0:
+            recs += N.surge_poll_flushed(h, 64, 50)
+        recs += N.surge_poll_flushed(h, 64, 0)
+        assert sorted(int(r.partition_id) for r in recs) == [1, 2]
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_reset(h)                                   # polled but unreleased views
+        assert ei.value.status == N.SURGE_E_STATE
+        snap = N.flushed_array(recs[0]).copy()
+        N.surge_release(h, recs[0])
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_release(h, recs[0])                        # double release
+        assert ei.value.status == N.SURGE_E_INVALID_ARG
+        N.surge_release(h, recs[1])
+        N.surge_reset(h)
+        with pytest.raises(N.SurgeError) as ei:
+            N.surge_release(h, recs[1])                        # record of the previous stream
+        assert ei.value.status == N.SURGE_E_INVALID_ARG
+        N.surge_submit_partition(h, 1, ids, np.array([4, 4, 4], np.int32))
+        N.surge_finish(h)
+        again = []
+        while N.surge_pending(h) > 0:
+            again += N.surge_poll_flushed(h, 64, 50)
+        again += N.surge_poll_flushed(h, 64, 0)
+        assert np.array_equal(N.flushed_array(again[0]), snap)
+        N.surge_release(h, again[0])
+    finally:
+        N.surge_destroy(h)
+
+
+def test_create_replicated_nccl_single_rank(N):
+    """K11 inside libsurge: surge_create_replicated opens an NCCL communicator (world of 1 on this
+    box), broadcasts the weight blob from rank 0 and builds the same encoder as surge_create: the
+    embeddings are bit-identical."""
+    ecfg = ENCODERS["minilm"]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(3)
+    lens = rng.integers(8, 21, size=500).astype(np.int32)
+    ids = rng.integers(1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    ref = _packed_encode(N, ecfg, w, lens, ids, True)
+    blob = torch.from_numpy(pack_blob(ecfg, w).view(np.uint16)).cuda()
+    h = N.surge_create_replicated(N.make_config(ecfg, 1000, 5000, weights_on_device=1), N.surge_nccl_unique_id(),
+                                  blob, n_weights=blob.numel())
+    try:
+        out = torch.zeros(len(lens), ecfg.hidden, device="cuda")
+        N.surge_encode_packed(h, torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(), lens, len(lens), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert N.surge_get_stats(h)["init_s"] > 0
+    finally:
+        N.surge_destroy(h)

@@ -219,3 +219,85 @@ def test_toy_safety_variant_hits_safety():
         A = agg.run_aggregator(wl.keys, wl.sizes, w.b_min, w.b_max)
         hits += any(sb.reason == agg.SAFETY for sb in A.flushes)
     assert hits >= 3
+
+
+# ----------------------------------------------------------------- LPT: independent pin (Graham)
+
+def _opt_makespan(loads, G):
+    """Exact minimum makespan of assigning `loads` to G identical ranks (brute force with symmetry
+    breaking: a piece may open at most one new, empty rank)."""
+    loads = sorted(loads, reverse=True)
+    best = [sum(loads)]
+    bins = [0] * G
+
+    def dfs(i, used):
+        if i == len(loads):
+            best[0] = min(best[0], max(bins))
+            return
+        for r in range(min(used + 1, G)):
+            if bins[r] + loads[i] >= best[0]:
+                continue
+            bins[r] += loads[i]
+            dfs(i + 1, max(used, r + 1))
+            bins[r] -= loads[i]
+
+    dfs(0, 0)
+    return best[0]
+
+
+def _small_instances(G, n_inst=60, seed=0):
+    """SuperBatches of <= 10 texts whose lengths all exceed U = ceil(T/(8G)), so every text is its
+    own LPT piece and the piece set is known without the oracle's cutting rule."""
+    rng = np.random.default_rng(1000 + G)
+    out = []
+    while len(out) < n_inst:
+        n = int(rng.integers(G + 1, 11))
+        lengths = rng.integers(1, 513, size=n)
+        T = int(lengths.sum())
+        if lengths.min() <= -(-T // (8 * G)):
+            continue
+        cuts = np.sort(rng.choice(np.arange(1, n), size=int(rng.integers(0, n)), replace=False))
+        sizes = np.diff(np.concatenate([[0], cuts, [n]])).tolist()
+        out.append((lengths, sizes))
+    return out
+
+
+def _greedy_makespan(tokens, G):
+    load = [0] * G
+    for t in tokens:
+        load[load.index(min(load))] += t
+    return max(load)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_lpt_graham_bound_vs_bruteforce_opt(G):
+    """Independent pin of the oracle's LPT plan (north star "token-count-balanced (LPT) split";
+    SURVEY §8(e)): Graham (1969) proves that list scheduling in LONGEST-PROCESSING-TIME order has
+    makespan <= (4/3 - 1/(3G)) * OPT.  OPT is brute-forced here on instances of <= 10 pieces; the
+    same instances scheduled in ascending order (a plausible mis-sort) break the bound on some of
+    them, so a wrong sort key in the oracle fails this test."""
+    bound = 4.0 / 3.0 - 1.0 / (3.0 * G)
+    spt_violations = 0
+    for lengths, sizes in _small_instances(G):
+        pieces, per_rank = agg.lpt_plan(lengths, sizes, G)
+        assert len(pieces) == len(lengths)                       # every text its own piece
+        loads = [sum(p.tokens for p in per_rank[r]) for r in range(G)]
+        opt = _opt_makespan([int(x) for x in lengths], G)
+        assert max(loads) <= bound * opt + 1e-9, (lengths, sizes, loads, opt)
+        assert max(loads) >= opt
+        if len(lengths) <= G:                                    # one piece per rank is optimal
+            assert max(loads) == opt
+        spt_violations += _greedy_makespan(sorted(int(x) for x in lengths), G) > bound * opt + 1e-9
+    assert spt_violations > 0, "instances too easy: an ascending-order schedule would also pass"
+
+
+def test_lpt_textbook_tight_instance():
+    """Graham's tight family: 2G+1 jobs G, ..., 2G-1 (each twice) and one job G, on G machines.
+    LPT makespan = 4G - 1, OPT = 3G: ratio 4/3 - 1/(3G) exactly.  Pieces = texts of those lengths."""
+    for G in (2, 3, 4):
+        jobs = [L for L in range(2 * G - 1, G - 1, -1) for _ in range(2)] + [G]
+        lengths = np.array(jobs) * 64                            # every text > U = ceil(T/(8G))
+        pieces, per_rank = agg.lpt_plan(lengths, [1] * len(jobs), G)
+        loads = [sum(p.tokens for p in per_rank[r]) for r in range(G)]
+        assert max(loads) == (4 * G - 1) * 64
+        assert _opt_makespan(list(lengths), G) == 3 * G * 64

@@ -1,24 +1,33 @@
 // epi_ln.cuh -- the residual + LayerNorm GEMM epilogue (K6 / K8; reading R9:
-// post-LN, biased variance, fp32 statistics), shared by the LN GEMM (gemm_tc.cu) and the fused tail
-// kernel (mlp_tc.cu) so both round identically.
+// post-LN, biased variance, fp32 statistics), shared by the LN GEMM (gemm_tc.cu) and the fused MLP
+// (mlp_tc.cu) so both round identically.
 //
-// Preloaded accumulator: before a tile's first MMA the epilogue writes bias + residual (fp32) into
-// the TMEM accumulator and every MMA of the tile accumulates onto it, so the accumulator ends as
-// v = bias + residual + A B^T.  The LN then only reads v -- no bias / residual traffic on its
-// critical path, and the residual source (an smem tile or HBM rows) is free as soon as the preload
-// is written, long before the LN runs.
-//
-// The accumulator row (BN fp32 columns in TMEM, lane = row) is split over NP warps of the same lane
-// quadrant q, each owning columns [c_lo, c_lo + HALF), hh = which part.
-//   pass 1: shifted partial sums of v (TMEM loads one step ahead);
-//   combine the parts (Chan's parallel variance) through smem (stats: [NP parts][128 rows]);
-//   pass 2: y = (v - mean) rstd gamma + beta -> bf16, handed to store(p, column) 32 columns at a time;
-//           optionally the columns just read are rewritten with the NEXT tile's preload (pre).
+// The accumulator row (BN fp32 columns in TMEM, lane = row) is split over two warps of the same
+// lane quadrant q, each owning columns [c_lo, c_lo + HALF), hh = which half.
+//   pass 1: v = acc + bias + residual, written back to TMEM in place, shifted partial sums (the
+//           residual slice and TMEM load of step k+1 are in flight while step k is computed; the
+//           first residual slice is fetched before the accumulator is ready);
+//   combine the halves (Chan's parallel variance) through smem (stats: [2 halves][128 rows]);
+//   pass 2: y = (v - mean) rstd gamma + beta -> bf16, handed to store(p, column) 32 columns at a time.
 #pragma once
 
 #include "common.cuh"
 
 namespace surge {
+
+// Residual source: load(k, rr) fills rr[16] = the 32 bf16 residual values of step k (columns
+// c_lo + 32 k ..), packed in pairs.  It is called one step ahead of use.
+struct ResidualGlobal {
+  const uint16_t* rrow;   // this row, column c_lo
+  __device__ __forceinline__ void operator()(int k, uint32_t (&rr)[16]) const {
+    const uint4* p = reinterpret_cast<const uint4*>(rrow + 32 * k);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = p[i];
+      rr[4 * i] = v.x; rr[4 * i + 1] = v.y; rr[4 * i + 2] = v.z; rr[4 * i + 3] = v.w;
+    }
+  }
+};
 
 #ifdef LN_TRACE
 __device__ long long g_ln_trace[32][4];
@@ -48,94 +57,27 @@ __device__ __forceinline__ void store_rows_32x32(uint8_t* stg, const uint32_t (&
   }
 }
 
-// ------------------------------------------------------------------------------ accumulator preloads
-// w[0..31] = fp32 bias[c + i] + residual[c + i] for the 32 columns from c.
-__device__ __forceinline__ void preload_values(const float* s_bias, int c, const uint32_t (&rs)[16], uint32_t (&w)[32]) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const float2 bb = *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
-    const f32x2 v = fadd2(f2(bb.x, bb.y), f2(bf16lo(rs[i]), bf16hi(rs[i])));
-    w[2 * i] = __float_as_uint(f2lo(v));
-    w[2 * i + 1] = __float_as_uint(f2hi(v));
-  }
-}
-
-// Residual row in global memory (this row, column c_lo): rs = its 32 bf16 values of step k, packed.
-__device__ __forceinline__ void load_row32(const uint16_t* row_c_lo, int k, uint32_t (&rs)[16]) {
-  const uint4* p = reinterpret_cast<const uint4*>(row_c_lo + 32 * k);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint4 v = p[i];
-    rs[4 * i] = v.x; rs[4 * i + 1] = v.y; rs[4 * i + 2] = v.z; rs[4 * i + 3] = v.w;
-  }
-}
-
-// No preload in pass 2 (the accumulator is not reused, or the caller preloads it otherwise).
-struct PreNone {
-  static constexpr bool kActive = false;
-  __device__ __forceinline__ bool on() const { return false; }
-  __device__ __forceinline__ void load(int, uint32_t (&)[16]) const {}
-  __device__ __forceinline__ void make(int, const uint32_t (&)[16], const uint32_t (&)[16], uint32_t (&)[32]) const {}
+// NP warps share a lane quadrant, each owning HALF = BN / NP columns (part hh).  PIPE: TMEM loads and
+// residual loads one step ahead (2 register buffers); !PIPE: one buffer (for register-limited kernels).
+struct LnNoOp {
+  __device__ __forceinline__ void operator()() const {}
 };
 
-// Preload of the next tile's row: bias + residual read from global (row pointer at column c_lo;
-// nullptr = no next tile).
-struct PreGlobal {
-  static constexpr bool kActive = true;
-  const uint16_t* row;
-  const float* s_bias;
-  __device__ __forceinline__ bool on() const { return row != nullptr; }
-  __device__ __forceinline__ void load(int k, uint32_t (&rs)[16]) const { load_row32(row, k, rs); }
-  __device__ __forceinline__ void make(int c, const uint32_t (&rs)[16], const uint32_t (&)[16], uint32_t (&w)[32]) const {
-    preload_values(s_bias, c, rs, w);
-  }
-};
-
-// Preload from this LN's own output: the next GEMM on the same rows adds its bias to the bf16 value
-// just produced (the fused tail: Y <- b2 + X1 while LN_a writes X1).
-struct PreFromOutput {
-  static constexpr bool kActive = true;
-  const float* s_bias;
-  __device__ __forceinline__ bool on() const { return true; }
-  __device__ __forceinline__ void load(int, uint32_t (&)[16]) const {}
-  __device__ __forceinline__ void make(int c, const uint32_t (&)[16], const uint32_t (&p)[16], uint32_t (&w)[32]) const {
-    preload_values(s_bias, c, p, w);
-  }
-};
-
-// Preload of a whole accumulator row part (columns [c_lo, c_lo + HALF)) from a global residual row:
-// the first tile of a CTA, before any MMA.
-template <int HALF>
-__device__ __forceinline__ void ln_preload(uint32_t taddr, int c_lo, const uint16_t* row_c_lo, const float* s_bias) {
-  constexpr int NSTEP = HALF / 32;
-  uint32_t rs[2][16];
-  load_row32(row_c_lo, 0, rs[0]);
-#pragma unroll
-  for (int k = 0; k < NSTEP; ++k) {
-    if (k + 1 < NSTEP) load_row32(row_c_lo, k + 1, rs[(k + 1) & 1]);
-    uint32_t w[32];
-    preload_values(s_bias, c_lo + 32 * k, rs[k & 1], w);
-    tmem_st32(taddr + c_lo + 32 * k, w);
-  }
-  tmem_st_wait();
-}
-
-// NP warps share a lane quadrant, each owning HALF = BN / NP columns (part hh).  PIPE: TMEM loads one
-// step ahead (2 register buffers); !PIPE: one buffer (for register-limited kernels).
-template <int BN, int HALF, bool PIPE = true, typename Ready, typename Store, typename Pre = PreNone,
+// pass1_done() runs once the residual has been read for the last time (after pass 1).
+template <int BN, int HALF, bool PIPE = true, typename Res, typename Ready, typename Store, typename P1 = LnNoOp,
           int NP = BN / HALF>
-__device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const float* s_gamma, const float* s_beta,
-                                            float4* stats, int q, int hh, int lane, float eps, Ready&& wait_ready,
-                                            Store&& store, const Pre& pre = Pre{}) {
+__device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
+                                            const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,
+                                            int lane, float eps, Ready&& wait_ready, Store&& store,
+                                            P1&& pass1_done = P1{}) {
 #ifdef LN_TRACE
   long long _lt = 0;
 #endif
   constexpr int NSTEP = HALF / 32;
   constexpr int NB = PIPE ? 2 : 1;
-  const bool pre_on = Pre::kActive && pre.on();
-  uint32_t rn[2][16];                          // next tile's residual slices (PreGlobal), one step ahead
-  if (pre_on) pre.load(0, rn[0]);              // in flight across pass 1
   uint32_t r[NB][32];
+  uint32_t rs[NB][16];
+  load_res(0, rs[0]);
   wait_ready();
   LNT(0);
   tmem_ld32(taddr + c_lo, r[0]);
@@ -144,18 +86,35 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const floa
 #pragma unroll
   for (int k = 0; k < NSTEP; ++k) {
     const int cur = PIPE ? (k & 1) : 0;
-    if (!PIPE && k > 0) tmem_ld32(taddr + c_lo + 32 * k, r[0]);
+    const int c = c_lo + 32 * k;
+    if (!PIPE && k > 0) {
+      tmem_ld32(taddr + c, r[0]);
+      load_res(k, rs[0]);
+    }
     tmem_ld_wait_regs(r[cur]);
-    if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + c_lo + 32 * (k + 1), r[cur ^ 1]);
-    if (k == 0) shift = __uint_as_float(r[cur][0]);
-    const f32x2 sh = f2(-shift, -shift);
+    if (PIPE && k + 1 < NSTEP) {
+      tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+      load_res(k + 1, rs[cur ^ 1]);
+    }
+    const uint32_t (&rr)[16] = rs[cur];
+    if (k == 0) shift = __uint_as_float(r[cur][0]) + s_bias[c] + bf16lo(rr[0]);
+    uint32_t w[32];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const f32x2 dv = fadd2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])), sh);
+      const float2 bb = *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
+      const f32x2 v = fadd2(fadd2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])),
+                                  f2(bb.x, bb.y)),
+                            f2(bf16lo(rr[i]), bf16hi(rr[i])));
+      const f32x2 dv = fadd2(v, f2(-shift, -shift));
       s1 = fadd2(s1, dv);
       s2 = ffma2(dv, dv, s2);
+      w[2 * i] = __float_as_uint(f2lo(v));
+      w[2 * i + 1] = __float_as_uint(f2hi(v));
     }
+    tmem_st32(taddr + c, w);
   }
+  tmem_st_wait();
+  pass1_done();
   LNT(1);
   const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
   stats[hh * 128 + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);
@@ -200,7 +159,6 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const floa
     if (!PIPE && k > 0) tmem_ld32(taddr + c, r[0]);
     tmem_ld_wait_regs(r[cur]);
     if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
-    if (pre_on && k + 1 < NSTEP) pre.load(k + 1, rn[(k + 1) & 1]);
     uint32_t p[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -211,13 +169,7 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const floa
       p[i] = pack_bf16x2(f2lo(y), f2hi(y));
     }
     store(p, c);
-    if (pre_on) {                              // these columns were read (wait::ld above): rewrite them
-      uint32_t w[32];
-      pre.make(c, rn[k & 1], p, w);
-      tmem_st32(taddr + c, w);
-    }
   }
-  if (pre_on) tmem_st_wait();
   LNT(3);
 }
 

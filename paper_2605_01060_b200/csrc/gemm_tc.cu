@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
             mbar_wait(&empty[s], ph ^ 1);
             if (b == 0) {
               if constexpr (EPI == EPI_BIAS_LN) {
-                // warm L2 with the next tile's residual rows (read by this tile's LN to preload them)
-                if (kb < N / 64 && t + sc.dt < sc.tend) tma_prefetch_2d(&tmR, kb * 64, sc.m0(t + sc.dt));
+                // warm L2 with this tile's residual rows (read by the LN epilogue)
+                if (kb < N / 64) tma_prefetch_2d(&tmR, kb * 64, m0);
               }
               if constexpr (PAIR) {               // both halves complete on the leader's barrier
                 if (leader) mbar_arrive_expect_tx(&full[s], 2 * A_STAGE_BYTES);
@@ -322,9 +322,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
       mbar_wait(&tempty[acc], aph ^ 1);
       mt_acc[8] += clock64() - _e0;
 #else
-      // epilogue drained this accumulator buffer (EPI_BIAS_LN: and preloaded it with bias + residual
-      // of this tile -- its first completion is the initial preload, so the parity is not inverted)
-      mbar_wait(&tempty[acc], EPI == EPI_BIAS_LN ? aph : aph ^ 1);
+      mbar_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
 #endif
 #ifndef ATT_GATE
 #define ATT_GATE 2
@@ -363,9 +361,8 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
 #pragma unroll
             for (int j = 0; j < T::N_MMA; ++j) {
               const uint64_t bd = b_desc + uint64_t((j * T::B_BOX * 128 + k * 32) >> 4);
-              constexpr bool PRE = EPI == EPI_BIAS_LN;   // accumulate onto the preloaded bias + residual
-              if constexpr (PAIR) tc_mma_bf16_pair(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), bd, idesc, PRE || (kb | k) != 0);
-              else tc_mma_bf16(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), bd, idesc, PRE || (kb | k) != 0);
+              if constexpr (PAIR) tc_mma_bf16_pair(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), bd, idesc, (kb | k) != 0);
+              else tc_mma_bf16(d0 + j * T::MMA_N, a_desc + uint64_t(k * 2), bd, idesc, (kb | k) != 0);
             }
           }
           if constexpr (PAIR) tc_commit_pair_mc(&empty[s], 0x3);   // frees the stage in both CTAs
@@ -399,20 +396,6 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
         s_beta[i] = beta[i];
       }
       named_bar_sync(5, T::EPI_WARPS * 32);
-      // preload bias + residual into the accumulator buffers of this CTA's first ACC tiles
-      const int q0 = warp & 3, c0 = ((warp - 4) >> 2) * T::HALF;
-      for (int j = 0; j < ACC; ++j) {
-        const int t = sc.t0 + j * sc.dt;
-        if (t >= sc.tend) break;
-        const int row = min(sc.m0(t) + q0 * 32 + lane, M - 1);
-        ln_preload<T::HALF>(tmem_base + j * BN + (uint32_t(q0 * 32) << 16), c0, res + size_t(row) * N + c0, s_bias);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[j]), 0));
-          else mbar_arrive(&tempty[j]);
-        }
-      }
     }
     if constexpr (T::BIAS_SMEM) {
       for (int i = threadIdx.x - 128; i < N; i += T::EPI_WARPS * 32) s_bias_all[i] = bias[i];
@@ -644,22 +627,17 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
           }
         }
       } else {
-        // LayerNorm over the full row (BN == N), two warps per row (column halves): epi_ln.cuh.  The
-        // accumulator holds bias + residual + A B^T; pass 2 preloads it for the tile ACC tiles ahead.
-        (void)ok;
-        const int tn = t + ACC * sc.dt;
-        const PreGlobal pre{tn < sc.tend ? res + size_t(min(sc.m0(tn) + q * 32 + lane, M - 1)) * N + c_lo : nullptr,
-                            s_bias};
+        // LayerNorm over the full row (BN == N), two warps per row (column halves): epi_ln.cuh
+        const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + c_lo};
         uint8_t* stg = sStg + (warp - 4) * T::STG_BUFS * 2048;
-        ln_epilogue<BN, T::HALF>(taddr, c_lo, s_gamma, s_beta, stats + (it & 1) * 2 * BM, q, hh, lane, eps,
-                                 [&] {
+        ln_epilogue<BN, T::HALF>(taddr, c_lo, rg, s_bias, s_gamma, s_beta, stats + (it & 1) * 2 * BM, q, hh, lane,
+                                 eps, [&] {
                                    mbar_wait(&tfull[acc], aph);
                                    tc_fence_after();
                                  },
                                  [&](const uint32_t (&p)[16], int col) {
                                    store_rows_32x32(stg, p, lane, C, m0 + q * 32, M, N, col);
-                                 },
-                                 pre);
+                                 });
       }
       if constexpr (!T::ATT) {
         tc_fence_before();

@@ -93,8 +93,7 @@ struct MlpArgs {
   int D, F;
   const float *b1, *b2, *gamma, *beta;       // FFN biases, LN_o
   const float *bo, *gamma1, *beta1;          // K6: out-proj bias, LN_a (when tmWo is set)
-  const uint16_t* x;         // residual rows the first GEMM's accumulator is preloaded with: X (K6
-                             // residual, when tmWo is set), else X1 (the A rows, K8 residual)
+  const uint16_t* x;         // X (K6 residual rows; when tmWo is set)
   uint16_t* out;             // X [M x D] output (in place over x when tmWo is set)
   float eps;
 };

@@ -88,6 +88,23 @@ struct MlpCfg {
 #define MW(bar, par, slot) mbar_wait(bar, par)
 #endif
 
+// LN residual from the resident A tile (128-byte-swizzled K-major: k-block c / 64, row r at r * 128 B,
+// 16-byte chunk j at (j ^ (r & 7)) * 16).
+struct ResidualSmemA {
+  const uint8_t* sA;
+  int row, c_lo;
+  __device__ __forceinline__ void operator()(int k, uint32_t (&rr)[16]) const {
+    const int c = c_lo + 32 * k;
+    const uint8_t* base = sA + (c >> 6) * (MBM * 128) + row * 128;
+    const int j0 = (c & 63) >> 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + (((j0 + i) ^ (row & 7)) << 4));
+      rr[4 * i] = v.x; rr[4 * i + 1] = v.y; rr[4 * i + 2] = v.z; rr[4 * i + 3] = v.w;
+    }
+  }
+};
+
 // Remote arrive with the default semantics (.release at .cta scope): after fence.proxy.async this
 // publishes the thread's generic-proxy shared-memory writes to the leader's MMA, as CUTLASS's 2-SM
 // pipelines do; .release.cluster would add a MEMBAR.ALL.GPU (measured ~1.5K cycles per chunk).
@@ -123,15 +140,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* hs_full = h_empty + 1;                           // leader, 2 x EPI_WARPS arrivals
   uint64_t* hs_empty = hs_full + 1;                          // both
   uint64_t* y_full = hs_empty + 1;                           // both
-  uint64_t* y_empty = y_full + 1;                            // leader, 2 x EPI_WARPS: Y drained + preloaded
-  uint64_t* y0_full = y_empty + 1;                           // both (OP): G0 retired
-  uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A, Y preloaded
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x1_ready + 1);
+  uint64_t* y_empty = y_full + 1;                            // leader, 2 x EPI_WARPS arrivals
+  uint64_t* a_free = y_empty + 1;                            // local: LN read its residual from A
+  uint64_t* y0_full = a_free + 1;                            // both (OP): G0 retired
+  uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A
+  uint64_t* xres_full = x1_ready + 1;                         // local (OP): X residual rows landed in A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xres_full + 1);
   uint8_t* sA = smem + T::HEAD;                              // [KB1][128 x 128 B]
   uint8_t* sHs = sA + T::A_BYTES;                            // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
-  float* s_pb = reinterpret_cast<float*>(stats + NP * MBM);  // LN only: bias of the accumulator it preloads
-  float* s_gamma = s_pb + D;
+  float* s_b2 = reinterpret_cast<float*>(stats + NP * MBM);  // LN only
+  float* s_gamma = s_b2 + D;
   float* s_beta = s_gamma + D;
   uint8_t* sW = sHs + T::SCRATCH;                            // [RING][STAGE]
 
@@ -158,8 +177,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(hs_empty, 1);
     mbar_init(y_full, 1);
     mbar_init(y_empty, 2 * EPI_WARPS);
+    mbar_init(a_free, EPI_WARPS);
     mbar_init(y0_full, 1);
     mbar_init(x1_ready, 2 * EPI_WARPS);
+    mbar_init(xres_full, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -225,7 +246,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the leader's a_full before producer 0's arrive.expect_tx: the transiently negative tx-count
       // cannot complete the phase while that arrival is pending.
       auto load_a = [&](int u, int m0) {
-        mbar_wait(a_empty, (ui & 1) ^ 1);       // MMAs done with the previous unit's A (the LNs never read it)
+        mbar_wait(a_empty, (ui & 1) ^ 1);       // MMAs done with the previous unit's A
+        mbar_wait(a_free, (ui & 1) ^ 1);        // its LN has read the residual rows
         if (leader && p == 0) mbar_arrive_expect_tx(a_full, 2u * T::A_BYTES);
         for (int kb = (OP && MLP_A_SPLIT) ? p : 0; kb < KB1; kb += (OP && MLP_A_SPLIT) ? 3 : 1)
           tma_load_2d_pair(sA + kb * MBM * 128, &tmX1, afull_c, kb * 64, m0, l2_policy_evict_first());
@@ -233,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           // warm L2 with the next unit's rows: its A load waits for this unit's LN (residual from A)
           if (MLP_PREFETCH && u + units < n_units)
             for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmX1, kb * 64, m0 + units * 2 * MBM);
-          if constexpr (OP)   // X rows of this unit: the previous unit's final LN preloads bo + X from them
+          if constexpr (OP)                              // LN0 residual rows (X), read from L2
             for (int kb = 0; kb < KB1; ++kb) tma_prefetch_2d(&tmR, kb * 64, m0);
         }
       };
@@ -246,7 +268,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int WO_EARLY = (OP && MLP_A_SPLIT) ? (RING < KB1 ? RING : KB1) : 0;
         if constexpr (OP) ring_wo(0, WO_EARLY);
         if ((OP && MLP_A_SPLIT) || p == 0) load_a(u, m0);   // !OP: producer 0 alone (unchanged)
-        if constexpr (OP) ring_wo(WO_EARLY, KB1);
+        if constexpr (OP) {
+          ring_wo(WO_EARLY, KB1);
+          if (p == 0) {
+            // once G0 has consumed O, the A tile takes this unit's X rows: the LN0 residual, read from
+            // smem instead of from L2 one step ahead (its latency bounded LN0's first pass)
+            mbar_wait(y0_full, ui & 1);
+            mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
+            for (int kb = 0; kb < KB1; ++kb)
+              tma_load_2d(sA + kb * MBM * 128, &tmR, xres_full, kb * 64, m0);
+          }
+        }
         for (int c = 0; c < NCH; ++c) {
           ring_w1(c);
           if (c > 0) ring_w2(c - 1);
@@ -272,7 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int ui = 0;
     auto g2 = [&](int c, int uiu) {
       if (!OP && c == 0) {
-        MW(y_empty, uiu & 1, 0);                     // Y drained by the previous LN and preloaded b2 + X1
+        MW(y_empty, (uiu & 1) ^ 1, 0);               // LN of the previous unit drained Y
         tc_fence_after();
       }
       MW(hs_full, gc & 1, 1);                        // both CTAs' Hs(c) written
@@ -289,7 +321,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int j = 0; j < T::N2_MMAS; ++j)
               tc_mma_bf16_pair(tmem_base + j * T::N2, ad + uint64_t(k * 2),
-                               bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, 1u);   // onto b2 + X1
+                               bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, (c | kb | k) != 0);
           tc_commit_pair_mc(&empty[s], 0x3);
         }
         __syncwarp();
@@ -305,8 +337,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       MW(a_full, ui & 1, 3);
       tc_fence_after();
       if constexpr (OP) {
-        // G0: Y = bo + X + O Wo^T (the previous LN drained Y and preloaded bo + X of this unit)
-        MW(y_empty, ui & 1, 0);
+        // G0: Y = O Wo^T (the previous unit's final LN has drained Y)
+        MW(y_empty, (ui & 1) ^ 1, 0);
         tc_fence_after();
         for (int kb = 0; kb < KB1; ++kb, ++sc) {
           const int s = int(sc % RING);
@@ -320,7 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int j = 0; j < T::N2_MMAS; ++j)
                 tc_mma_bf16_pair(tmem_base + j * T::N2, ad + uint64_t(k * 2),
-                                 bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, 1u);   // onto bo + X
+                                 bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, (kb | k) != 0);
             tc_commit_pair_mc(&empty[s], 0x3);
           }
           __syncwarp();
@@ -373,33 +405,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;                    // TMEM lane quadrant
     const int hh = (warp - 4) >> 2;            // column part (0 .. NP-1)
     const int row_l = q * 32 + lane;           // row within the CTA tile
-    const int c_lo = hh * (D / NP);            // this warp's LN columns
     const uint32_t hs_full_c = mapa_shared(smem_u32(hs_full), 0);
     const uint32_t h_empty_c = mapa_shared(smem_u32(h_empty), 0);
     const uint32_t y_empty_c = mapa_shared(smem_u32(y_empty), 0);
     const uint32_t t_row = tmem_base + (uint32_t(q * 32) << 16);
-    // Y preloads (epi_ln.cuh): OP: bo + X before G0 (the residual of LN_a), then b2 + X1 before G2;
-    // !OP: b2 + X1 before G2.  `first_bias` / `first_rows` name the one a unit starts with.
-    const float* first_bias = OP ? bo : b2;
-    const uint16_t* first_rows = xres;         // OP: X; !OP: X1 (the A rows)
-    // LN constants (in Hs scratch, idle during either LN): s_pb = bias of the accumulator this LN
-    // preloads, s_gamma / s_beta = this LN's affine parameters
-    auto load_consts = [&](const float* pb, const float* g, const float* bt, auto&& before_store) {
-      constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
-      float cv[PER];
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
-        cv[i] = k < D ? __ldg(pb + k) : k < 2 * D ? __ldg(g + k - D) : k < 3 * D ? __ldg(bt + k - 2 * D) : 0.f;
-      }
-      before_store();
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
-        if (k < 3 * D) s_pb[k] = cv[i];
-      }
-      asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
-    };
     uint32_t hc = 0;
     int ui = 0;
 #ifdef MLP_TRACE
@@ -409,23 +418,30 @@ __global__ void __launch_bounds__(THREADS, 1)
 #define ETR(i) do {} while (0)
 #endif
     const uint32_t x1_ready_c = mapa_shared(smem_u32(x1_ready), 0);
-    if (unit0 < n_units) {                     // preload Y for this CTA's first unit
-      load_consts(first_bias, gamma, beta, [] {});
-      const int row = min(unit0 * 2 * MBM + rank * MBM + row_l, M - 1);
-      ln_preload<D / NP>(t_row, c_lo, first_rows + size_t(row) * D + c_lo, s_pb);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(y_empty_c);
-      asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");   // s_pb read by every warp
-    }
     for (int u = unit0; u < n_units; u += units, ++ui) {
       const int m0 = u * 2 * MBM + rank * MBM;
-      const int un = u + units;                // this CTA's next unit (its Y preload comes from this unit's final LN)
       if constexpr (OP) {
-        // ---- LN0 epilogue (K6): X1 = LN_a(Y) with Y = bo + X + O Wo^T -> bf16 into the A tile
-        // (swizzled K-major, the G1 operand); the columns it read are rewritten with b2 + X1 (G2's init)
-        load_consts(b2, gamma1, beta1, [] {});   // Hs idle: the previous unit's LN is done, chunk 0 not yet
-        ln_epilogue<D, D / NP, (NP <= 2)>(t_row, c_lo, s_gamma, s_beta, stats, q, hh, lane, eps,
+        // ---- LN0 epilogue (K6): X1 = LN_a(Y + bo + X) -> bf16 into the A tile (swizzled K-major)
+        {
+          constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
+          float cv[PER];
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+            cv[i] = k < D ? __ldg(bo + k) : k < 2 * D ? __ldg(gamma1 + k - D) : k < 3 * D ? __ldg(beta1 + k - 2 * D) : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {     // Hs idle: the previous unit's LN is done, chunk 0 not yet
+            const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+            if (k < 3 * D) s_b2[k] = cv[i];
+          }
+          asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+        }
+        const int row = m0 + row_l;
+        (void)row;
+        const ResidualSmemA rg{sA, row_l, hh * (D / NP)};
+        mbar_wait(xres_full, ui & 1);          // X rows in the A tile (G0 is done with O)
+        ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
                                 tc_fence_after();
@@ -437,9 +453,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 for (int i = 0; i < 4; ++i)
                                   *reinterpret_cast<uint4*>(base + (((j0 + i) ^ (row_l & 7)) << 4)) =
                                       make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
-                              },
-                              PreFromOutput{s_pb});
-        tc_fence_before();                     // Y reads / preload writes done before G2(0) accumulates
+                              });
+        tc_fence_before();                     // Y reads done before G2(0) may accumulate into Y
         fence_proxy_async_smem();              // X1 (generic writes) -> visible to the MMA
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_release(x1_ready_c);
@@ -492,18 +507,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive_cluster_release(hs_full_c);
         ETR(6);
       }
-      // ---- final LN: X2 = LN_o(Y), Y = b2 + X1 + H W2^T; output staged per warp in Hs (free after
-      // G2(last)); the columns it read are rewritten with the next unit's preload
-      ETR(0);
-      load_consts(first_bias, gamma, beta, [&] {
+      // ---- LN epilogue: X2 = LN(Y + b2 + X1); output staged per warp in Hs (free after G2(last))
+      {
+        constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
+        float cv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {       // loads in flight while G2(last) finishes
+          const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+          cv[i] = k < D ? __ldg(b2 + k) : k < 2 * D ? __ldg(gamma + k - D) : k < 3 * D ? __ldg(beta + k - 2 * D) : 0.f;
+        }
+        ETR(0);
         mbar_wait(y_full, ui & 1);            // Hs no longer read by the MMA
         ETR(7);
-      });
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
+          if (k < 3 * D) s_b2[k] = cv[i];
+        }
+        asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+      }
+      // residual X1 = this unit's A tile, still resident (the next unit's A load waits for a_free)
+      const ResidualSmemA ra{sA, row_l, hh * (D / NP)};
       uint8_t* stg0 = sHs + (warp - 4) * (MLP_STG * 2048);
-      const PreGlobal pre{un < n_units ? first_rows + size_t(min(un * 2 * MBM + rank * MBM + row_l, M - 1)) * D + c_lo
-                                       : nullptr,
-                          s_pb};
-      ln_epilogue<D, D / NP, (NP <= 2)>(t_row, c_lo, s_gamma, s_beta, stats, q, hh, lane, eps,
+      ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();
@@ -511,7 +537,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                             [&](const uint32_t (&p)[16], int col) {
                               store_rows_32x32(stg0, p, lane, out, m0 + q * 32, M, D, col);
                             },
-                            pre);
+                            [&] {                // residual read for the last time: the A tile may take
+                              __syncwarp();      // the next unit's rows while pass 2 runs
+                              if (lane == 0) mbar_arrive(a_free);
+                            });
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(y_empty_c);

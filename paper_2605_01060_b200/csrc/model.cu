@@ -396,7 +396,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     if (mlp_fused_ && mlp_fused_supported(d, f)) {
       // K7 + K8 fused: X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1), H stays on chip
       MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, nullptr, nullptr, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
-                nullptr, nullptr, nullptr, ws.X1, ws.X, s_.eps};
+                nullptr, nullptr, nullptr, nullptr, ws.X, s_.eps};
       if (P) prof->begin(st, &ev);
       SURGE_TRY(launch_mlp(a, st));
       if (P) prof->end(KK_MLP, st, ev, 4 * M * F * D, 2 * (2 * F * D + 2 * M * D));

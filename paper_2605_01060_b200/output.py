@@ -6,9 +6,13 @@
   2^a s backoff (scaled by `backoff_s` for tests), non-blocking submit;
 * the buffer lifetime rule: the polled buffer must outlive every upload that references it --
   the upload closure owns the piece and calls `surge_release` when the write is done;
-* idempotent resume: the output path is deterministic (`<run_id>/<key>/<row_begin>.arrow`),
-  a partition is complete when its `_SUCCESS.<rows>` marker exists, and `completed()` is the O(P)
-  existence scan a restarted run uses to skip partitions;
+* idempotent resume (P:419-421): the output path is deterministic (`<run_id>/<key>/<row_begin>.arrow`);
+  every durable piece gets a marker `_PIECE.<row_begin>.<n_rows>.<partition_rows>` written after its
+  data, so completion is decided per piece, by whichever process (rank) uploaded it: a partition is
+  complete when its markers tile [0, partition_rows) exactly.  `completed()` is the O(P) scan a
+  restarted run uses to skip partitions; `prepare_resume()` also deletes the files of incomplete
+  partitions (their piece boundaries may differ in the re-run), and `read_partition()` reads only
+  marked pieces;
 * the I/O overlap ratio rho (`eq:overlap`) per SuperBatch.
 
 Tokenisation, real object stores and their latency profiles stay out of scope (SURVEY.md §8 OUT).
@@ -68,6 +72,12 @@ class LocalStorage:
         with open(os.path.join(self.root, path), "rb") as f:
             return f.read()
 
+    def delete(self, path: str) -> None:
+        try:
+            os.remove(os.path.join(self.root, path))
+        except FileNotFoundError:
+            pass
+
     def exists(self, path: str) -> bool:
         return os.path.exists(os.path.join(self.root, path))
 
@@ -82,17 +92,59 @@ def piece_path(run_id: str, key: int, row_begin: int) -> str:
     return f"{run_id}/{key:020d}/{row_begin:012d}.arrow"
 
 
-def success_path(run_id: str, key: int, rows: int) -> str:
-    return f"{run_id}/{key:020d}/_SUCCESS.{rows}"
+def marker_path(run_id: str, key: int, row_begin: int, n_rows: int, partition_rows: int) -> str:
+    return f"{run_id}/{key:020d}/_PIECE.{row_begin:012d}.{n_rows}.{partition_rows}"
+
+
+def _pieces(storage, run_id: str, key_dir: str):
+    """Marked pieces of one partition directory: sorted [(row_begin, n_rows, partition_rows)]."""
+    out = []
+    for f in storage.list(f"{run_id}/{key_dir}"):
+        if f.startswith("_PIECE."):
+            _, b, n, rows = f.split(".")
+            out.append((int(b), int(n), int(rows)))
+    return sorted(out)
+
+
+def _covers(pieces) -> bool:
+    """The marked pieces tile [0, partition_rows) exactly (in whatever process they were written)."""
+    if not pieces:
+        return False
+    rows = pieces[0][2]
+    at = 0
+    for b, n, r in pieces:
+        if r != rows or b != at:
+            return False
+        at += n
+    return at == rows
 
 
 def completed(storage, run_id: str) -> set:
-    """Resume scan: keys whose every row has been written (success marker present)."""
+    """Resume scan: keys whose every row is durable, from the per-piece markers of all ranks."""
+    return {int(name) for name in storage.list(run_id) if _covers(_pieces(storage, run_id, name))}
+
+
+def prepare_resume(storage, run_id: str) -> set:
+    """Before a restarted run (once, on one rank): the complete partitions (to skip), after deleting the
+    files of every incomplete one -- the re-run may cut it into different pieces, and a stale piece
+    must not survive next to the new ones."""
     done = set()
     for name in storage.list(run_id):
-        if any(f.startswith("_SUCCESS.") for f in storage.list(f"{run_id}/{name}")):
+        if _covers(_pieces(storage, run_id, name)):
             done.add(int(name))
+        else:
+            for f in storage.list(f"{run_id}/{name}"):
+                storage.delete(f"{run_id}/{name}/{f}")
     return done
+
+
+def read_partition(storage, run_id: str, key: int) -> np.ndarray:
+    """E_k of a complete partition: its marked pieces in row order (unmarked files are ignored)."""
+    pcs = _pieces(storage, run_id, f"{key:020d}")
+    if not _covers(pcs):
+        raise KeyError(f"partition {key} is not complete")
+    parts = [deserialize(storage.read(piece_path(run_id, key, b))) for b, n, _ in pcs if n > 0]
+    return np.concatenate(parts) if parts else np.zeros((0, 0), np.float32)
 
 
 class AsyncUploader:
@@ -109,7 +161,6 @@ class AsyncUploader:
         self.pool = ThreadPoolExecutor(max_workers=workers)
         self.pending: dict[str, Future] = {}
         self.lock = threading.Lock()
-        self.rows_done: dict[int, int] = {}        # key -> rows written
         self.t_ser = self.t_upl = 0.0
         self.failures: list = []
 
@@ -147,13 +198,10 @@ class AsyncUploader:
                 self.t_upl += t2 - t1
             if err is not None:
                 return False
-            with self.lock:
-                n = self.rows_done.get(key, 0) + rows.shape[0]
-                self.rows_done[key] = n
-                finished = n == partition_rows
-            if finished:                       # all pieces of the partition are durable
-                return self._write_retry(success_path(self.run_id, key, partition_rows), b"") is None
-            return True
+            # the piece is durable: its marker makes it count, whichever rank wrote the other pieces
+            row_begin = int(path.rsplit("/", 1)[1].split(".")[0])
+            return self._write_retry(marker_path(self.run_id, key, row_begin, rows.shape[0], partition_rows),
+                                     b"") is None
         finally:
             if self.release is not None and piece is not None:
                 self.release(piece)

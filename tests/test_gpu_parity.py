@@ -357,7 +357,7 @@ def test_output_side_upload_and_resume(N, tmp_path):
     for attempt, storage in enumerate((Dying(str(tmp_path), 12), O.LocalStorage(str(tmp_path)))):
         h = N.surge_create(N.make_config(ecfg, wcfg.b_min, wcfg.b_max), pack_blob(ecfg, w))
         try:
-            skip = O.completed(storage, "run")
+            skip = O.prepare_resume(storage, "run")
             if attempt == 1:
                 assert 0 < len(skip) < len(parts)
             up = O.AsyncUploader(storage, "run", workers=8, backoff_s=0.001,
@@ -369,9 +369,56 @@ def test_output_side_upload_and_resume(N, tmp_path):
     st = O.LocalStorage(str(tmp_path))
     assert O.completed(st, "run") == {int(k) for k in wl.keys}
     for key, ids, lens in wl:
-        files = [f for f in st.list(f"run/{int(key):020d}") if f.endswith(".arrow")]
-        got = np.concatenate([O.deserialize(st.read(f"run/{int(key):020d}/{f}")) for f in sorted(files)])
+        assert np.array_equal(O.read_partition(st, "run", int(key)), direct[int(key)])
+
+
+def test_output_side_two_ranks_crash_and_resume(N, tmp_path):
+    """NEXT N4 at world_size 2: two ranks (two handles on this GPU, each with its own
+    uploader) write only their LPT pieces; the first run's storage dies for both mid-stream; the
+    restarted ranks skip the partitions whose piece markers (from either rank) tile them, re-encode the
+    rest, and the stored union equals the oracle (north-star gate) and the world_size 1 encoding bit for
+    bit."""
+    from paper_2605_01060_b200 import output as O
+    ecfg = ENCODERS["toy"]
+    wcfg = scaled(WORKLOADS["toy"], n_texts=1500, n_partitions=30, b_min=200, b_max=1000)
+    w = make_weights(ecfg, seed=1234, init="pin")
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=4)
+    direct, _, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+
+    class Dying(O.LocalStorage):
+        def __init__(self, root, budget):
+            super().__init__(root)
+            self.budget = budget
+
+        def write(self, path, data):
+            if self.budget <= 0:
+                raise OSError("storage gone")
+            self.budget -= 1
+            super().write(path, data)
+
+    parts = list(wl)
+    for attempt in range(2):
+        skip = O.prepare_resume(O.LocalStorage(str(tmp_path)), "run")     # rank 0, before the ranks start
+        if attempt == 1:
+            assert 0 < len(skip) < len(parts)
+        for rank in range(2):
+            storage = Dying(str(tmp_path), 20) if attempt == 0 else O.LocalStorage(str(tmp_path))
+            h = N.surge_create(N.make_config(ecfg, wcfg.b_min, wcfg.b_max, rank=rank, world_size=2),
+                               pack_blob(ecfg, w))
+            try:
+                up = O.AsyncUploader(storage, "run", workers=4, backoff_s=0.001,
+                                     release=lambda r, h=h: N.surge_release(h, r))
+                O.encode_to_storage(N, h, parts, up, skip=skip)
+                up.close()
+            finally:
+                N.surge_destroy(h)
+    st = O.LocalStorage(str(tmp_path))
+    assert O.completed(st, "run") == {int(k) for k in wl.keys}
+    E = oenc.Encoder(ecfg, w)
+    for key, ids, lens in wl:
+        got = O.read_partition(st, "run", int(key))
         assert np.array_equal(got, direct[int(key)])
+        compare(got, E.encode_texts(texts_of(ids, lens)))
 
 
 @pytest.mark.parametrize("enc", ["toy", "bgebase"])

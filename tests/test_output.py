@@ -58,3 +58,37 @@ def test_overlap_ratio():
     assert O.overlap_ratio(1.0, 1.0, 1.0) == pytest.approx(0.5)     # half of the I/O exposed
     assert O.overlap_ratio(0.0, 1.0, 0.0) == 0.0
     assert O.overlap_ratio(1.0, 0.0, 0.0) == 1.0
+
+
+def test_two_uploaders_piece_markers_and_stale_pieces(tmp_path):
+    """world_size 2: each rank has its own uploader and writes only its LPT pieces.  Completion is per
+    piece (markers), so a partition split across ranks is complete once both ranks' pieces are durable
+    -- no process ever sees all of its rows.  A stale piece left by an earlier run (other piece
+    boundaries) is ignored by read_partition and removed by prepare_resume with its incomplete
+    partition."""
+    st = O.LocalStorage(str(tmp_path))
+    rng = np.random.default_rng(2)
+    m = rng.standard_normal((10, 4)).astype(np.float32)
+    r0 = O.AsyncUploader(st, "run", workers=2)
+    r1 = O.AsyncUploader(st, "run", workers=2)
+    r0.submit(1, 0, 10, m[:3])           # partition 1: rows [0,3) on rank 0, [3,10) on rank 1
+    r1.submit(1, 3, 10, m[3:])
+    r1.submit(2, 0, 10, m[:4])           # partition 2: rank 0's piece [4,10) never arrives (crash)
+    r0.close()
+    r1.close()
+    assert O.completed(st, "run") == {1}
+    assert np.array_equal(O.read_partition(st, "run", 1), m)
+    with pytest.raises(KeyError):
+        O.read_partition(st, "run", 2)
+    # a stale unmarked piece next to a complete partition is ignored by the reader
+    st.write(O.piece_path("run", 1, 5), O.serialize(m[5:]))
+    assert np.array_equal(O.read_partition(st, "run", 1), m)
+    # resume: complete partitions are kept, incomplete ones are wiped before the re-run
+    assert O.prepare_resume(st, "run") == {1}
+    assert st.list("run/" + f"{2:020d}") == []
+    up = O.AsyncUploader(st, "run", workers=2)
+    up.submit(2, 0, 10, m[:5])           # re-run with different boundaries
+    up.submit(2, 5, 10, m[5:])
+    up.close()
+    assert O.completed(st, "run") == {1, 2}
+    assert np.array_equal(O.read_partition(st, "run", 2), m)

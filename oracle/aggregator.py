@@ -11,6 +11,12 @@ import numpy as np
 
 EFFICIENCY, SAFETY, END_OF_STREAM = "efficiency", "safety", "end_of_stream"
 
+# What B_max does (readings R2/R3 and R23):
+LABEL = "label"          # literal Alg.1: B_max only labels the flush; never split (default)
+SPLIT = "split"          # §6: "splitting the oversized partition across consecutive SuperBatches"
+PREFLUSH = "preflush"    # §3.2: flush the buffer before a partition that would push it past
+                         # B_max; an oversized partition is "emitted ... as its own SuperBatch"
+
 
 class DuplicateKey(ValueError):
     pass
@@ -22,8 +28,9 @@ class SuperBatch:
     idx: int
     reason: str
     keys: list            # partition keys, arrival order
-    sizes: list           # n_k per member
+    sizes: list           # texts per member (n_k, or a piece of it under SPLIT)
     refs: list            # caller payload per member (e.g. partition index)
+    row0: list = field(default_factory=list)   # first row of the member within its partition (SPLIT)
 
     @property
     def total(self) -> int:
@@ -48,10 +55,12 @@ class Aggregator:
     the buffer; an empty residual does not flush.
     """
 
-    def __init__(self, b_min: int, b_max: int):
+    def __init__(self, b_min: int, b_max: int, policy: str = LABEL):
         if not (0 < b_min < b_max):          # S:229
             raise ValueError("need 0 < b_min < b_max")
-        self.b_min, self.b_max = int(b_min), int(b_max)
+        if policy not in (LABEL, SPLIT, PREFLUSH):
+            raise ValueError(policy)
+        self.b_min, self.b_max, self.policy = int(b_min), int(b_max), policy
         self.partitions: list = []           # P:262 `partitions <- []`
         self.total = 0                       # P:262 `total <- 0`
         self.flushes: list[SuperBatch] = []
@@ -74,17 +83,48 @@ class Aggregator:
         if n == 0:
             self.empty_keys.append(key)
             return None
-        self.partitions.append((key, n, ref))    # P:275 partitions.append((key, copy(texts)))
+        if self.policy == SPLIT:
+            return self._add_split(key, n, ref)
+        if self.policy == PREFLUSH and self.partitions and self.total + n > self.b_max:
+            # P:304 "fires only when a single arriving partition would push the running total past
+            # B_max": the buffer flushes first, so no SuperBatch but a lone oversized partition
+            # ("emitting the partition as its own SuperBatch") exceeds B_max
+            self._flush(SAFETY)
+        self.partitions.append((key, n, ref, 0))  # P:275 partitions.append((key, copy(texts)))
         self.total += n                           # P:276 total <- total + |texts|
         self.nmax_seen = max(self.nmax_seen, n)
         self.peak_buffered = max(self.peak_buffered, self.total)
         # Lemma, exact integer prefix form: buffer < B_min before the add, plus n_k.
         assert self.total <= self.b_min - 1 + self.nmax_seen, "Lemma bound violated"
+        if self.policy == PREFLUSH:              # S <= B_max unless the partition is alone
+            assert self.total <= self.b_max or len(self.partitions) == 1
         if self.total >= self.b_max:              # P:277 memory-safety trigger
             return self._flush(SAFETY)
         elif self.total >= self.b_min:            # P:278 efficiency trigger
             return self._flush(EFFICIENCY)
         return None
+
+    def _add_split(self, key, n: int, ref):
+        """SPLIT: texts of the arriving partition fill the buffer up to exactly B_max, which
+        flushes (the Safety trigger), and the rest continues into the next SuperBatches; the boundary
+        records (row0) let the pieces be reassembled ("boundary tracking").  Every SuperBatch
+        then holds at most B_max texts (the Lemma's S <= B_max)."""
+        self.nmax_seen = max(self.nmax_seen, n)
+        row0, last = 0, None
+        while self.total + (n - row0) >= self.b_max:
+            take = self.b_max - self.total
+            self.partitions.append((key, take, ref, row0))
+            self.total += take
+            self.peak_buffered = max(self.peak_buffered, self.total)
+            row0 += take
+            last = self._flush(SAFETY)
+        if row0 < n:
+            self.partitions.append((key, n - row0, ref, row0))
+            self.total += n - row0
+            self.peak_buffered = max(self.peak_buffered, self.total)
+            if self.total >= self.b_min:          # P:278 (total < B_max here)
+                last = self._flush(EFFICIENCY)
+        return last
 
     def finish(self):
         """End of stream: Alg.1 line 9 `AddPartition(curKey,curTexts); Flush()`."""
@@ -97,15 +137,15 @@ class Aggregator:
         """Flush() -- P:282-296 (the encode/slice/upload part lives in oracle.pipeline)."""
         sb = SuperBatch(len(self.flushes), reason,
                         [p[0] for p in self.partitions], [p[1] for p in self.partitions],
-                        [p[2] for p in self.partitions])
+                        [p[2] for p in self.partitions], [p[3] for p in self.partitions])
         self.flushes.append(sb)
         self.partitions, self.total = [], 0      # P:295 partitions <- []; total <- 0
         return sb
 
 
-def run_aggregator(keys, sizes, b_min: int, b_max: int) -> Aggregator:
+def run_aggregator(keys, sizes, b_min: int, b_max: int, policy: str = LABEL) -> Aggregator:
     """Feed a whole arrival sequence through the aggregator and finish."""
-    agg = Aggregator(b_min, b_max)
+    agg = Aggregator(b_min, b_max, policy)
     for i, (k, n) in enumerate(zip(keys, sizes)):
         agg.add_partition(k, int(n), ref=i)
     agg.finish()

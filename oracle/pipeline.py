@@ -38,13 +38,15 @@ class PipelineResult:
 
 
 def run(workload, b_min: int, b_max: int, encoder: Encoder | None = None, world: int = 1,
-        rows: dict | None = None) -> PipelineResult:
+        rows: dict | None = None, policy: str = agg.LABEL) -> PipelineResult:
     """Drive Alg.1 over `workload` (an iterable of (key, ids, lengths)).
 
     encoder=None runs the integer path only.  `rows` optionally restricts encoding to
-    {key: [row indices within the partition]} (sampled parity at full size).
+    {key: [row indices within the partition]} (sampled parity at full size).  Under the SPLIT
+    policy a member is a piece (rows [row0, row0 + n)) of its partition; E_k is reassembled from
+    the pieces by their row offsets ("boundary tracking ensures correct reassembly").
     """
-    A = agg.Aggregator(b_min, b_max)
+    A = agg.Aggregator(b_min, b_max, policy)
     parts = {}
     results, emb = [], {}
 
@@ -52,10 +54,13 @@ def run(workload, b_min: int, b_max: int, encoder: Encoder | None = None, world:
         if sb is None:
             return
         ids_list, lens_list = [], []
-        for key in sb.keys:
-            ids_k, lens_k = parts.pop(key)
-            ids_list.append(ids_k)
-            lens_list.append(lens_k)
+        for key, n, r0 in zip(sb.keys, sb.sizes, sb.row0):
+            ids_k, lens_k = parts[key]
+            tok = np.concatenate([[0], np.cumsum(lens_k)])
+            ids_list.append(ids_k[tok[r0]:tok[r0 + n]])
+            lens_list.append(lens_k[r0:r0 + n])
+            if r0 + n == len(lens_k):
+                parts.pop(key)
         all_ids = np.concatenate(ids_list)                  # allTexts.extend(texts)
         lengths = np.concatenate(lens_list).astype(np.int64)
         packed = agg.pack(lengths, sb.sizes)               # bounds
@@ -66,16 +71,20 @@ def run(workload, b_min: int, b_max: int, encoder: Encoder | None = None, world:
         if encoder is not None:                             # E = f(allTexts)
             cu = packed.cu_seqlens
             for j, (start, end, key) in enumerate(sb.bounds()):   # E_k = E[start:end] P:290-291
-                want = range(end - start) if rows is None else rows.get(key, [])
-                E = {}
+                r0 = sb.row0[j]
+                want = range(r0, r0 + end - start) if rows is None else \
+                    [i for i in rows.get(key, []) if r0 <= i < r0 + end - start]
+                E = emb.setdefault(key, {})
                 for i in want:
-                    g = start + i
+                    g = start + i - r0
                     E[i] = encoder.encode_text(all_ids[cu[g]:cu[g + 1]])
-                emb[key] = E
 
     for key, ids, lengths in workload:
         parts[key] = (np.asarray(ids), np.asarray(lengths))
-        on_flush(A.add_partition(key, len(lengths)))
+        before = len(A.flushes)
+        A.add_partition(key, len(lengths))
+        for sb in A.flushes[before:]:          # PREFLUSH / SPLIT may flush more than once per add
+            on_flush(sb)
     on_flush(A.finish())
     for k in A.empty_keys:
         parts.pop(k, None)

@@ -301,3 +301,58 @@ def test_lpt_textbook_tight_instance():
         loads = [sum(p.tokens for p in per_rank[r]) for r in range(G)]
         assert max(loads) == (4 * G - 1) * 64
         assert _opt_makespan(list(lengths), G) == 3 * G * 64
+
+
+# ------------------------------------------------------ B_max policies (reading R23)
+
+@pytest.mark.parametrize("ex", GOLD["bmax_policy_examples"], ids=lambda e: e["policy"] + ":" + e["cite"][:8])
+def test_bmax_policy_examples(ex):
+    A = agg.run_aggregator(range(len(ex["sizes"])), ex["sizes"], ex["b_min"], ex["b_max"], ex["policy"])
+    got = [{"reason": sb.reason, "total": sb.total, "members": len(sb.keys)} for sb in A.flushes]
+    assert got == ex["expect"]
+
+
+@pytest.mark.parametrize("policy", [agg.SPLIT, agg.PREFLUSH])
+def test_bmax_policy_invariants(policy):
+    """Brute force over random and adversarial orders: every row of every partition lands exactly once,
+    in order; SPLIT caps every SuperBatch at B_max (the Lemma's S <= B_max; eq:memory M(B_max),
+    P:305); PREFLUSH caps it at B_max unless one oversized partition is alone; Efficiency
+    flushes hold >= B_min texts; the Theorem's F <= ceil(N / B_min) + (oversized splits) holds."""
+    rng = np.random.default_rng(7)
+    for trial in range(300):
+        b_min = int(rng.integers(5, 60))
+        b_max = b_min + int(rng.integers(1, 120))
+        sizes = rng.integers(0, 4 * b_max, size=int(rng.integers(1, 40)))
+        if trial % 3 == 0:
+            sizes = np.sort(sizes)                 # largest last (adversarial, SURVEY O8)
+        A = agg.run_aggregator(range(len(sizes)), sizes, b_min, b_max, policy)
+        rows = {k: 0 for k in range(len(sizes))}
+        for sb in A.flushes:
+            for k, n, r0 in zip(sb.keys, sb.sizes, sb.row0):
+                assert n > 0 and r0 == rows[k]     # contiguous pieces, in row order
+                rows[k] += n
+            if policy == agg.SPLIT:
+                assert sb.total <= b_max
+            else:
+                assert sb.total <= b_max or len(sb.keys) == 1
+            if sb.reason == agg.EFFICIENCY:
+                assert b_min <= sb.total < b_max or (policy == agg.PREFLUSH and len(sb.keys) == 1)
+        assert all(rows[k] == int(sizes[k]) for k in rows)
+        assert A.peak_buffered <= (b_max if policy == agg.SPLIT else max(b_max, int(sizes.max())))
+        if policy == agg.SPLIT:
+            assert A.peak_buffered <= b_max and agg.memory_bound_bytes(A.peak_buffered, 47, 384) <= \
+                agg.memory_bound_bytes(b_max, 47, 384)
+
+
+def test_bmax_policies_agree_without_oversized_partitions():
+    """Special case: when no arrival can reach B_max (B_min - 1 + n_max < B_max, so the Safety
+    trigger never fires), all three readings reduce to the same Alg.1 flush sequence."""
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        b_min, b_max = 100, 400
+        sizes = rng.integers(0, 300, size=50)
+        seqs = []
+        for policy in (agg.LABEL, agg.SPLIT, agg.PREFLUSH):
+            A = agg.run_aggregator(range(len(sizes)), sizes, b_min, b_max, policy)
+            seqs.append([(sb.reason, sb.keys, sb.sizes) for sb in A.flushes])
+        assert seqs[0] == seqs[1] == seqs[2]

@@ -116,13 +116,17 @@ def test_pool_closed_forms():
     assert np.array_equal(enc.mean_pool_l2(np.zeros((3, 4))), np.zeros(4))   # max(||v||, 1e-12) guard
 
 
-def test_unit_norm_and_invariance_toy():
-    """O3 unit norm on every row; O4 packed-SuperBatch path == PBP path bit-exactly."""
+@pytest.mark.parametrize("policy,b_max", [("label", None), ("split", 70), ("preflush", 70)])
+def test_unit_norm_and_invariance_toy(policy, b_max):
+    """O3 unit norm on every row; O4 packed-SuperBatch path == PBP path bit-exactly (also when SPLIT
+    cuts partitions across SuperBatches and reassembles them by row offset)."""
     ecfg, wcfg = ENCODERS["toy"], WORKLOADS["toy"]
     w = make_weights(ecfg, seed=1234)
     E = enc.Encoder(ecfg, w)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=0)
-    res = pipeline.run(wl, wcfg.b_min, wcfg.b_max, encoder=E)
+    res = pipeline.run(wl, wcfg.b_min, b_max or wcfg.b_max, encoder=E, policy=policy)
+    if policy == "split":
+        assert any(len(set(sb.sb.keys)) < len(sb.sb.keys) or any(r > 0 for r in sb.sb.row0) for sb in res.superbatches)
     pbp = pipeline.encode_pbp(wl, E)
     assert len(res.superbatches) >= 2
     for key, M in res.embeddings.items():

@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--encoder", default="minilm", choices=["minilm", "bgebase", "bgelarge", "toy"],
                     help="encoder class (the headline is minilm; bgebase/bgelarge = NEXT N1)")
     ap.add_argument("--n-texts", type=int, default=0, help="override N (default: the config's 10M)")
+    ap.add_argument("--n-partitions", type=int, default=0, help="override P")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--chunk-tokens", type=int, default=0)
     ap.add_argument("--att-fused", type=int, default=1, choices=[0, 1],
@@ -52,6 +53,10 @@ def parse():
                     help="1: K7 FFN1+GELU and K8 FFN2+LN as one kernel (default); 0: separate GEMMs")
     ap.add_argument("--tail-fused", type=int, default=1, choices=[0, 1],
                     help="1: K6 out-proj+LN also inside the fused MLP kernel (default); 0: own kernel")
+    ap.add_argument("--bmax-policy", default="label", choices=["label", "split", "preflush"],
+                    help="what B_max does (include/surge.h SURGE_BMAX_*): literal Alg.1 (default), "
+                         "split oversized partitions (P:1271), or flush before them (P:304/P:308)")
+    ap.add_argument("--b-min", type=int, default=0, help="override the workload's B_min (B_max = 5 B_min)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -141,9 +146,7 @@ def run_host_only(args, world, rank):
     import torch.distributed as dist
     from paper_2605_01060_b200 import native as N
     ecfg = ENCODERS[args.encoder]
-    wcfg = WORKLOADS[args.workload]
-    if args.n_texts:
-        wcfg = scaled(wcfg, n_texts=args.n_texts)
+    wcfg = workload_cfg(args)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
     t0 = time.perf_counter()
     sbs, peak = N.surge_aggregate(wl.sizes.astype(np.int64), wcfg.b_min, wcfg.b_max)
@@ -164,6 +167,20 @@ def run_host_only(args, world, rank):
                           "texts_per_rank": [int(x[0]) for x in per_rank],
                           "tokens_per_rank": [int(x[1]) for x in per_rank],
                           "n_texts": wl.n_texts, "n_tokens": wl.n_tokens}), flush=True)
+
+
+def workload_cfg(args):
+    """BASELINE.json workload named by --workload, with the optional N / P / B_min overrides."""
+    from dataclasses import replace
+    wcfg = WORKLOADS[args.workload]
+    kw = {}
+    if args.n_texts:
+        kw["n_texts"] = args.n_texts
+    if args.n_partitions:
+        kw["n_partitions"] = args.n_partitions
+    if args.b_min:
+        kw.update(b_min=args.b_min, b_max=5 * args.b_min)      # B_max = 5 B_min (P:867)
+    return replace(wcfg, **kw) if kw else wcfg
 
 
 def _oracle_flops_per_text(ecfg, l: int) -> float:
@@ -218,9 +235,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     ecfg = ENCODERS[args.encoder]
-    wcfg = WORKLOADS[args.workload]
-    if args.n_texts:
-        wcfg = scaled(wcfg, n_texts=args.n_texts)
+    wcfg = workload_cfg(args)
     w = make_weights(ecfg, seed=1234)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
     from oracle import pool as opool
@@ -300,15 +315,14 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ecfg = ENCODERS[args.encoder]
-    wcfg = WORKLOADS[args.workload]
-    if args.n_texts:
-        wcfg = scaled(wcfg, n_texts=args.n_texts)
+    wcfg = workload_cfg(args)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=args.seed)
     # weights: rank 0 draws them; libsurge replicates them with one NCCL broadcast (K11)
     w = make_weights(ecfg, seed=1234) if rank == 0 or world == 1 else None
     n_w = sum(int(np.prod(s)) for s in [v.shape for v in (w or make_weights_shapes(ecfg)).values()])
+    policy = N.BMAX_POLICIES[args.bmax_policy]
     cfg = N.make_config(ecfg, wcfg.b_min, wcfg.b_max, rank=rank, world_size=world, device=local,
-                        chunk_tokens=args.chunk_tokens, weights_on_device=1)
+                        chunk_tokens=args.chunk_tokens, weights_on_device=1, bmax_policy=policy)
     blob_dev = torch.from_numpy(pack_blob(ecfg, w).view(np.uint16)).to(dev) if w is not None else None
     if world > 1:
         import torch.distributed as dist
@@ -326,18 +340,20 @@ def main():
     d_ids = torch.from_numpy(wl.ids).to(dev)
     d_len = torch.from_numpy(wl.lengths).to(dev)
     d_out = torch.empty(wl.n_texts, ecfg.hidden, dtype=torch.float32, device=dev)
-    text_off, tok_off = wl.text_off, wl.tok_off
+    text_off = wl.text_off
+    text_tok = np.concatenate([[0], np.cumsum(wl.lengths, dtype=np.int64)])   # first token of every text
 
     def step(limit_sb=None):
-        sbs, _ = N.surge_aggregate(sizes, wcfg.b_min, wcfg.b_max)         # a1 (host, Alg.1)
-        for j, (a, b, _r) in enumerate(sbs):
+        sbs, _ = N.surge_aggregate_ex(sizes, wcfg.b_min, wcfg.b_max, policy)   # a1 (host, Alg.1 + B_max policy)
+        for j, (_r, members) in enumerate(sbs):
             if limit_sb is not None and j >= limit_sb:
                 break
-            t0, t1 = int(text_off[a]), int(text_off[b])
-            k0 = int(tok_off[a])
-            N.surge_encode_superbatch(h, d_ids.data_ptr() + 4 * k0, d_len.data_ptr() + 4 * t0,
-                                      wl.lengths[t0:t1], sizes[a:b], d_out.data_ptr() + 4 * t0 * ecfg.hidden,
-                                      stream)
+            p0, r0, _ = members[0]
+            t0 = int(text_off[p0]) + r0                 # a SuperBatch is a contiguous run of texts
+            rows = np.array([m[2] for m in members], np.int64)
+            t1 = t0 + int(rows.sum())
+            N.surge_encode_superbatch(h, d_ids.data_ptr() + 4 * int(text_tok[t0]), d_len.data_ptr() + 4 * t0,
+                                      wl.lengths[t0:t1], rows, d_out.data_ptr() + 4 * t0 * ecfg.hidden, stream)
         return len(sbs)
 
     if args.profile_run:

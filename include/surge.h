@@ -50,6 +50,23 @@ typedef enum {
 
 typedef struct surge_ctx* surge_handle;
 
+/*
+ * What B_max does (surge_config.bmax_policy; readings R2/R3/R23):
+ *   SURGE_BMAX_LABEL    literal Alg.1: total >= b_max labels the flush Safety; a partition
+ *                       is never split and flushes together with the buffer (default).
+ *   SURGE_BMAX_SPLIT    P:1271 "splitting the oversized partition across consecutive SuperBatches":
+ *                       the arriving partition's texts fill the buffer up to exactly b_max, which
+ *                       flushes (Safety); the rest continues into the next SuperBatches.  Every
+ *                       SuperBatch holds <= b_max texts (the Lemma's S <= B_max); a partition
+ *                       may come back as several pieces (row_begin), possibly from several SuperBatches.
+ *   SURGE_BMAX_PREFLUSH P:304 / P:308: before adding a partition that would push the buffer past b_max
+ *                       the buffer flushes (Safety); a partition of > b_max texts is then emitted as
+ *                       its own SuperBatch.  S <= b_max unless one oversized partition is alone.
+ */
+#define SURGE_BMAX_LABEL 0
+#define SURGE_BMAX_SPLIT 1
+#define SURGE_BMAX_PREFLUSH 2
+
 /* Output element types (surge_config.out_dtype, surge_flushed.dtype). */
 #define SURGE_F32 0    /* float32 unit vectors: the paper's output (pa.float32()), default */
 #define SURGE_BF16 1   /* bf16 bit patterns (uint16): half the D2H / host bytes per text           */
@@ -84,6 +101,7 @@ typedef struct {
   int32_t weights_on_device;    /* 1: `weights` passed to surge_create is a device pointer       */
   int32_t out_dtype;            /* SURGE_F32 (default) or SURGE_BF16: element type of every output
                                    row (streaming pieces and the device-level d_out buffers)      */
+  int32_t bmax_policy;          /* SURGE_BMAX_LABEL (default), SURGE_BMAX_SPLIT, SURGE_BMAX_PREFLUSH */
 } surge_config;
 
 /*
@@ -304,10 +322,26 @@ surge_status surge_aggregate(const int64_t* sizes, int64_t n_partitions, int64_t
                              int64_t* n_superbatches, int64_t* peak_buffered);
 
 /*
+ * Alg.1 under a B_max policy as a pure host function (the aggregator the streaming path runs):
+ * partitions of `sizes` (arrival order) -> SuperBatches of members, a member being a partition or,
+ * under SURGE_BMAX_SPLIT, a contiguous piece of one.
+ *   member j: m_partition[j] (index into sizes), m_row0[j] (first row within the partition),
+ *             m_rows[j] (texts); members are listed SuperBatch by SuperBatch, in stream order.
+ *   SuperBatch i = members [sb_first[i], sb_first[i+1]), reason sb_reason[i] (0 efficiency,
+ *             1 safety, 2 end of stream); sb_first has n_superbatches + 1 entries.
+ * Zero-size partitions never enter a SuperBatch.  SURGE_E_INVALID_ARG if a capacity is too small.
+ */
+surge_status surge_aggregate_ex(const int64_t* sizes, int64_t n_partitions, int64_t b_min, int64_t b_max,
+                                int32_t policy, int64_t member_capacity, int64_t* m_partition, int64_t* m_row0,
+                                int64_t* m_rows, int64_t sb_capacity, int64_t* sb_first, int32_t* sb_reason,
+                                int64_t* n_superbatches, int64_t* n_members, int64_t* peak_buffered);
+
+/*
  * One SuperBatch, device-resident (the step surge_submit_partition's pipeline runs per flush):
  *   d_ids     device int32[sum(lengths)], the SuperBatch's texts concatenated (Flush allTexts)
  *   d_lengths device int32[n_texts];  h_lengths host int32[n_texts] (same values, cuts chunks)
- *   h_sizes   host int64[n_members], n_k of each member in arrival order (bounds)
+ *   h_sizes   host int64[n_members], texts of each member in arrival order (bounds; a
+ *             member may be a piece of a partition, see surge_aggregate_ex)
  *   d_out     device [n_texts * d] (cfg.out_dtype): rows of THIS rank's LPT pieces are written at their
  *             SuperBatch row positions (all rows when world_size == 1); other rows are untouched.
  * K2 LPT plan (world_size > 1) -> gather of the rank's pieces -> K1 pack -> encoder chunks ->

@@ -46,6 +46,41 @@ inline int alg1_decide(int64_t total, int64_t b_min, int64_t b_max) {
   return -1;
 }
 
+// One AddPartition under a B_max policy (include/surge.h SURGE_BMAX_*), as steps over the arriving
+// partition's rows: append rows [row0, row0 + rows) to the open SuperBatch, or seal it (Flush).
+// `total` = texts already buffered (< b_min between calls).
+struct AggStep {
+  bool seal;
+  int64_t row0, rows;
+  int reason;
+};
+
+void plan_add(int64_t total, int64_t n, int64_t b_min, int64_t b_max, int policy, std::vector<AggStep>& out) {
+  out.clear();
+  if (policy == SURGE_BMAX_SPLIT) {          // fill to exactly b_max, flush, continue
+    int64_t row0 = 0;
+    while (total + (n - row0) >= b_max) {
+      const int64_t take = b_max - total;
+      out.push_back({false, row0, take, 0});
+      out.push_back({true, 0, 0, REASON_SAFETY});
+      row0 += take;
+      total = 0;
+    }
+    if (row0 < n) {
+      out.push_back({false, row0, n - row0, 0});
+      if (total + (n - row0) >= b_min) out.push_back({true, 0, 0, REASON_EFFICIENCY});
+    }
+    return;
+  }
+  if (policy == SURGE_BMAX_PREFLUSH && total > 0 && total + n > b_max) {   // P:304 / P:308
+    out.push_back({true, 0, 0, REASON_SAFETY});
+    total = 0;
+  }
+  out.push_back({false, 0, n, 0});           // P:275-276 append, total += n
+  const int r = alg1_decide(total + n, b_min, b_max);
+  if (r >= 0) out.push_back({true, 0, 0, r});
+}
+
 double secs(Clock::time_point a, Clock::time_point b) { return std::chrono::duration<double>(b - a).count(); }
 
 struct PinnedBuf {
@@ -110,7 +145,8 @@ struct SuperBatch {
   int64_t index = 0;
   int reason = 0;
   std::vector<uint64_t> keys;
-  std::vector<int64_t> sizes;
+  std::vector<int64_t> sizes;                // texts of each member
+  std::vector<int64_t> row0, part_rows;      // member = rows [row0, row0 + size) of a partition of part_rows
   std::vector<int64_t> text_off, tok_off;   // per member, within the staging buffer
   int64_t n_texts = 0, n_tokens = 0;
   PinnedBuf stage;                           // ids [n_tokens] then lengths [n_texts] (int32)
@@ -215,7 +251,8 @@ struct Ctx {
 
   // ---- aggregator state (producer thread)
   std::vector<uint64_t> buf_keys;
-  std::vector<int64_t> buf_sizes, buf_text_off, buf_tok_off;
+  std::vector<int64_t> buf_sizes, buf_text_off, buf_tok_off, buf_row0, buf_part_rows;
+  std::vector<AggStep> plan;
   int64_t total = 0, total_tokens = 0;
   PinnedBuf stage;                   // open SuperBatch staging
   std::vector<int32_t> stage_len_tmp;  // lengths of the open SuperBatch (host, pageable)
@@ -512,6 +549,8 @@ int seal(Ctx* c, int reason) {
   sb->reason = reason;
   sb->keys.swap(c->buf_keys);
   sb->sizes.swap(c->buf_sizes);
+  sb->row0.swap(c->buf_row0);
+  sb->part_rows.swap(c->buf_part_rows);
   sb->text_off.swap(c->buf_text_off);
   sb->tok_off.swap(c->buf_tok_off);
   sb->n_texts = c->total;
@@ -606,6 +645,7 @@ surge_status surge_create(const surge_config* cfg, const uint16_t* weights, size
     return SURGE_E_INVALID_ARG;
   if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return SURGE_E_INVALID_ARG;
   if (k.out_dtype != SURGE_F32 && k.out_dtype != SURGE_BF16) return SURGE_E_INVALID_ARG;
+  if (k.bmax_policy < SURGE_BMAX_LABEL || k.bmax_policy > SURGE_BMAX_PREFLUSH) return SURGE_E_INVALID_ARG;
   ModelShape s{k.vocab_size, k.max_position, k.type_vocab_size, k.hidden, k.layers, k.heads, k.ffn, k.ln_eps};
   if (n_weights != blob_elems(s)) return SURGE_E_INVALID_ARG;
 
@@ -740,13 +780,13 @@ surge_status surge_submit_partition(surge_handle h, uint64_t partition_id, const
     for (int64_t i = 0; i < ntok; ++i) bad |= uint32_t(uint32_t(token_ids[i]) >= V);
     if (bad) return SURGE_E_TOKEN_ID;
   }
-  // backpressure: would this add seal a SuperBatch while the pipeline is full?
-  const bool will_seal = n_texts > 0 && (c->total + n_texts >= c->cfg.b_min);
-  if (will_seal) {
-    std::unique_lock<std::mutex> g(c->mu);
-    if (c->cfg.nonblocking_submit && c->inflight_sbs >= c->cfg.max_inflight) return SURGE_E_AGAIN;
-    c->cv_space.wait(g, [&] { return c->inflight_sbs < c->cfg.max_inflight || c->poisoned; });
-    if (c->poisoned) return surge_status(c->poisoned);
+  // the add as Alg.1 steps under the B_max policy (appends and seals)
+  plan_add(c->total, n_texts, c->cfg.b_min, c->cfg.b_max, c->cfg.bmax_policy, c->plan);
+  // backpressure: a seal needs a free pipeline slot (nonblocking: refuse before consuming anything)
+  const bool will_seal = n_texts > 0 && std::any_of(c->plan.begin(), c->plan.end(), [](const AggStep& s) { return s.seal; });
+  if (will_seal && c->cfg.nonblocking_submit) {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (c->inflight_sbs >= c->cfg.max_inflight) return SURGE_E_AGAIN;
   }
   if (!c->have_first_submit) {
     std::lock_guard<std::mutex> g(c->mu);
@@ -768,26 +808,42 @@ surge_status surge_submit_partition(surge_handle h, uint64_t partition_id, const
     }
     return SURGE_OK;
   }
-  // copy(texts) into pinned staging (Alg.1)
-  if (!ensure_pinned_keep(c->stage, size_t(c->total_tokens + ntok) * 4, size_t(c->total_tokens) * 4)) {
-    c->set_error(SURGE_E_OOM, "pinned staging allocation failed");
-    return SURGE_E_OOM;
-  }
-  std::memcpy(static_cast<int32_t*>(c->stage.p) + c->total_tokens, token_ids, size_t(ntok) * 4);
-  c->stage_len_tmp.insert(c->stage_len_tmp.end(), lengths, lengths + n_texts);
-  c->buf_keys.push_back(partition_id);
-  c->buf_sizes.push_back(n_texts);
-  c->buf_text_off.push_back(c->total);
-  c->buf_tok_off.push_back(c->total_tokens);
-  c->total += n_texts;                 // total <- total + |texts|
-  c->total_tokens += ntok;
-  {
+  int64_t tok_row = 0, tok_at = 0;   // token offset (within the partition) of row tok_row
+  for (const AggStep& step : c->plan) {
+    if (step.seal) {
+      {
+        std::unique_lock<std::mutex> g(c->mu);
+        c->cv_space.wait(g, [&] { return c->inflight_sbs < c->cfg.max_inflight || c->poisoned; });
+        if (c->poisoned) return surge_status(c->poisoned);
+      }
+      if (int r = seal(c, step.reason)) return surge_status(r);
+      continue;
+    }
+    // copy(texts) of rows [row0, row0 + rows) into pinned staging (Alg.1)
+    while (tok_row < step.row0) tok_at += lengths[tok_row++];
+    int64_t pt = 0;
+    for (int64_t i = step.row0; i < step.row0 + step.rows; ++i) pt += lengths[i];
+    if (!ensure_pinned_keep(c->stage, size_t(c->total_tokens + pt) * 4, size_t(c->total_tokens) * 4)) {
+      c->set_error(SURGE_E_OOM, "pinned staging allocation failed");
+      return SURGE_E_OOM;
+    }
+    std::memcpy(static_cast<int32_t*>(c->stage.p) + c->total_tokens, token_ids + tok_at, size_t(pt) * 4);
+    c->stage_len_tmp.insert(c->stage_len_tmp.end(), lengths + step.row0, lengths + step.row0 + step.rows);
+    c->buf_keys.push_back(partition_id);
+    c->buf_sizes.push_back(step.rows);
+    c->buf_row0.push_back(step.row0);
+    c->buf_part_rows.push_back(n_texts);
+    c->buf_text_off.push_back(c->total);
+    c->buf_tok_off.push_back(c->total_tokens);
+    c->total += step.rows;               // total <- total + |texts|
+    c->total_tokens += pt;
+    tok_at += pt;
+    tok_row = step.row0 + step.rows;
     std::lock_guard<std::mutex> g(c->mu);
     c->st.peak_buffered_texts = std::max(c->st.peak_buffered_texts, c->total);
     c->st.peak_buffered_bytes = std::max(c->st.peak_buffered_bytes, (c->total_tokens + c->total) * 4);
   }
-  const int reason = alg1_decide(c->total, c->cfg.b_min, c->cfg.b_max);
-  return surge_status(reason >= 0 ? seal(c, reason) : 0);
+  return SURGE_OK;
 }
 
 surge_status surge_finish(surge_handle h) {
@@ -840,9 +896,9 @@ surge_status surge_poll_flushed(surge_handle h, surge_flushed* out, int64_t max_
       continue;
     }
     const LptPiece& p = r.sb->pieces[r.piece];
-    f.row_begin = p.first_row - r.sb->text_off[p.member];
+    f.row_begin = r.sb->row0[p.member] + (p.first_row - r.sb->text_off[p.member]);
     f.n_rows = p.n_rows;
-    f.partition_rows = r.sb->sizes[p.member];
+    f.partition_rows = r.sb->part_rows[p.member];
     f.data = static_cast<const uint8_t*>(r.sb->out.p) +
              size_t(r.sb->piece_local_row[r.piece]) * c->shape.d * c->model.out_elem_bytes();
     f.superbatch = r.sb->index;
@@ -1194,6 +1250,51 @@ surge_status surge_aggregate(const int64_t* sizes, int64_t n_partitions, int64_t
   if (open && total > 0 && !emit(n_partitions, REASON_END)) return SURGE_E_INVALID_ARG;
   if (sb_first && F > 0) sb_first[F] = n_partitions;   // trailing empty partitions join the last range
   *n_superbatches = F;
+  if (peak_buffered) *peak_buffered = peak;
+  return SURGE_OK;
+}
+
+surge_status surge_aggregate_ex(const int64_t* sizes, int64_t n_partitions, int64_t b_min, int64_t b_max,
+                                int32_t policy, int64_t member_capacity, int64_t* m_partition, int64_t* m_row0,
+                                int64_t* m_rows, int64_t sb_capacity, int64_t* sb_first, int32_t* sb_reason,
+                                int64_t* n_superbatches, int64_t* n_members, int64_t* peak_buffered) {
+  using namespace surge;
+  if (!n_superbatches || !n_members || n_partitions < 0 || b_min <= 0 || b_max <= b_min ||
+      (n_partitions > 0 && !sizes) || policy < SURGE_BMAX_LABEL || policy > SURGE_BMAX_PREFLUSH)
+    return SURGE_E_INVALID_ARG;
+  std::vector<AggStep> plan;
+  int64_t total = 0, peak = 0, F = 0, M = 0;
+  auto seal_sb = [&](int reason) -> bool {
+    if (F >= sb_capacity) return false;
+    if (sb_reason) sb_reason[F] = reason;
+    ++F;
+    if (sb_first) sb_first[F] = M;
+    total = 0;
+    return true;
+  };
+  if (sb_first && sb_capacity >= 0) sb_first[0] = 0;
+  for (int64_t k = 0; k < n_partitions; ++k) {
+    const int64_t n = sizes[k];
+    if (n < 0) return SURGE_E_INVALID_ARG;
+    if (n == 0) continue;                 // completes immediately, never buffered
+    plan_add(total, n, b_min, b_max, policy, plan);
+    for (const AggStep& st : plan) {
+      if (st.seal) {
+        if (!seal_sb(st.reason)) return SURGE_E_INVALID_ARG;
+        continue;
+      }
+      if (M >= member_capacity) return SURGE_E_INVALID_ARG;
+      if (m_partition) m_partition[M] = k;
+      if (m_row0) m_row0[M] = st.row0;
+      if (m_rows) m_rows[M] = st.rows;
+      ++M;
+      total += st.rows;                   // total <- total + |texts|
+      peak = std::max(peak, total);
+    }
+  }
+  if (total > 0 && !seal_sb(REASON_END)) return SURGE_E_INVALID_ARG;   // Alg.1 final Flush
+  *n_superbatches = F;
+  *n_members = M;
   if (peak_buffered) *peak_buffered = peak;
   return SURGE_OK;
 }

@@ -44,7 +44,7 @@ class surge_config(C.Structure):
                 ("ln_eps", C.c_float), ("b_min", C.c_int64), ("b_max", C.c_int64),
                 ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
                 ("chunk_tokens", C.c_int32), ("max_inflight", C.c_int32), ("nonblocking_submit", C.c_int32),
-                ("weights_on_device", C.c_int32), ("out_dtype", C.c_int32)]
+                ("weights_on_device", C.c_int32), ("out_dtype", C.c_int32), ("bmax_policy", C.c_int32)]
 
 
 class surge_flushed(C.Structure):
@@ -78,6 +78,8 @@ SURGE_OPT_TAIL_FUSED = 3
 SURGE_OPT_POOLING = 4
 SURGE_POOL_MEAN, SURGE_POOL_CLS = 0, 1
 SURGE_F32, SURGE_BF16 = 0, 1
+SURGE_BMAX_LABEL, SURGE_BMAX_SPLIT, SURGE_BMAX_PREFLUSH = 0, 1, 2
+BMAX_POLICIES = {"label": 0, "split": 1, "preflush": 2}
 
 
 class surge_superbatch_info(C.Structure):
@@ -113,6 +115,8 @@ _SIGS = {
     "surge_op_attention": (C.c_int, [_p, _p, C.c_int64, C.c_int32, C.c_int32, _p, _p]),
     "surge_op_layernorm": (C.c_int, [_p, C.c_int64, C.c_int32, _p, _p, C.c_float, _p, _p]),
     "surge_op_meanpool_l2": (C.c_int, [_p, _p, C.c_int64, C.c_int32, _p, _p]),
+    "surge_aggregate_ex": (C.c_int, [_p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int64, _p, _p, _p,
+                                     C.c_int64, _p, _p, _i64p, _i64p, _i64p]),
     "surge_aggregate": (C.c_int, [_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _p, _p, _i64p, _i64p]),
     "surge_encode_superbatch": (C.c_int, [_p, _p, _p, _p, C.c_int64, _p, C.c_int64, _p, _p]),
     "surge_profile_enable": (C.c_int, [_p, C.c_int32]),
@@ -163,11 +167,11 @@ def surge_version() -> str:
 
 def make_config(enc, b_min: int, b_max: int, rank: int = 0, world_size: int = 1, device: int = 0,
                 chunk_tokens: int = 0, max_inflight: int = 0, nonblocking_submit: int = 0,
-                weights_on_device: int = 0, out_dtype: int = 0) -> surge_config:
+                weights_on_device: int = 0, out_dtype: int = 0, bmax_policy: int = 0) -> surge_config:
     """surge_config from a synth.configs.EncoderConfig-like object."""
     return surge_config(enc.vocab_size, enc.max_position, enc.type_vocab_size, enc.hidden, enc.layers, enc.heads,
                         enc.ffn, enc.ln_eps, b_min, b_max, rank, world_size, device, chunk_tokens, max_inflight,
-                        nonblocking_submit, weights_on_device, out_dtype)
+                        nonblocking_submit, weights_on_device, out_dtype, bmax_policy)
 
 
 def surge_create(cfg: surge_config, weights, n_weights: int | None = None):
@@ -352,6 +356,28 @@ def surge_aggregate(sizes, b_min: int, b_max: int):
     _check(None, lib.surge_aggregate(sz.ctypes.data, sz.size, b_min, b_max, cap, first.ctypes.data,
                                      reason.ctypes.data, C.byref(n), C.byref(peak)), "surge_aggregate")
     return [(int(first[j]), int(first[j + 1]), REASONS[int(reason[j])]) for j in range(n.value)], peak.value
+
+
+def surge_aggregate_ex(sizes, b_min: int, b_max: int, policy: int = 0):
+    """-> (list of SuperBatches [(reason, [(partition index, row0, rows), ...])], peak_buffered) --
+    Alg.1 under a B_max policy (host-only)."""
+    sz = np.ascontiguousarray(sizes, dtype=np.int64)
+    nonzero = int((sz > 0).sum())
+    total = int(sz.sum())
+    scap = 2 * nonzero + total // max(b_max, 1) + 2     # SuperBatches (PREFLUSH: <= 2 per partition)
+    mcap = nonzero + scap                               # members (SPLIT: <= one extra piece per seal)
+    mp, mr0, mr = np.zeros(mcap, np.int64), np.zeros(mcap, np.int64), np.zeros(mcap, np.int64)
+    first, reason = np.zeros(scap + 1, np.int64), np.zeros(scap, np.int32)
+    F, M, peak = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(None, lib.surge_aggregate_ex(sz.ctypes.data, sz.size, b_min, b_max, policy, mcap, mp.ctypes.data,
+                                        mr0.ctypes.data, mr.ctypes.data, scap, first.ctypes.data,
+                                        reason.ctypes.data, C.byref(F), C.byref(M), C.byref(peak)),
+           "surge_aggregate_ex")
+    out = []
+    for j in range(F.value):
+        a, b = int(first[j]), int(first[j + 1])
+        out.append((REASONS[int(reason[j])], [(int(mp[i]), int(mr0[i]), int(mr[i])) for i in range(a, b)]))
+    return out, peak.value
 
 
 def surge_encode_superbatch(h, d_ids, d_lengths, h_lengths: np.ndarray, h_sizes: np.ndarray, d_out, stream=None):

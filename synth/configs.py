@@ -80,6 +80,10 @@ WORKLOADS = {
     "minilm": WorkloadConfig("minilm", n_texts=10_000_000, n_partitions=4000, sigma=1.72),
     "minilm_s1.0": WorkloadConfig("minilm_s1.0", n_texts=10_000_000, n_partitions=4000, sigma=1.0),
     "minilm_s2.5": WorkloadConfig("minilm_s2.5", n_texts=10_000_000, n_partitions=4000, sigma=2.5),
+    # C5 skew/scale stress (BASELINE.json configs[4]; tab:sigma-sweep P:764-785, tab:scaling P:1195-1223)
+    "c5_s1.0": WorkloadConfig("c5_s1.0", n_texts=100_000_000, n_partitions=40_000, sigma=1.0),
+    "c5_s1.72": WorkloadConfig("c5_s1.72", n_texts=100_000_000, n_partitions=40_000, sigma=1.72),
+    "c5_s2.5": WorkloadConfig("c5_s2.5", n_texts=100_000_000, n_partitions=40_000, sigma=2.5),
     # C4 long-length variant (seq <= 512)
     "long": WorkloadConfig("long", n_texts=10_000_000, n_partitions=4000, sigma=1.72,
                            length_model="long"),

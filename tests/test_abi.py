@@ -113,3 +113,29 @@ def test_nccl_unique_id_without_gpu():
     from paper_2605_01060_b200 import native as N
     a, b = N.surge_nccl_unique_id(), N.surge_nccl_unique_id()
     assert len(a) == len(b) == 128 and a != b
+
+
+@pytest.mark.parametrize("policy", ["label", "split", "preflush"])
+def test_native_aggregate_ex_equals_oracle(policy):
+    """surge_aggregate_ex (the aggregator the streaming path runs) == the oracle's Alg.1 under every
+    B_max reading: SuperBatch reasons, members (partition, row0, rows) and the peak, bit-exact."""
+    from oracle import aggregator as oagg
+    from paper_2605_01060_b200 import native as N
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        b_min = int(rng.integers(5, 80))
+        b_max = b_min + int(rng.integers(1, 200))
+        sizes = rng.integers(0, 5 * b_max, size=int(rng.integers(1, 60)))
+        if trial % 2:
+            sizes = np.sort(sizes)
+        got, peak = N.surge_aggregate_ex(sizes, b_min, b_max, N.BMAX_POLICIES[policy])
+        A = oagg.run_aggregator(range(len(sizes)), sizes, b_min, b_max, policy)
+        want = [(sb.reason, list(zip(sb.refs, sb.row0, sb.sizes))) for sb in A.flushes]
+        assert got == want
+        assert peak == A.peak_buffered
+    from synth.configs import WORKLOADS, ENCODERS, scaled
+    from synth.workload import make_workload
+    wl = make_workload(scaled(WORKLOADS["minilm_s2.5"], n_texts=2_000_000, n_partitions=800), 30522, 512, seed=1)
+    got, peak = N.surge_aggregate_ex(wl.sizes, 20_000, 100_000, N.BMAX_POLICIES[policy])
+    A = oagg.run_aggregator(range(len(wl.sizes)), wl.sizes, 20_000, 100_000, policy)
+    assert got == [(sb.reason, list(zip(sb.refs, sb.row0, sb.sizes))) for sb in A.flushes] and peak == A.peak_buffered

@@ -577,3 +577,45 @@ def test_create_replicated_nccl_single_rank(N):
         assert N.surge_get_stats(h)["init_s"] > 0
     finally:
         N.surge_destroy(h)
+
+
+@pytest.mark.parametrize("enc,policy", [("toy", "split"), ("toy", "preflush"), ("minilm", "split")])
+def test_bmax_policies_streaming(N, enc, policy):
+    """NEXT N2: the B_max readings SPLIT and PREFLUSH on the streaming ABI.
+    Integer parity with the oracle's aggregator under the same policy (SuperBatch members, texts,
+    reasons, Safety count, peak buffered); under SPLIT every SuperBatch holds <= B_max texts and split
+    partitions come back as pieces whose row offsets reassemble them (P:1271 "boundary tracking");
+    the reassembled embeddings equal the literal-Alg.1 run bit for bit (the policy changes only
+    which invocation computes a row) and the oracle under the north-star gate."""
+    ecfg = ENCODERS[enc]
+    if enc == "toy":
+        wcfg = scaled(WORKLOADS["toy"], n_texts=1500, n_partitions=30, b_min=60, b_max=100)
+        w = make_weights(ecfg, seed=1234, init="pin")
+    else:
+        wcfg = scaled(WORKLOADS["minilm_s2.5"], n_texts=40_000, n_partitions=16, b_min=2000, b_max=10_000)
+        w = make_weights(ecfg, seed=1234)
+    wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=5)
+    assert wl.sizes.max() > wcfg.b_max                     # an oversized partition exists
+    label, _, _, _ = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max)
+    got, sbs, stats, pieces = run_lib(N, ecfg, w, wl, wcfg.b_min, wcfg.b_max, bmax_policy=N.BMAX_POLICIES[policy])
+    A = oagg.run_aggregator([int(k) for k in wl.keys], wl.sizes, wcfg.b_min, wcfg.b_max, policy)
+    assert [(s["reason"], s["members"], s["n_texts"]) for s in sbs] == \
+        [(f.reason, [int(k) for k in f.keys], f.total) for f in A.flushes]
+    assert stats["safety_flushes"] == sum(f.reason == oagg.SAFETY for f in A.flushes) > 0
+    assert stats["peak_buffered_texts"] == A.peak_buffered
+    if policy == "split":
+        assert max(s["n_texts"] for s in sbs) <= wcfg.b_max and A.peak_buffered <= wcfg.b_max
+        assert any(len(parts) > 1 for _, parts in pieces.values())
+    else:
+        assert all(s["n_texts"] <= wcfg.b_max or len(s["members"]) == 1 for s in sbs)
+    assert set(got) == set(label)
+    for key in label:
+        assert np.array_equal(got[key], label[key])
+    E = oenc.Encoder(ecfg, w)
+    rng = np.random.default_rng(9)
+    for key, ids, lens in wl:
+        T = texts_of(ids, lens)
+        rows = range(len(lens)) if enc == "toy" else sorted({0, len(lens) - 1, *rng.integers(0, len(lens), size=3).tolist()})
+        rows = list(rows)
+        if rows:
+            compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))

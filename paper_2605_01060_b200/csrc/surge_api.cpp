@@ -304,33 +304,6 @@ namespace {
     }                                                                                             \
   } while (0)
 
-bool ensure_pinned(PinnedBuf& b, size_t bytes) {
-  if (b.cap >= bytes) return true;
-  size_t ncap = std::max(bytes, b.cap * 2);
-  ncap = std::max<size_t>(ncap, 1 << 20);
-  void* p = nullptr;
-  if (cudaHostAlloc(&p, ncap, cudaHostAllocPortable) != cudaSuccess) return false;
-  if (b.p) cudaFreeHost(b.p);
-  b.p = p;
-  b.cap = ncap;
-  return true;
-}
-
-bool ensure_pinned_keep(PinnedBuf& b, size_t bytes, size_t keep) {
-  if (b.cap >= bytes) return true;
-  size_t ncap = std::max(bytes, b.cap * 2);
-  ncap = std::max<size_t>(ncap, 1 << 20);
-  void* p = nullptr;
-  if (cudaHostAlloc(&p, ncap, cudaHostAllocPortable) != cudaSuccess) return false;
-  if (b.p) {
-    std::memcpy(p, b.p, keep);
-    cudaFreeHost(b.p);
-  }
-  b.p = p;
-  b.cap = ncap;
-  return true;
-}
-
 template <typename T>
 cudaError_t ensure_dev(T** p, size_t& cap, size_t n) {
   if (cap >= n && *p) return cudaSuccess;
@@ -341,6 +314,37 @@ cudaError_t ensure_dev(T** p, size_t& cap, size_t n) {
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), ncap * sizeof(T));
   cap = e == cudaSuccess ? ncap : 0;
   return e;
+}
+
+// Pinned buffers are never freed on the hot path (cudaFreeHost can stall the submitting thread
+// behind the device's queued work, and page-locking is slow): a buffer that must grow is replaced by
+// the best-fitting pooled buffer or a fresh allocation (25% headroom), and the old one returns to the
+// pool.  `mu` guards the pool (the CUDA callback and surge_release push into it).
+bool grow_pinned(PinnedBuf& b, size_t bytes, size_t keep, std::vector<PinnedBuf>& pool, std::mutex& mu) {
+  if (b.cap >= bytes && b.p) return true;
+  PinnedBuf nb{};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    int best = -1;
+    for (int i = 0; i < int(pool.size()); ++i)
+      if (pool[i].cap >= bytes && (best < 0 || pool[i].cap < pool[best].cap)) best = i;
+    if (best >= 0) {
+      nb = pool[best];
+      pool.erase(pool.begin() + best);
+    }
+  }
+  if (!nb.p) {
+    const size_t cap = std::max<size_t>(bytes + bytes / 4, size_t(1) << 20);
+    if (cudaHostAlloc(&nb.p, cap, cudaHostAllocPortable) != cudaSuccess) return false;
+    nb.cap = cap;
+  }
+  if (b.p) {
+    if (keep) std::memcpy(nb.p, b.p, keep);
+    std::lock_guard<std::mutex> g(mu);
+    pool.push_back(b);
+  }
+  b = nb;
+  return true;
 }
 
 PinnedBuf take_from_pool(std::vector<PinnedBuf>& pool, size_t bytes) {
@@ -557,7 +561,7 @@ int seal(Ctx* c, int reason) {
   sb->n_tokens = c->total_tokens;
   // append lengths after the ids in the staging buffer (ids occupy [0, n_tokens))
   const size_t need = size_t(sb->n_tokens + sb->n_texts) * 4;
-  if (!ensure_pinned_keep(c->stage, need, size_t(sb->n_tokens) * 4)) {
+  if (!grow_pinned(c->stage, need, size_t(sb->n_tokens) * 4, c->stage_pool, c->mu)) {
     c->set_error(SURGE_E_OOM, "pinned staging allocation of %zu bytes failed", need);
     return SURGE_E_OOM;
   }
@@ -584,9 +588,10 @@ int seal(Ctx* c, int reason) {
   {
     std::lock_guard<std::mutex> g(c->mu);
     sb->index = int64_t(c->sbs.size());
-    sb->out = take_from_pool(c->out_pool, size_t(sb->local_texts) * c->shape.d * c->model.out_elem_bytes());
+    sb->out = PinnedBuf{};
   }
-  if (!ensure_pinned(sb->out, size_t(std::max<int64_t>(sb->local_texts, 1)) * c->shape.d * c->model.out_elem_bytes())) {
+  if (!grow_pinned(sb->out, size_t(std::max<int64_t>(sb->local_texts, 1)) * c->shape.d * c->model.out_elem_bytes(), 0,
+                   c->out_pool, c->mu)) {
     c->set_error(SURGE_E_OOM, "pinned output allocation failed");
     return SURGE_E_OOM;
   }
@@ -823,7 +828,7 @@ surge_status surge_submit_partition(surge_handle h, uint64_t partition_id, const
     while (tok_row < step.row0) tok_at += lengths[tok_row++];
     int64_t pt = 0;
     for (int64_t i = step.row0; i < step.row0 + step.rows; ++i) pt += lengths[i];
-    if (!ensure_pinned_keep(c->stage, size_t(c->total_tokens + pt) * 4, size_t(c->total_tokens) * 4)) {
+    if (!grow_pinned(c->stage, size_t(c->total_tokens + pt) * 4, size_t(c->total_tokens) * 4, c->stage_pool, c->mu)) {
       c->set_error(SURGE_E_OOM, "pinned staging allocation failed");
       return SURGE_E_OOM;
     }

@@ -73,7 +73,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if jobs or not os.path.exists(OUT) or force:
-        run([cc, *ARCH, "-shared", "-o", OUT, *objs, "-lpthread", "-ldl"])
+        run([cc, *ARCH, "-shared", "-o", OUT, *objs, "-lpthread", "-ldl",
+             *os.environ.get("NVCC_LINK_EXTRA", "").split()])   # e.g. the TSAN runtime (scripts/sanitize.sh)
     return OUT
 
 

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>   // types and prototypes only: libnccl.so.2 is opened at run time (nccl_api())
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a profiler is attached
 
 #include <algorithm>
 #include <atomic>
@@ -38,6 +39,13 @@ struct Ctx;
 namespace {
 
 constexpr int REASON_EFFICIENCY = 0, REASON_SAFETY = 1, REASON_END = 2;
+
+// NVTX range for the host runtime's timeline (nsys / ncu --nvtx): seal (Flush), per-SuperBatch
+// enqueue on the worker, per-chunk encode.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Alg.1 AddPartition decision after `total += n`: Safety first, then Efficiency.
 inline int alg1_decide(int64_t total, int64_t b_min, int64_t b_max) {
@@ -396,6 +404,7 @@ void CUDART_CB on_chunk_done(void* arg) {
 
 // Encode one sealed SuperBatch on the worker thread (asynchronously enqueued on the streams).
 int process_superbatch(Ctx* c, SuperBatch* sb) {
+  NvtxRange nvtx_sb("surge.superbatch");
   const int d = c->shape.d;
   if (sb->local_texts == 0) {
     std::lock_guard<std::mutex> g(c->mu);
@@ -487,6 +496,7 @@ int process_superbatch(Ctx* c, SuperBatch* sb) {
   while (s0 < LS) {
     int64_t s1 = s0 + 1;
     while (s1 < LS && int64_t(host_cu[s1 + 1]) - host_cu[s0] <= cap) ++s1;
+    NvtxRange nvtx_chunk("surge.chunk");
     const int b = int(c->chunk_counter++ & 1);
     CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->s_comp, c->e_free[b], 0));
     int64_t nl = 0;
@@ -548,6 +558,7 @@ void worker_main(Ctx* c) {
 
 // Seal the open SuperBatch (Flush) and hand it to the worker.
 int seal(Ctx* c, int reason) {
+  NvtxRange nvtx_seal("surge.seal");
   auto sbp = std::make_unique<SuperBatch>();
   SuperBatch* sb = sbp.get();
   sb->reason = reason;

@@ -11,6 +11,7 @@ are numpy arrays.  torch is used only by callers for device memory and streams.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import os
 
 import numpy as np
@@ -228,11 +229,18 @@ def surge_finish(h):
     return _check(h, lib.surge_finish(h), "surge_finish")
 
 
+_poll_tls = threading.local()
+
+
 def surge_poll_flushed(h, max_items: int = 4096, timeout_ms: int = 0):
-    buf = (surge_flushed * max_items)()
+    """Completed pieces (copies of the records; their data stays library-owned until released).  The
+    record buffer is cached per thread, so a poll costs no allocation proportional to max_items."""
+    buf = getattr(_poll_tls, "buf", None)
+    if buf is None or len(buf) < max_items:
+        buf = _poll_tls.buf = (surge_flushed * max_items)()
     n = C.c_int64()
     _check(h, lib.surge_poll_flushed(h, buf, max_items, timeout_ms, C.byref(n)), "surge_poll_flushed")
-    return [buf[i] for i in range(n.value)]
+    return [surge_flushed.from_buffer_copy(buf[i]) for i in range(n.value)]
 
 
 def flushed_array(rec: surge_flushed) -> np.ndarray:

@@ -8,7 +8,11 @@ r, and reports max over ranks -- the device time bench.py would take at N GPUs, 
 NCCL weight broadcast.  Same workload, timing and warm-up rules as bench.py (CUDA events on the
 launching stream, inputs resident in HBM).
 
-    python scripts/rank_emulation.py [--worlds 1 2 4 8] [--steps 2] [--warmup 1]
+    python scripts/rank_emulation.py [--worlds 1 2 4 8] [--steps 2] [--warmup 1] [--e2e]
+
+--e2e adds the end-to-end number of every rank: the streaming C ABI from host memory (every rank
+submits the WHOLE partition stream -- Alg.1 runs on every rank -- and encodes, copies back, polls and
+releases only its own LPT pieces), wall clock per rank, job value = N texts / max over ranks.
 """
 from __future__ import annotations
 
@@ -36,12 +40,37 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--n-texts", type=int, default=0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--e2e", action="store_true")
     args = ap.parse_args()
+
     dev = torch.device("cuda", 0)
     ecfg, wcfg = ENCODERS["minilm"], WORKLOADS["minilm"]
     if args.n_texts:
         wcfg = scaled(wcfg, n_texts=args.n_texts)
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=0)
+    parts = [wl.partition(k) for k in range(len(wl.sizes))]
+
+    def run_stream(h):
+        n_rows = 0
+        t0 = time.perf_counter()
+        for key, ids, lens in parts:
+            N.surge_submit_partition(h, key, ids, lens)
+            for r in N.surge_poll_flushed(h, 4096, 0):
+                n_rows += r.n_rows
+                N.surge_release(h, r)
+        t_sub = time.perf_counter() - t0
+        N.surge_finish(h)
+        while N.surge_pending(h) > 0:
+            for r in N.surge_poll_flushed(h, 4096, 20):
+                n_rows += r.n_rows
+                N.surge_release(h, r)
+        for r in N.surge_poll_flushed(h, 4096, 0):
+            n_rows += r.n_rows
+            N.surge_release(h, r)
+        wall = time.perf_counter() - t0
+        st = N.surge_get_stats(h)
+        N.surge_reset(h)
+        return wall, t_sub, n_rows, st
     blob = torch.from_numpy(pack_blob(ecfg, make_weights(ecfg, seed=1234)).view(np.uint8)).to(dev)
     sizes = wl.sizes.astype(np.int64)
     d_ids = torch.from_numpy(wl.ids).to(dev)
@@ -79,7 +108,12 @@ def main():
             st1 = N.surge_get_stats(h)
             ms = e0.elapsed_time(e1) / args.steps
             launches = (st1["kernel_launches"] - st0["kernel_launches"]) // args.steps
-            per_rank.append({"rank": rank, "ms_per_step": ms, "launches_per_step": int(launches)})
+            rec = {"rank": rank, "ms_per_step": ms, "launches_per_step": int(launches)}
+            if args.e2e:
+                run_stream(h)                                  # warm-up (pinned pools)
+                wall, t_sub, n_rows, st = run_stream(h)
+                rec.update(e2e_s=wall, e2e_submit_s=t_sub, e2e_rows=n_rows, e2e_ttfo_s=st["ttfo_s"])
+            per_rank.append(rec)
             N.surge_destroy(h)
         ms_max = max(r["ms_per_step"] for r in per_rank)
         ms_min = min(r["ms_per_step"] for r in per_rank)
@@ -89,6 +123,12 @@ def main():
         row = {"n_gpus": world, "ms_per_step_max": ms_max, "ms_per_step_min": ms_min,
                "texts_per_s": value, "efficiency_vs_1": value / (base * world) if base else None,
                "ranks": per_rank}
+        if args.e2e:
+            e2e_max = max(r["e2e_s"] for r in per_rank)
+            assert sum(r["e2e_rows"] for r in per_rank) == wl.n_texts
+            row.update(e2e_s_max=e2e_max, e2e_texts_per_s=wl.n_texts / e2e_max,
+                       e2e_over_device=(wl.n_texts / e2e_max) / value,
+                       e2e_submit_s_max=max(r["e2e_submit_s"] for r in per_rank))
         rows.append(row)
         print(json.dumps({k: v for k, v in row.items() if k != "ranks"}), flush=True)
     out = {"workload": f"minilm: N={wl.n_texts} texts, P={len(sizes)} sigma=1.72, B_min={wcfg.b_min}",

@@ -468,26 +468,16 @@ def ncu_traffic(kernel: str):
 
 
 def run_e2e(N, h, wl, args, world, rank, dev):
-    """Streaming C ABI from host memory: submit every partition, poll + release, finish, drain."""
+    """The public streaming path (driver.stream over the C ABI) from host memory: every partition
+    submitted in arrival order, pieces polled and released on a second thread, finish, drain."""
     import torch
     h_dim = ENCODERS[args.encoder].hidden
     parts = [wl.partition(k) for k in range(len(wl.sizes))]
 
+    from paper_2605_01060_b200.driver import stream
+
     def one():
-        n_rows = 0
-        for key, ids, lens in parts:
-            N.surge_submit_partition(h, key, ids, lens)
-            for r in N.surge_poll_flushed(h, 4096, 0):
-                n_rows += r.n_rows
-                N.surge_release(h, r)
-        N.surge_finish(h)
-        while N.surge_pending(h) > 0:
-            for r in N.surge_poll_flushed(h, 4096, 20):
-                n_rows += r.n_rows
-                N.surge_release(h, r)
-        for r in N.surge_poll_flushed(h, 4096, 0):
-            n_rows += r.n_rows
-            N.surge_release(h, r)
+        n_rows = stream(N, h, parts)        # submit on this thread, poll + release on a second one
         st = N.surge_get_stats(h)
         N.surge_reset(h)
         return n_rows, st

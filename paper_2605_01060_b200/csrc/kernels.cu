@@ -9,6 +9,7 @@
 #include "internal.h"
 
 #include <climits>
+#include <type_traits>
 
 namespace surge {
 
@@ -190,52 +191,65 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict
       ty[i][0] = bf16lo(tt.x); ty[i][1] = bf16hi(tt.x); ty[i][2] = bf16lo(tt.y); ty[i][3] = bf16hi(tt.y);
     }
   }
-  for (int32_t t = a; t < b; ++t) {
-    const int32_t id = ids[t];
-    const uint2* wr = reinterpret_cast<const uint2*>(word + size_t(id) * D);
-    const uint2* pr = reinterpret_cast<const uint2*>(pos + size_t(t - a) * D);
-    float v[PER][4];
-    float s = 0.f;
+  // NT tokens of the text at a time: independent gather -> reduce -> store chains interleave (the
+  // per-token chain is latency-bound: two L2 gathers, then two dependent warp reductions)
+  auto tokens = [&](auto nt_tag, int32_t t) {
+    constexpr int NT = decltype(nt_tag)::value;
+    float v[NT][PER][4];
+    float s[NT];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int g = lane + 32 * i;
-      if (g < G) {
-        const uint2 w2 = __ldg(wr + g), p2 = __ldg(pr + g);
-        v[i][0] = bf16lo(w2.x) + bf16lo(p2.x) + ty[i][0];
-        v[i][1] = bf16hi(w2.x) + bf16hi(p2.x) + ty[i][1];
-        v[i][2] = bf16lo(w2.y) + bf16lo(p2.y) + ty[i][2];
-        v[i][3] = bf16hi(w2.y) + bf16hi(p2.y) + ty[i][3];
-        s += v[i][0] + v[i][1] + v[i][2] + v[i][3];
-      } else {
-        v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
-      }
-    }
-    const float mean = warp_sum(s) * (1.0f / D);
-    float q = 0.f;
+    for (int u = 0; u < NT; ++u) {
+      const int32_t id = ids[t + u];
+      const uint2* wr = reinterpret_cast<const uint2*>(word + size_t(id) * D);
+      const uint2* pr = reinterpret_cast<const uint2*>(pos + size_t(t + u - a) * D);
+      s[u] = 0.f;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int g = lane + 32 * i;
-      if (g < G) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float dv = v[i][k] - mean;
-          q += dv * dv;
+      for (int i = 0; i < PER; ++i) {
+        const int g = lane + 32 * i;
+        if (g < G) {
+          const uint2 w2 = __ldg(wr + g), p2 = __ldg(pr + g);
+          v[u][i][0] = bf16lo(w2.x) + bf16lo(p2.x) + ty[i][0];
+          v[u][i][1] = bf16hi(w2.x) + bf16hi(p2.x) + ty[i][1];
+          v[u][i][2] = bf16lo(w2.y) + bf16lo(p2.y) + ty[i][2];
+          v[u][i][3] = bf16hi(w2.y) + bf16hi(p2.y) + ty[i][3];
+          s[u] += v[u][i][0] + v[u][i][1] + v[u][i][2] + v[u][i][3];
+        } else {
+          v[u][i][0] = v[u][i][1] = v[u][i][2] = v[u][i][3] = 0.f;
         }
       }
     }
-    const float rstd = rsqrtf(warp_sum(q) * (1.0f / D) + eps);
-    uint2* xr = reinterpret_cast<uint2*>(x + size_t(t - tok0) * D);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int g = lane + 32 * i;
-      if (g < G) {
-        float y[4];
+    for (int u = 0; u < NT; ++u) {
+      const float mean = warp_sum(s[u]) * (1.0f / D);
+      float q = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) y[k] = (v[i][k] - mean) * rstd * g4[i][k] + b4[i][k];
-        xr[g] = make_uint2(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]));
+      for (int i = 0; i < PER; ++i) {
+        const int g = lane + 32 * i;
+        if (g < G) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float dv = v[u][i][k] - mean;
+            q += dv * dv;
+          }
+        }
+      }
+      const float rstd = rsqrtf(warp_sum(q) * (1.0f / D) + eps);
+      uint2* xr = reinterpret_cast<uint2*>(x + size_t(t + u - tok0) * D);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int g = lane + 32 * i;
+        if (g < G) {
+          float y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) y[k] = (v[u][i][k] - mean) * rstd * g4[i][k] + b4[i][k];
+          xr[g] = make_uint2(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]));
+        }
       }
     }
-  }
+  };
+  int32_t t = a;
+  for (; t + 2 <= b; t += 2) tokens(std::integral_constant<int, 2>{}, t);
+  if (t < b) tokens(std::integral_constant<int, 1>{}, t);
 }
 
 // ------------------------------------------------------------------------- K5 varlen attention

@@ -65,3 +65,48 @@ class SurgeEncoder:
         st = self.stats()
         return [dict(N.surge_get_superbatch(self.h, i), members=N.surge_get_superbatch_members(self.h, i))
                 for i in range(st["superbatches"])]
+
+
+def stream(N, h, partitions, consume=None, poll_batch: int = 4096) -> int:
+    """Submit (key, ids, lengths) in arrival order on this thread while a second thread polls and
+    releases the completed pieces (the threading model of include/surge.h: one producer; poll /
+    release from any thread).  A submit that blocks on backpressure -- or on a long run of Safety
+    flushes under SURGE_BMAX_SPLIT -- therefore never holds back the release of finished pieces, so
+    their pinned buffers return to the pool instead of new ones being page-locked.  `consume(rec)`
+    (optional) sees every piece before it is released.  Returns the number of rows delivered."""
+    import threading
+    done = threading.Event()
+    rows = [0]
+    err = []
+
+    def poller():
+        try:
+            while True:
+                recs = N.surge_poll_flushed(h, poll_batch, 5)
+                for r in recs:
+                    rows[0] += int(r.n_rows)
+                    if consume is not None:
+                        consume(r)
+                    N.surge_release(h, r)
+                if not recs and done.is_set() and N.surge_pending(h) == 0:
+                    for r in N.surge_poll_flushed(h, poll_batch, 0):
+                        rows[0] += int(r.n_rows)
+                        if consume is not None:
+                            consume(r)
+                        N.surge_release(h, r)
+                    return
+        except BaseException as e:   # noqa: BLE001 -- re-raised on the submitting thread
+            err.append(e)
+
+    t = threading.Thread(target=poller, daemon=True)
+    t.start()
+    try:
+        for key, ids, lengths in partitions:
+            N.surge_submit_partition(h, key, ids, lengths)
+        N.surge_finish(h)
+    finally:
+        done.set()
+        t.join()
+    if err:
+        raise err[0]
+    return rows[0]

@@ -31,6 +31,7 @@ def one(sigma: str, policy: str, n_texts: int, n_partitions: int) -> dict:
     from dataclasses import replace
 
     from paper_2605_01060_b200 import native as N
+    from paper_2605_01060_b200.driver import stream
     from synth.configs import ENCODERS, WORKLOADS
     from synth.weights import make_weights, pack_blob
     from synth.workload import make_workload
@@ -52,34 +53,12 @@ def one(sigma: str, policy: str, n_texts: int, n_partitions: int) -> dict:
     try:
         # warm-up on a prefix (kernels, pinned pools for the common SuperBatch sizes)
         k_warm = int(np.searchsorted(np.cumsum(wl.sizes), 2_000_000)) + 1
-        n_rows = 0
-        for key, ids, lens in parts[:k_warm]:
-            N.surge_submit_partition(h, key, ids, lens)
-            for r in N.surge_poll_flushed(h, 4096, 0):
-                N.surge_release(h, r)
-        N.surge_finish(h)
-        while N.surge_pending(h) > 0:
-            for r in N.surge_poll_flushed(h, 4096, 20):
-                N.surge_release(h, r)
-        for r in N.surge_poll_flushed(h, 4096, 0):
-            N.surge_release(h, r)
+        stream(N, h, parts[:k_warm])
         N.surge_reset(h)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for key, ids, lens in parts:
-            N.surge_submit_partition(h, key, ids, lens)
-            for r in N.surge_poll_flushed(h, 4096, 0):
-                n_rows += r.n_rows
-                N.surge_release(h, r)
+        n_rows = stream(N, h, parts)              # submit here, poll + release on a second thread
         t_submit = time.perf_counter() - t0
-        N.surge_finish(h)
-        while N.surge_pending(h) > 0:
-            for r in N.surge_poll_flushed(h, 4096, 20):
-                n_rows += r.n_rows
-                N.surge_release(h, r)
-        for r in N.surge_poll_flushed(h, 4096, 0):
-            n_rows += r.n_rows
-            N.surge_release(h, r)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         st = N.surge_get_stats(h)

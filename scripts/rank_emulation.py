@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import time
 import os
 import sys
 
@@ -50,29 +51,16 @@ def main():
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=0)
     parts = [wl.partition(k) for k in range(len(wl.sizes))]
 
+    from paper_2605_01060_b200.driver import stream
+
     def run_stream(h):
-        n_rows = 0
         t0 = time.perf_counter()
-        for key, ids, lens in parts:
-            N.surge_submit_partition(h, key, ids, lens)
-            for r in N.surge_poll_flushed(h, 4096, 0):
-                n_rows += r.n_rows
-                N.surge_release(h, r)
-        t_sub = time.perf_counter() - t0
-        N.surge_finish(h)
-        while N.surge_pending(h) > 0:
-            for r in N.surge_poll_flushed(h, 4096, 20):
-                n_rows += r.n_rows
-                N.surge_release(h, r)
-        for r in N.surge_poll_flushed(h, 4096, 0):
-            n_rows += r.n_rows
-            N.surge_release(h, r)
+        n_rows = stream(N, h, parts)          # submit on this thread, poll + release on a second one
         wall = time.perf_counter() - t0
         st = N.surge_get_stats(h)
         N.surge_reset(h)
-        return wall, t_sub, n_rows, st
-    blob = torch.from_numpy(pack_blob(ecfg, make_weights(ecfg, seed=1234)).view(np.uint8)).to(dev)
-    sizes = wl.sizes.astype(np.int64)
+        return wall, wall, n_rows, st
+
     d_ids = torch.from_numpy(wl.ids).to(dev)
     d_len = torch.from_numpy(wl.lengths).to(dev)
     d_out = torch.empty(wl.n_texts, ecfg.hidden, dtype=torch.float32, device=dev)

@@ -161,17 +161,20 @@ __device__ __forceinline__ void attn_key_block(uint32_t k_addr, uint32_t v_addr,
 // operation sequence is the single-head one, so results do not depend on NH):
 //   sQt : the tile's first query row at head 0's columns; sK / sV : the text's first key row at
 //   head 0's columns; head h is DH columns further right in each; len = text length,
-//   nt = ceil(len / 16) key blocks.
+//   nt = ceil(len / 16) key blocks; q_rows = query rows of the tile inside the text; sZ = a zero row
+//   (same column base) read instead of the rows past the text, which may belong to the next text
+//   whose O another warp is writing over its Q (their values would only reach discarded rows).
 // Returns the unnormalised accumulators o[h] (mma C-fragment layout: row g = lane / 4 in
 // o[h][n][0..1], row g + 8 in o[h][n][2..3], columns 8 n + 2 (lane % 4) + {0, 1}) and the
 // reciprocal row sums ia[h] (row g), ib[h] (row g + 8): O = o * i.
 template <int DH, int LDS, int NH>
 __device__ __forceinline__ void attn_query_tile(const uint16_t* sQt, const uint16_t* sK, const uint16_t* sV,
                                                 int len, int nt, float qscale, int lane, float (&o)[NH][DH / 8][4],
-                                                float (&ia)[NH], float (&ib)[NH]) {
+                                                float (&ia)[NH], float (&ib)[NH], int q_rows, const uint16_t* sZ) {
   const int c4 = lane & 3;
   uint32_t qa[NH][DH / 16][4];
-  const uint32_t q_addr = smem_u32(sQt + ((lane & 7) + ((lane >> 3) & 1) * 8) * LDS + (lane >> 4) * 8);
+  const int qr = (lane & 7) + ((lane >> 3) & 1) * 8;
+  const uint32_t q_addr = smem_u32((qr < q_rows ? sQt + qr * LDS : sZ) + (lane >> 4) * 8);
 #pragma unroll
   for (int h = 0; h < NH; ++h)
 #pragma unroll

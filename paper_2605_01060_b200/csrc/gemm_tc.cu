@@ -51,7 +51,10 @@ struct TileCfg {
   static constexpr bool ATT = EPI == EPI_QKV_ATTN;
   // attention epilogue: 16 warps at d_h = 32 (MiniLM; 12 -> 16 warps: QKV+attention 1138 -> 1128
   // ms/step), 12 elsewhere (their attention registers spill at the 96-register cap of 16 warps)
-  static constexpr int SPLIT = ATT ? (DH == 32 ? 4 : 3)
+#ifndef ATT_SPLIT32
+#define ATT_SPLIT32 4
+#endif
+  static constexpr int SPLIT = ATT ? (DH == 32 ? ATT_SPLIT32 : 3)
                                : EPI != EPI_BIAS_GELU ? 2 : BN % 128 == 0 ? 4 : BN % 96 == 0 ? 3 : 2;
   static constexpr int EPI_WARPS = 4 * SPLIT;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
           float o[NHU][DH / 8][4];
           float ia[NHU], ib[NHU];
           attn_query_tile<DH, LDS, NHU>(sQt, sAtt + ta * LDS + (HG + h0) * DH, sAtt + ta * LDS + (2 * HG + h0) * DH,
-                                        len, nt, att.qscale, lane, o, ia, ib);
+                                        len, nt, att.qscale, lane, o, ia, ib, len - 16 * qt, sAtt + BM * LDS + h0 * DH);
           __syncwarp();   // every lane has read its Q fragments before O overwrites the tile
           attn_store_tile<DH, NHU>(sQt, LDS, qt, len, lane, o, ia, ib);
         }

@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
       uint16_t* sQt = sQ + (ta + 16 * qt) * LDS;
       float o[HG][DH / 8][4];
       float ia[HG], ib[HG];
-      attn_query_tile<DH, LDS, HG>(sQt, sK + ta * LDS, sV + ta * LDS, len, nt, qscale, lane, o, ia, ib);
+      attn_query_tile<DH, LDS, HG>(sQt, sK + ta * LDS, sV + ta * LDS, len, nt, qscale, lane, o, ia, ib, len - 16 * qt,
+                                   sQ + nr * LDS);
       __syncwarp();   // every lane has read its Q fragments before O overwrites the tile
       attn_store_tile<DH, HG>(sQt, LDS, qt, len, lane, o, ia, ib);
     }
@@ -553,7 +554,8 @@ __global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel
     if (16 * qt < len) {
       float o[1][DH / 8][4];
       float ia[1], ib[1];
-      attn_query_tile<DH, LDS, 1>(sQ + 16 * warp * LDS, sK, sV, len, nt, qscale, lane, o, ia, ib);
+      attn_query_tile<DH, LDS, 1>(sQ + 16 * warp * LDS, sK, sV, len, nt, qscale, lane, o, ia, ib, nq - 16 * warp,
+                                  sQ + A::QROWS * LDS);
       attn_store_tile<DH, 1>(out + size_t(a + 16 * qt) * d + h * DH, size_t(d), qt, len, lane, o, ia, ib);
     }
     __syncthreads();                             // sQ reused by the next query block

@@ -61,6 +61,8 @@ def main():
         N.surge_reset(h)
         return wall, wall, n_rows, st
 
+    blob = torch.from_numpy(pack_blob(ecfg, make_weights(ecfg, seed=1234)).view(np.uint8)).to(dev)
+    sizes = wl.sizes.astype(np.int64)
     d_ids = torch.from_numpy(wl.ids).to(dev)
     d_len = torch.from_numpy(wl.lengths).to(dev)
     d_out = torch.empty(wl.n_texts, ecfg.hidden, dtype=torch.float32, device=dev)

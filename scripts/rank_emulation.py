@@ -51,11 +51,11 @@ def main():
     wl = make_workload(wcfg, ecfg.vocab_size, ecfg.max_position, seed=0)
     parts = [wl.partition(k) for k in range(len(wl.sizes))]
 
-    from paper_2605_01060_b200.driver import stream
+    from paper_2605_01060_b200.driver import stream as drive_stream
 
     def run_stream(h):
         t0 = time.perf_counter()
-        n_rows = stream(N, h, parts)          # submit on this thread, poll + release on a second one
+        n_rows = drive_stream(N, h, parts)    # submit on this thread, poll + release on a second one
         wall = time.perf_counter() - t0
         st = N.surge_get_stats(h)
         N.surge_reset(h)

@@ -389,6 +389,12 @@ typedef struct {
 #define SURGE_OPT_POOLING 4
 #define SURGE_POOL_MEAN 0
 #define SURGE_POOL_CLS 1
+/*   SURGE_OPT_ATT_TC (default 0; effective with SURGE_OPT_ATT_FUSED, hidden size 384, d_h = 32): the
+ *     fused QKV + attention kernel computes S = Q K^T and O = P V on the tcgen05 tensor cores (Q and
+ *     P read from tensor memory; one CTA per SM); 0 = the CTA-pair kernel whose attention runs on
+ *     mma.sync in the GEMM epilogue.  Same bf16 Q/K/V/P values and softmax formula; the fp32
+ *     accumulation order differs, so the two agree to rounding (not bit for bit). */
+#define SURGE_OPT_ATT_TC 5
 surge_status surge_set_option(surge_handle h, int32_t option, int64_t value);
 
 surge_status surge_profile_enable(surge_handle h, int32_t on);   /* on: clears counters */

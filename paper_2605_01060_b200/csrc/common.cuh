@@ -130,7 +130,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef MBAR_SLEEP_ALL
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity);
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_sleep(bar, parity); }
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#endif
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -138,6 +144,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n}" ::"r"(addr),
       "r"(parity)
+      : "memory");
+}
+
+// Wait with a suspend-time hint: the thread sleeps until the phase completes (or ~hint ns) instead of
+// re-polling, so waiting warps do not take issue slots from the working warps of their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(addr),
+      "r"(parity), "r"(1000000)
       : "memory");
 }
 

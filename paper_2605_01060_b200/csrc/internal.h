@@ -78,6 +78,11 @@ int gemm_bn_for(int N, int K, int epi);
 bool gemm_use_pair(int N, int K, int epi);
 uint32_t gemm_b_box_rows(int N, int K, int epi);   // TMA box rows of the B (weight) tensor map
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);
+// K4 + K5 with the attention on tcgen05 (qkv_attn_tc.cu): one CTA per SM, S = Q K^T and O = P V as
+// tensor-core MMAs with Q and P read from TMEM.  d = 384, d_h = 32 (MiniLM class); same arguments as
+// the EPI_QKV_ATTN GEMM (text-aligned tile records, permuted W_qkv with 96-row TMA boxes).
+bool qkv_attn_tc_supported(int d, int heads);
+cudaError_t launch_qkv_attn_tc(const GemmArgs& g, cudaStream_t st);
 // LN GEMMs fuse the LayerNorm into the epilogue when the full row fits one CTA's TMEM (d in {64, 384});
 // otherwise they write fp32 pre-LN rows (EPI_BIAS_RES) and launch_layernorm finishes them.
 inline bool fused_ln(int d) { return d == 64 || d == 384; }
@@ -233,6 +238,7 @@ class DeviceModel {
   const float* emb_b() const { return emb_b_; }
   // fused QKV + attention kernel on/off (on by default; off = separate K4 GEMM + K5 kernels)
   void set_att_fused(bool on) { att_fused_ = on; }
+  void set_att_tc(bool on) { att_tc_ = on; }
   bool att_fused() const { return att_fused_; }
   // fused MLP kernel on/off (on by default; off = separate K7 GELU GEMM + K8 LN GEMM)
   void set_mlp_fused(bool on) { mlp_fused_ = on; }
@@ -247,6 +253,7 @@ class DeviceModel {
  private:
   ModelShape s_{};
   bool att_fused_ = true;
+  bool att_tc_ = false;       // fused QKV + attention on tcgen05 where supported (qkv_attn_tc.cu)
   bool mlp_fused_ = true;
   bool tail_fused_ = true;
   int pooling_ = 0;

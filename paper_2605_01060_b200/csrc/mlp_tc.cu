@@ -40,6 +40,9 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 #ifndef MLP_A_SPLIT
 #define MLP_A_SPLIT 1               // A-tile boxes issued by all three producers (0: producer 0 alone)
 #endif
+#ifndef MLP_PINGPONG
+#define MLP_PINGPONG 0              // 1: A tile and weight ring swap shared-memory regions every unit (measured neutral)
+#endif
 #ifndef MLP_PREFETCH
 #define MLP_PREFETCH 0              // L2 prefetch of the next unit's A rows (measured: no effect)
 #endif
@@ -70,7 +73,12 @@ struct MlpCfg {
   static constexpr int LN_STG = EPI_WARPS * MLP_STG * 2048;
   static constexpr int LN_SCRATCH = ((LN_STG + NP * MBM * 16 + 3 * D * 4 + 1023) / 1024) * 1024;
   static constexpr int SCRATCH = LN_SCRATCH > HS_BYTES ? LN_SCRATCH : HS_BYTES;
-  static constexpr int SMEM = 1024 + HEAD + A_BYTES + SCRATCH + RING * STAGE;
+  // MLP_PINGPONG: two equal regions that alternate between the A tile and the weight ring, unit by
+  // unit, so the next unit's A tile loads into the drained ring region as soon as the last MMA of
+  // the unit retires (instead of after the final LN has read its residual from the A tile)
+  static constexpr int REGION = MLP_PINGPONG ? (A_BYTES > RING * STAGE ? A_BYTES : RING * STAGE) : 0;
+  static constexpr int SMEM = MLP_PINGPONG ? 1024 + HEAD + 2 * REGION + SCRATCH
+                                           : 1024 + HEAD + A_BYTES + SCRATCH + RING * STAGE;
   static_assert(SMEM <= 227 * 1024, "shared memory");
   static_assert(D % 64 == 0 && D <= 384, "Y must fit TMEM next to the H chunk");
   static_assert(KB1 % 3 == 0 || KB1 == 1, "W1 k-blocks pack 3 per stage");
@@ -146,13 +154,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A
   uint64_t* xres_full = x1_ready + 1;                         // local (OP): X residual rows landed in A
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xres_full + 1);
-  uint8_t* sA = smem + T::HEAD;                              // [KB1][128 x 128 B]
-  uint8_t* sHs = sA + T::A_BYTES;                            // [2][128 x 128 B]
+  uint8_t* const sR0 = smem + T::HEAD;                       // [KB1][128 x 128 B] (PINGPONG: region 0)
+  uint8_t* sHs = sR0 + (MLP_PINGPONG ? T::REGION : T::A_BYTES);   // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
   float* s_b2 = reinterpret_cast<float*>(stats + NP * MBM);  // LN only
   float* s_gamma = s_b2 + D;
   float* s_beta = s_gamma + D;
-  uint8_t* sW = sHs + T::SCRATCH;                            // [RING][STAGE]
+  uint8_t* const sR1 = sHs + T::SCRATCH;                     // [RING][STAGE] (PINGPONG: region 1)
+  // unit ui: A tile in region ui % 2, weight ring in the other (fixed roles without PINGPONG)
+  auto region_a = [&](int ui) { return (MLP_PINGPONG && (ui & 1)) ? sR1 : sR0; };
+  auto region_w = [&](int ui) { return (MLP_PINGPONG && (ui & 1)) ? sR0 : sR1; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = int(blockIdx.x & 1);
@@ -204,6 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t afull_c = mapa_shared(smem_u32(a_full), 0);
       uint32_t sc = 0;                                   // ring stage counter
       int ui = 0;
+      uint8_t* sW = region_w(0);
+      uint8_t* sA = region_a(0);
       auto ring_w1 = [&](int c) {
         for (int s2 = 0; s2 < S1; ++s2, ++sc) {
           const int s = int(sc % RING);
@@ -246,10 +259,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the leader's a_full before producer 0's arrive.expect_tx: the transiently negative tx-count
       // cannot complete the phase while that arrival is pending.
       auto load_a = [&](int u, int m0) {
-        mbar_wait(a_empty, (ui & 1) ^ 1);       // MMAs done with the previous unit's A
-        mbar_wait(a_free, (ui & 1) ^ 1);        // its LN has read the residual rows
+        if (MLP_PINGPONG) {
+          mbar_wait(y_full, (ui & 1) ^ 1);      // every MMA of the previous unit retired: its ring region is free
+        } else {
+          mbar_wait(a_empty, (ui & 1) ^ 1);     // MMAs done with the previous unit's A
+          mbar_wait(a_free, (ui & 1) ^ 1);      // its LN has read the residual rows
+        }
+#ifdef MLP_NO_ALOAD   // timing experiment only (wrong results): the A tile is not reloaded
+        if (leader && p == 0) mbar_arrive(a_full);
+        if (true) return;
+#endif
         if (leader && p == 0) mbar_arrive_expect_tx(a_full, 2u * T::A_BYTES);
-        for (int kb = (OP && MLP_A_SPLIT) ? p : 0; kb < KB1; kb += (OP && MLP_A_SPLIT) ? 3 : 1)
+        constexpr bool SPLIT_A = (OP || MLP_PINGPONG) && MLP_A_SPLIT;
+        for (int kb = SPLIT_A ? p : 0; kb < KB1; kb += SPLIT_A ? 3 : 1)
           tma_load_2d_pair(sA + kb * MBM * 128, &tmX1, afull_c, kb * 64, m0, l2_policy_evict_first());
         if (p == 0) {
           // warm L2 with the next unit's rows: its A load waits for this unit's LN (residual from A)
@@ -261,6 +283,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       for (int u = unit0; u < n_units; u += units, ++ui) {
         const int m0 = u * 2 * MBM + rank * MBM;
+        sA = region_a(ui);
+        sW = region_w(ui);
+        if (MLP_PINGPONG) {
+          // this unit's ring region is the previous unit's A tile: free once its MMAs are done with it
+          // and its final LN has read the residual rows; the A tile goes first (it needs only y_full)
+          load_a(u, m0);
+          mbar_wait(a_empty, (ui & 1) ^ 1);
+          mbar_wait(a_free, (ui & 1) ^ 1);
+          if constexpr (OP) {
+            ring_wo(0, KB1);
+            if (p == 0) {
+              mbar_wait(y0_full, ui & 1);
+              mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
+              for (int kb = 0; kb < KB1; ++kb)
+                tma_load_2d(sA + kb * MBM * 128, &tmR, xres_full, kb * 64, m0);
+            }
+          }
+          for (int c = 0; c < NCH; ++c) {
+            ring_w1(c);
+            if (c > 0) ring_w2(c - 1);
+          }
+          ring_w2(NCH - 1);
+          continue;
+        }
         // OP: the first RING Wo stages need only ring slots freed by the previous unit's G2, so
         // every producer issues its share of them before it waits for the A tile to be released;
         // the remaining Wo stages need slots that G0 frees, i.e. after A has landed (issuing them
@@ -291,9 +337,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // -------------------------------------------------------------------- MMA issuer (leader)
     constexpr uint32_t idesc1 = umma_idesc_bf16(2 * MBM, FC);
     constexpr uint32_t idesc2 = umma_idesc_bf16(2 * MBM, T::N2);
-    const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
     const uint64_t hs_desc0 = umma_desc_sw128(smem_u32(sHs));
-    const uint64_t w_desc0 = umma_desc_sw128(smem_u32(sW));
+    uint64_t a_desc0 = umma_desc_sw128(smem_u32(region_a(0)));
+    uint64_t w_desc0 = umma_desc_sw128(smem_u32(region_w(0)));
 #ifdef MLP_TRACE
     long long tw[5] = {0, 0, 0, 0, 0};
     const long long t_start = clock64();
@@ -334,6 +380,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       ++gc;
     };
     for (int u = unit0; u < n_units; u += units, ++ui) {
+      a_desc0 = umma_desc_sw128(smem_u32(region_a(ui)));
+      w_desc0 = umma_desc_sw128(smem_u32(region_w(ui)));
       MW(a_full, ui & 1, 3);
       tc_fence_after();
       if constexpr (OP) {
@@ -420,6 +468,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t x1_ready_c = mapa_shared(smem_u32(x1_ready), 0);
     for (int u = unit0; u < n_units; u += units, ++ui) {
       const int m0 = u * 2 * MBM + rank * MBM;
+      uint8_t* const sA = region_a(ui);
       if constexpr (OP) {
         // ---- LN0 epilogue (K6): X1 = LN_a(Y + bo + X) -> bf16 into the A tile (swizzled K-major)
         {
@@ -441,6 +490,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         (void)row;
         const ResidualSmemA rg{sA, row_l, hh * (D / NP)};
         mbar_wait(xres_full, ui & 1);          // X rows in the A tile (G0 is done with O)
+#if defined(MLP_SKIP_LN) && (MLP_SKIP_LN & 1)   // timing experiment only (wrong results)
+        mbar_wait(y0_full, ui & 1);
+        tc_fence_after();
+        if (false)
+#endif
         ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
@@ -529,13 +583,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       // residual X1 = this unit's A tile, still resident (the next unit's A load waits for a_free)
       const ResidualSmemA ra{sA, row_l, hh * (D / NP)};
       uint8_t* stg0 = sHs + (warp - 4) * (MLP_STG * 2048);
+#if defined(MLP_SKIP_LN) && (MLP_SKIP_LN & 2)   // timing experiment only (wrong results)
+      mbar_wait(y_full, ui & 1);
+      tc_fence_after();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_free);
+      if (false)
+#endif
       ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();
                             },
                             [&](const uint32_t (&p)[16], int col) {
+#ifndef MLP_NO_FSTORE   // timing experiment only (wrong results)
                               store_rows_32x32(stg0, p, lane, out, m0 + q * 32, M, D, col);
+#else
+                              if (p[0] == 0x7fffffffu && col < 0) out[0] = 0;
+#endif
                             },
                             [&] {                // residual read for the last time: the A tile may take
                               __syncwarp();      // the next unit's rows while pass 2 runs

@@ -353,7 +353,8 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       g.att_rec = ws.att_rec; g.n_att_tiles = n_tiles;
       g.head_dim = d / s_.heads; g.qscale = 1.4426950408889634f / sqrtf(float(d / s_.heads));
       if (P) prof->begin(st, &ev);
-      SURGE_TRY(launch_gemm(g, st));
+      if (att_tc_ && qkv_attn_tc_supported(d, s_.heads)) SURGE_TRY(launch_qkv_attn_tc(g, st));
+      else SURGE_TRY(launch_gemm(g, st));
       if (P) prof->end(KK_QKV_ATTN, st, ev, 2 * M * 3 * D * D + 4 * D * sum_l2, 2 * (M * D + 3 * D * D + M * D));
       g.att_rec = nullptr; g.n_att_tiles = 0;
       k += 1;

@@ -246,10 +246,11 @@ def test_larger_encoder_classes_sample(N, enc, length_model):
         compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))
 
 
-def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True, tail_fused=True):
+def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True, tail_fused=True, att_tc=True):
     h = N.surge_create(N.make_config(ecfg, 1000, 5000, chunk_tokens=chunk_tokens), pack_blob(ecfg, w))
     try:
         N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, 1 if fused else 0)
+        N.surge_set_option(h, N.SURGE_OPT_ATT_TC, 1 if att_tc else 0)
         N.surge_set_option(h, N.SURGE_OPT_MLP_FUSED, 1 if mlp_fused else 0)
         N.surge_set_option(h, N.SURGE_OPT_TAIL_FUSED, 1 if tail_fused else 0)
         out = torch.zeros(len(lens), ecfg.hidden, device="cuda")
@@ -281,13 +282,34 @@ def test_fused_qkv_attention_matches_separate_path_and_oracle(N, enc):
     max_len = min(128, ecfg.max_position)
     lens = _edge_lengths(rng, 700, max_len)
     ids = rng.integers(4 if enc == "toy" else 1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
-    fused = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096)
+    fused = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096, att_tc=False)
     sep = _packed_encode(N, ecfg, w, lens, ids, False, chunk_tokens=4096)
     assert np.array_equal(fused, sep)
     E = oenc.Encoder(ecfg, w)
     T = texts_of(ids, lens)
     rows = sorted({*range(20), len(lens) - 1, *rng.integers(0, len(lens), size=12).tolist()})
     compare(fused[rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def test_tcgen05_attention_vs_oracle_and_mma_sync_path(N):
+    """K4+K5 with S = Q K^T and O = P V on tcgen05 (qkv_attn_tc.cu; MiniLM class, d_h = 32) on the edge
+    lengths of the text-aligned tiles (1, 15/16/17, 31/32/33, 63/64/65, 127, 128-token texts, one-text
+    tiles, padding tiles) in 4096-token chunks: every row vs the fp64 oracle under the gate, and vs the
+    mma.sync path (same bf16 Q/K/V/P, fp32 accumulation order differs: DESIGN.md reading R21)."""
+    ecfg = ENCODERS["minilm"]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(5)
+    lens = _edge_lengths(rng, 300, 128)
+    ids = rng.integers(1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    tc = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096, att_tc=True)
+    ms = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096, att_tc=False)
+    d = np.abs(tc.astype(np.float64) - ms)
+    print(f"tcgen05 vs mma.sync attention: max|d| {d.max():.3g}, mean|d| {d.mean():.3g}")
+    assert d.max() <= 2e-3 and d.mean() <= 1e-4
+    E = oenc.Encoder(ecfg, w)
+    T = texts_of(ids, lens)
+    c, a = compare(tc, np.stack([E.encode_text(t) for t in T]))
+    print(f"tcgen05 attention vs oracle, {len(T)} rows: min cos {c:.6f}, max|d| {a:.3g}")
 
 
 def test_fused_path_falls_back_for_long_texts(N):

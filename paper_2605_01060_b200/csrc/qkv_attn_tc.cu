@@ -26,11 +26,10 @@
 //
 // Warps: 0, 2, 3 TMA producers (B slice once, the A ring); 1 MMA issuer; 2 also allocates TMEM;
 // 4..15 epilogue, warp w reads TMEM lane quadrant w % 4 (rows 32 (w % 4) ..), part (w - 4) / 4:
-//   part 0: V -> registers -> smem (after PV(t-1) has read the previous V) and the text window [ta, te)
-//   of every row (from the tile's 128-bit start-of-text mask, one coalesced 128-byte load of the
-//   record) -> a shared table;
-//   parts 1, 2: head h = part - 1: staging of Q_h -> TMEM and K_h -> smem, O of tile t-1 (TMEM ->
-//   / rowsum -> global), softmax of tile t.
+//   part 0: Q -> TMEM, K -> smem, and the text window [ta, te) of every row (from the tile's 128-bit
+//   start-of-text mask, one coalesced 128-byte load of the record) -> a shared table;
+//   parts 1, 2: head h = part - 1: V_h -> registers -> smem (after PV(t-1, h) has read the previous
+//   one), O of tile t-1 (TMEM -> / rowsum -> global), softmax of tile t.
 // Numerics vs the mma.sync path (attn_tile.cuh): same bf16 Q/K/V/P values and softmax formula (one
 // max per text: the round-1 path takes one per 32 keys, i.e. the same for texts <= 32 tokens); fp32
 // accumulation order of S, P V and the row sum differs (not bit-identical; reading R21).
@@ -156,9 +155,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* bfull = empty + STAGES;
   uint64_t* tfull = bfull + 1;       // QKV(t) retired (commit)
   uint64_t* tempty = tfull + 1;      // accumulator read by the staging (12 warps)
-  uint64_t* qk_ready = tempty + 1;   // Q in TMEM, K in smem (head warps), row windows in smem (part 0)
-  uint64_t* v_ready = qk_ready + 1;  // V in smem (4 warps: part 0)
-  uint64_t* sfull = v_ready + 1;     // [2] S(t, h) retired (commit)
+  uint64_t* qk_ready = tempty + 1;   // Q in TMEM, K in smem, row windows in smem (4 warps: part 0)
+  uint64_t* v_ready = qk_ready + 1;  // [2] V_h in smem (4 warps: part 1 + h)
+  uint64_t* sfull = v_ready + 2;     // [2] S(t, h) retired (commit)
   uint64_t* pready = sfull + 2;      // [2] P(t, h) in TMEM (4 warps: part 1 + h)
   uint64_t* ofull = pready + 2;      // [2] PV(t, h) retired (commit)
   uint64_t* oempty = ofull + 2;      // [2] O(t, h) read from TMEM (4 warps: part 1 + h)
@@ -187,9 +186,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(bfull, 1);
     mbar_init(tfull, 1);
     mbar_init(tempty, EPI_WARPS);
-    mbar_init(qk_ready, EPI_WARPS);
-    mbar_init(v_ready, 4);
+    mbar_init(qk_ready, 4);
     for (int h = 0; h < 2; ++h) {
+      mbar_init(&v_ready[h], 4);
       mbar_init(&sfull[h], 1);
       mbar_init(&pready[h], 4);
       mbar_init(&ofull[h], 1);
@@ -290,7 +289,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       TL(kb_hi == KB1 ? E_QHI : E_QLO, it + 1);
     };
     auto pv = [&](int j, int h) {        // O(j, h) = P_h V_h
-      if (h == 0) QW(v_ready, j & 1, 0);
+      QW(&v_ready[h], j & 1, 0);
       QW(&pready[h], j & 1, 1);
       TL(h ? E_PV1 : E_PV0, j);
       tc_fence_after();
@@ -361,26 +360,40 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int i = threadIdx.x - 128; i < BN; i += 32 * EPI_WARPS) s_bias[i] = __ldg(bias + n0 + i);
     asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
     if (part == 0) {
-      // ---------------- part 0: V staging and the row windows of the tile
+      // ---------------- part 0: Q -> TMEM (TS operand of S), K -> smem (row = key, [K_h0 | K_h1]) and the
+      // text window [ta, te) of every row of the tile -> wtab
       for (int t = t0; t < n_tiles; t += dt, ++it) {
         const int32_t* R = rec + size_t(t) * ATT_REC_INTS;
         const int nrows = __ldg(R + 1), ntexts = __ldg(R + 2);
         const uint32_t tsw = uint32_t(__ldg(R + 4 + lane));   // start rows of texts 4 lane .. 4 lane + 3
         mbar_wait_sleep(tfull, it & 1);
         TL(E_STG, it);
-        ETR(0);
         tc_fence_after();
-        uint32_t a0[32], a1[32], vv[2][16];
-        tmem_ld32(tl + T_ACC + 2 * HG * DH, a0);
-        tmem_ld32(tl + T_ACC + 2 * HG * DH + DH, a1);
+        uint32_t a0[32], a1[32], pk[16];
+        tmem_ld32(tl + T_ACC, a0);
+        tmem_ld32(tl + T_ACC + DH, a1);
+        tmem_ld_wait_regs(a0);
+        tmem_ld_wait_regs(a1);
+        bias_pack32(a0, bs, pk);
+        tmem_st16(tl + T_Q, pk);
+        bias_pack32(a1, bs + DH, pk);
+        tmem_st16(tl + T_Q + DH / 2, pk);
+        tmem_ld32(tl + T_ACC + HG * DH, a0);
+        tmem_ld32(tl + T_ACC + HG * DH + DH, a1);
         tmem_ld_wait_regs(a0);
         tmem_ld_wait_regs(a1);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);               // (with the head warps) the next QKV may overwrite
+        if (lane == 0) mbar_arrive(tempty);
         TL(E_TE, it);
-        bias_pack32(a0, bs + 2 * HG * DH, vv[0]);
-        bias_pack32(a1, bs + 2 * HG * DH + DH, vv[1]);
+#pragma unroll
+        for (int h = 0; h < HG; ++h) {
+          bias_pack32(h ? a1 : a0, bs + HG * DH + h * DH, pk);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(sK + sw128_off(r, h * DH + 8 * j)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
         // this row's text window [ta, te) from the tile's 128-bit start-of-text mask
         uint32_t m0w = 0u, m1w = 0u, m2w = 0u, m3w = 0u;
 #pragma unroll
@@ -408,31 +421,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           te = te < nrows ? te : nrows;
         }
         wtab[(it & 1) * BM + r] = uint16_t(ta | (te << 8));
+        fence_proxy_async_smem();                         // K (generic writes) -> the S MMA
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(qk_ready);             // releases wtab to the softmax warps
+        if (lane == 0) mbar_arrive(qk_ready);             // also releases wtab to the softmax warps
         TL(E_QKR, it);
         ETR(1);
-        // V of tile t (row = key, [V_h0 | V_h1]: the MN-major B operand of P V), after PV(t-1, h0 / h1)
-        // have read V(t-1)
-        if (it > 0) {
-          mbar_wait_sleep(&ofull[0], (it - 1) & 1);
-          mbar_wait_sleep(&ofull[1], (it - 1) & 1);
-        }
-        ETR(2);
-#pragma unroll
-        for (int h = 0; h < HG; ++h)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint4*>(sV + sw128_off(r, h * DH + 8 * j)) =
-                make_uint4(vv[h][4 * j], vv[h][4 * j + 1], vv[h][4 * j + 2], vv[h][4 * j + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(v_ready);
-        TL(E_VR, it);
-        ETR(3);
       }
     } else {
-      // ---------------- parts 1, 2: head h = part - 1: O of tile t-1, softmax of tile t
+      // ---------------- parts 1, 2: head h = part - 1: V_h of tile t -> smem, O of tile t-1, softmax of tile t
       const int h = part - 1;
       const uint32_t sh = tl + T_S + 128 * h;
       float l_prev = 1.f;
@@ -466,37 +464,33 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int t = t0; t < n_tiles; t += dt, ++it) {
         const int32_t* R = rec + size_t(t) * ATT_REC_INTS;
         const int row0 = __ldg(R), nrows = __ldg(R + 1);
+        uint32_t vv[16];
         {
-          // staging of head h: Q_h -> TMEM (TS operand of S), K_h -> smem (row = key, [K_h0 | K_h1])
+          // V_h of tile t: + bias -> bf16 pairs (written to smem once PV(t-1, h) has read V_h(t-1))
           mbar_wait(tfull, it & 1);
           tc_fence_after();
-          uint32_t a[32], pk[16];
-          tmem_ld32(tl + T_ACC + h * DH, a);
-          tmem_ld_wait_regs(a);
-          bias_pack32(a, bs + h * DH, pk);
-          tmem_st16(tl + T_Q + (DH / 2) * h, pk);
-          tmem_ld32(tl + T_ACC + HG * DH + h * DH, a);
+          uint32_t a[32];
+          tmem_ld32(tl + T_ACC + 2 * HG * DH + h * DH, a);
           tmem_ld_wait_regs(a);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty);
-          bias_pack32(a, bs + HG * DH + h * DH, pk);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint4*>(sK + sw128_off(r, h * DH + 8 * j)) =
-                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          fence_proxy_async_smem();                       // K (generic writes) -> the S MMA
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(qk_ready);
+          bias_pack32(a, bs + 2 * HG * DH + h * DH, vv);
         }
-        // wtab of tile it (part 0).  Checked before this warp releases S_h (oempty below): the next
+        // wtab of tile it (part 0).  Checked before this warp releases S_h (oempty in the drain): the next
         // phase of qk_ready needs S(it, h), so it cannot complete before this wait has seen phase it.
         mbar_wait(qk_ready, it & 1);
         const uint32_t w = wtab[(it & 1) * BM + r];
         const int ta = int(w & 0xffu), te = int(w >> 8);
         if (it > 0) drain(it - 1);
+        TL(h ? E_DR1 : E_DR0, it);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)                       // V_h (row = key; the MN-major B operand of P V)
+          *reinterpret_cast<uint4*>(sV + sw128_off(r, h * DH + 8 * j)) =
+              make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&v_ready[h]);
         ETR(2);
         // softmax(t, h): the warp loads the 16-column pieces covering its rows' windows
         const int lo = __reduce_min_sync(0xffffffffu, te > ta ? ta : BM);
@@ -504,7 +498,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int p0 = lo >> 4, p1 = hi > lo ? (hi - 1) >> 4 : -1;   // pieces [p0, p1]
         const float qs = qscale;
         ETR(3);
-        TL(h ? E_DR1 : E_DR0, it);
         mbar_wait(&sfull[h], it & 1);
         TL(h ? E_SF1 : E_SF0, it);
         ETR(4);

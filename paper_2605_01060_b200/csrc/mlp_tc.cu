@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "epi_ln.cuh"
@@ -40,6 +41,12 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 #ifndef MLP_A_SPLIT
 #define MLP_A_SPLIT 1               // A-tile boxes issued by all three producers (0: producer 0 alone)
 #endif
+#ifndef MLP_LN_PIPE
+#define MLP_LN_PIPE 1               // NP = 3: LN TMEM loads one step ahead too
+#endif
+#ifndef MLP_STORE_DIRECT
+#define MLP_STORE_DIRECT 0          // 1: final LN output as 32-byte stores from registers (measured equal)
+#endif
 #ifndef MLP_PINGPONG
 #define MLP_PINGPONG 0              // 1: A tile and weight ring swap shared-memory regions every unit (measured neutral)
 #endif
@@ -49,16 +56,17 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 constexpr int RING = MLP_RING;      // weight ring stages
 constexpr int STAGE = 24 * 1024;    // 3 W1 k-blocks (64 rows x 128 B each) or 1 W2 k-block (2 x 96 rows)
 #ifndef MLP_EPI_WARPS
-#define MLP_EPI_WARPS 8   // 16 measured slower (tail 2148 -> 2344 ms/step: 96-register cap)
+#define MLP_EPI_WARPS 8   // d = 384: 8 or 12 (16 measured slower: tail 2148 -> 2344 ms/step, 96-register cap)
 #endif
-constexpr int EPI_WARPS = MLP_EPI_WARPS;   // 4 lane quadrants x NP column parts
-constexpr int NP = EPI_WARPS / 4;
-constexpr int HC = FC / NP;                // H-chunk columns per epilogue warp
-constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr uint32_t H_COL = 384;     // TMEM column of the H chunk
 
 template <int D>
 struct MlpCfg {
+  // epilogue warps: 4 lane quadrants x NP column parts (d = 64: 8)
+  static constexpr int EPI_WARPS = D == 384 ? MLP_EPI_WARPS : 8;
+  static constexpr int NP = EPI_WARPS / 4;
+  static constexpr int HC = FC / NP;                 // H-chunk columns per epilogue warp (NP = 3: 48, 48, 32)
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int KB1 = D / 64;                 // k-blocks of the first GEMM
   static constexpr int A_BYTES = KB1 * MBM * 128;    // resident X1 rows
   static constexpr int HS_BYTES = 2 * MBM * 128;     // one H chunk, 2 k-blocks
@@ -70,7 +78,7 @@ struct MlpCfg {
   // beta (3 D floats, copied in per unit) live in Hs, which is idle while the LN epilogue runs.
   // LN scratch (aliases Hs, which is idle during the LN): output staging [8 warps][MLP_STG][2 KB],
   // stats [2 halves][128] float4, b2 / gamma / beta
-  static constexpr int LN_STG = EPI_WARPS * MLP_STG * 2048;
+  static constexpr int LN_STG = MLP_STORE_DIRECT ? 0 : EPI_WARPS * MLP_STG * 2048;
   static constexpr int LN_SCRATCH = ((LN_STG + NP * MBM * 16 + 3 * D * 4 + 1023) / 1024) * 1024;
   static constexpr int SCRATCH = LN_SCRATCH > HS_BYTES ? LN_SCRATCH : HS_BYTES;
   // MLP_PINGPONG: two equal regions that alternate between the A tile and the weight ring, unit by
@@ -85,6 +93,20 @@ struct MlpCfg {
   static_assert(B2_BOX * 128 * N2_MMAS <= STAGE, "W2 k-block fits a stage");
 };
 
+// MLP_TL: per-unit event timeline of CTA 0 (units 10..13 of the 4th launch), buffered in global memory and
+// printed at the end of the kernel (timing experiments only)
+#ifdef MLP_TL
+__device__ long long g_mtl_t0;
+__device__ int g_mtl_launch;
+__device__ long long g_mtlbuf[4][16];
+enum { M_AFULL, M_G0ISS, M_Y0, M_XRES, M_X1R, M_G1_0, M_YFULL, M_AFREE, M_YEMPTY, M_XLOAD, M_N };
+__device__ const char* const g_mtl_names[M_N] = {"a_full(iss)", "g0_issued", "y0_full(epi)", "xres_full(epi)",
+    "x1_ready(iss)", "g1c0_issued", "y_full(epi)", "a_free(epi)", "y_empty(epi)", "x_load(prod)"};
+#define MTL(ev, j) do { if (blockIdx.x == 0 && g_mtl_launch == 3 && (j) >= 10 && (j) < 14 && (threadIdx.x & 31) == 0 && \
+    (threadIdx.x < 128 || (threadIdx.x >> 5) == 4)) g_mtlbuf[(j) - 10][ev] = clock64() - g_mtl_t0; } while (0)
+#else
+#define MTL(ev, j) do {} while (0)
+#endif
 #ifdef MLP_TRACE
 #define MW(bar, par, slot)                      \
   do {                                          \
@@ -126,7 +148,7 @@ __device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_add
 // FFN runs on that X1; X1 never reaches HBM.  The final output overwrites X in place (each CTA reads
 // its LN0 residual rows of X before it writes them).
 template <int D, bool OP>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmWo,
                   const __grid_constant__ CUtensorMap tmR, int M, int F, const float* __restrict__ b1,
@@ -134,6 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   const float* __restrict__ bo, const float* __restrict__ gamma1, const float* __restrict__ beta1,
                   const uint16_t* __restrict__ xres, uint16_t* __restrict__ out, float eps) {
   using T = MlpCfg<D>;
+  constexpr int EPI_WARPS = T::EPI_WARPS, NP = T::NP, HC = T::HC;
   constexpr int KB1 = T::KB1;
   constexpr int S1 = KB1 == 1 ? 1 : KB1 / 3;         // ring stages per W1 chunk
   constexpr int KPS = KB1 == 1 ? 1 : 3;              // W1 k-blocks per stage
@@ -153,7 +176,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* y0_full = a_free + 1;                            // both (OP): G0 retired
   uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A
   uint64_t* xres_full = x1_ready + 1;                         // local (OP): X residual rows landed in A
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xres_full + 1);
+  uint64_t* okb_free = xres_full + 1;                         // [KB1] both (OP): G0 done with O k-block kb
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(okb_free + KB1);
   uint8_t* const sR0 = smem + T::HEAD;                       // [KB1][128 x 128 B] (PINGPONG: region 0)
   uint8_t* sHs = sR0 + (MLP_PINGPONG ? T::REGION : T::A_BYTES);   // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
@@ -192,6 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(y0_full, 1);
     mbar_init(x1_ready, 2 * EPI_WARPS);
     mbar_init(xres_full, 1);
+    for (int kb = 0; kb < KB1; ++kb) mbar_init(&okb_free[kb], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -202,6 +227,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+#ifdef MLP_DEPHASE
+  // timing experiment: odd pairs start MLP_DEPHASE cycles late, so the CTA pairs' LayerNorm phases (and
+  // their HBM bursts: O / X tile loads, X stores) interleave with other pairs' MMA phases
+  if ((unit0 & 1) != 0) {
+    const long long t_end = clock64() + MLP_DEPHASE;
+    while (clock64() < t_end) __nanosleep(1000);
+  }
+#endif
 
   if (warp == 0 || warp == 2 || warp == 3) {
     griddep_wait();                            // A (O or X1) and the residual rows come from the previous kernel
@@ -294,10 +327,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           if constexpr (OP) {
             ring_wo(0, KB1);
             if (p == 0) {
-              mbar_wait(y0_full, ui & 1);
-              mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
-              for (int kb = 0; kb < KB1; ++kb)
+              for (int kb = 0; kb < KB1; ++kb) {
+                mbar_wait(&okb_free[kb], ui & 1);
+                if (kb == 0) {
+                  MTL(M_XLOAD, ui);
+                  mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
+                }
                 tma_load_2d(sA + kb * MBM * 128, &tmR, xres_full, kb * 64, m0);
+              }
             }
           }
           for (int c = 0; c < NCH; ++c) {
@@ -317,12 +354,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         if constexpr (OP) {
           ring_wo(WO_EARLY, KB1);
           if (p == 0) {
-            // once G0 has consumed O, the A tile takes this unit's X rows: the LN0 residual, read from
-            // smem instead of from L2 one step ahead (its latency bounded LN0's first pass)
-            mbar_wait(y0_full, ui & 1);
-            mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
-            for (int kb = 0; kb < KB1; ++kb)
+            // as G0 consumes O k-block by k-block, each freed k-block of the A tile takes the same columns
+            // of this unit's X rows: the LN0 residual, read from smem (its load overlaps G0)
+            for (int kb = 0; kb < KB1; ++kb) {
+              mbar_wait(&okb_free[kb], ui & 1);
+              if (kb == 0) {
+                MTL(M_XLOAD, ui);
+                mbar_arrive_expect_tx(xres_full, uint32_t(T::A_BYTES));
+              }
               tma_load_2d(sA + kb * MBM * 128, &tmR, xres_full, kb * 64, m0);
+            }
           }
         }
         for (int c = 0; c < NCH; ++c) {
@@ -382,7 +423,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int u = unit0; u < n_units; u += units, ++ui) {
       a_desc0 = umma_desc_sw128(smem_u32(region_a(ui)));
       w_desc0 = umma_desc_sw128(smem_u32(region_w(ui)));
+#ifdef MLP_TL
+      if (ui == 0 && blockIdx.x == 0 && lane == 0) g_mtl_t0 = clock64();
+#endif
       MW(a_full, ui & 1, 3);
+      MTL(M_AFULL, ui);
       tc_fence_after();
       if constexpr (OP) {
         // G0: Y = O Wo^T (the previous unit's final LN has drained Y)
@@ -402,12 +447,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_mma_bf16_pair(tmem_base + j * T::N2, ad + uint64_t(k * 2),
                                  bd + uint64_t((j * T::B2_BOX * 128 + k * 32) >> 4), idesc2, (kb | k) != 0);
             tc_commit_pair_mc(&empty[s], 0x3);
+            tc_commit_pair_mc(&okb_free[kb], 0x3);   // O k-block kb read: X may take its place
           }
           __syncwarp();
         }
         if (elect_one()) tc_commit_pair_mc(y0_full, 0x3);
         __syncwarp();
+        MTL(M_G0ISS, ui);
         MW(x1_ready, ui & 1, 1);                      // both CTAs' X1 written into A
+        MTL(M_X1R, ui);
         tc_fence_after();
       }
       for (int c = 0; c < NCH; ++c) {
@@ -436,6 +484,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (c == NCH - 1) tc_commit_pair_mc(a_empty, 0x3);   // A free for the next unit
         }
         __syncwarp();
+        if (c == 0) MTL(M_G1_0, ui);
         ++hc;
         if (c > 0) g2(c - 1, ui);
       }
@@ -490,14 +539,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         (void)row;
         const ResidualSmemA rg{sA, row_l, hh * (D / NP)};
         mbar_wait(xres_full, ui & 1);          // X rows in the A tile (G0 is done with O)
+        MTL(M_XRES, ui);
 #if defined(MLP_SKIP_LN) && (MLP_SKIP_LN & 1)   // timing experiment only (wrong results)
         mbar_wait(y0_full, ui & 1);
         tc_fence_after();
         if (false)
 #endif
-        ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
+                                MTL(M_Y0, ui);
                                 tc_fence_after();
                               },
                               [&](const uint32_t (&p)[16], int col) {   // row row_l, columns col .. col+31
@@ -514,28 +565,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive_cluster_release(x1_ready_c);
         asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");   // LN0 scratch free
       }
-      for (int c = 0; c < NCH; ++c, ++hc) {
-        // H(c) columns [HC hh, HC hh + HC) of this row: TMEM -> registers, then release the accumulator
-        const float4* bp = reinterpret_cast<const float4*>(b1 + c * FC + HC * hh);
-        float4 bb[HC / 4];
+      // H(c) columns [col0, col0 + W) of this row: TMEM -> registers (then the accumulator is released),
+      // + bias, GELU, bf16 -> Hs (k-block col / 64, 16-byte chunk (col % 64) / 8 at (chunk ^ (row & 7)))
+      auto gelu_chunk = [&](auto wc, int col0, int c) {
+        constexpr int W = decltype(wc)::value;
+        const float4* bp = reinterpret_cast<const float4*>(b1 + c * FC + col0);
+        float4 bb[W / 4];
 #pragma unroll
-        for (int i = 0; i < HC / 4; ++i) bb[i] = __ldg(bp + i);
-        uint32_t rh[HC];
+        for (int i = 0; i < W / 4; ++i) bb[i] = __ldg(bp + i);
+        uint32_t rh[W];
         ETR(0);
         mbar_wait(h_full, hc & 1);
         ETR(1);
         tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < HC / 32; ++s) tmem_ld32(t_row + H_COL + HC * hh + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(rh + 32 * s));
+        for (int s = 0; s < W / 32; ++s) tmem_ld32(t_row + H_COL + col0 + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(rh + 32 * s));
+        if constexpr (W % 32 == 16) tmem_ld16(t_row + H_COL + col0 + W - 16, *reinterpret_cast<uint32_t(*)[16]>(rh + W - 16));
 #pragma unroll
-        for (int s = 0; s < HC / 32; ++s) tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(rh + 32 * s));
+        for (int s = 0; s < W / 32; ++s) tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(rh + 32 * s));
+        if constexpr (W % 32 == 16) tmem_ld_wait_regs16(*reinterpret_cast<uint32_t(*)[16]>(rh + W - 16));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(h_empty_c);
         ETR(2);
-        uint32_t pk[HC / 2];
+        uint32_t pk[W / 2];
 #pragma unroll
-        for (int i = 0; i < HC / 4; ++i) {
+        for (int i = 0; i < W / 4; ++i) {
           float v0 = __uint_as_float(rh[4 * i]) + bb[i].x, v1 = __uint_as_float(rh[4 * i + 1]) + bb[i].y;
           float v2 = __uint_as_float(rh[4 * i + 2]) + bb[i].z, v3 = __uint_as_float(rh[4 * i + 3]) + bb[i].w;
           gelu2(v0, v1);
@@ -546,20 +601,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         ETR(3);
         mbar_wait(hs_empty, (hc & 1) ^ 1);      // Hs free: G2(c-1) retired
         ETR(4);
-        // columns [HC hh, +HC) of Hs, row row_l: k-block (HC hh) / 64, 16-byte chunks j at (j ^ (row & 7))
-        {
-          uint8_t* hrow = sHs + ((HC * hh) >> 6) * MBM * 128 + row_l * 128;
-          const int j0 = ((HC * hh) & 63) >> 3;
 #pragma unroll
-          for (int j = 0; j < HC / 8; ++j)
-            *reinterpret_cast<uint4*>(hrow + (((j0 + j) ^ (row_l & 7)) << 4)) =
-                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        for (int j = 0; j < W / 8; ++j) {
+          const int col = col0 + 8 * j;
+          *reinterpret_cast<uint4*>(sHs + (col >> 6) * MBM * 128 + row_l * 128 + ((((col & 63) >> 3) ^ (row_l & 7)) << 4)) =
+              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
         ETR(5);
         fence_proxy_async_smem();              // generic-proxy writes -> visible to the MMA (async proxy)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster_release(hs_full_c);
         ETR(6);
+      };
+      for (int c = 0; c < NCH; ++c, ++hc) {
+        if constexpr (NP == 3) {               // 128 columns over 3 warps: 48 + 48 + 32
+          if (hh < 2) gelu_chunk(std::integral_constant<int, 48>{}, 48 * hh, c);
+          else gelu_chunk(std::integral_constant<int, 32>{}, 96, c);
+        } else {
+          gelu_chunk(std::integral_constant<int, HC>{}, HC * hh, c);
+        }
       }
       // ---- LN epilogue: X2 = LN(Y + b2 + X1); output staged per warp in Hs (free after G2(last))
       {
@@ -572,6 +632,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         ETR(0);
         mbar_wait(y_full, ui & 1);            // Hs no longer read by the MMA
+        MTL(M_YFULL, ui);
         ETR(7);
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
@@ -590,14 +651,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) mbar_arrive(a_free);
       if (false)
 #endif
-      ln_epilogue<D, D / NP, (NP <= 2)>(t_row, hh * (D / NP), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+      ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE)>(t_row, hh * (D / NP), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();
                             },
                             [&](const uint32_t (&p)[16], int col) {
 #ifndef MLP_NO_FSTORE   // timing experiment only (wrong results)
+#if MLP_STORE_DIRECT
+                              store_row_64B(p, lane, out, m0 + q * 32, M, D, col);
+#else
                               store_rows_32x32(stg0, p, lane, out, m0 + q * 32, M, D, col);
+#endif
 #else
                               if (p[0] == 0x7fffffffu && col < 0) out[0] = 0;
 #endif
@@ -605,10 +670,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                             [&] {                // residual read for the last time: the A tile may take
                               __syncwarp();      // the next unit's rows while pass 2 runs
                               if (lane == 0) mbar_arrive(a_free);
+                              MTL(M_AFREE, ui);
                             });
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(y_empty_c);
+      MTL(M_YEMPTY, ui);
       // LN constants / stats (in Hs) consumed before the next unit's first chunk overwrites Hs
       ETR(10);
       asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
@@ -630,6 +697,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   cluster_sync();
+#ifdef MLP_TL
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (g_mtl_launch == 3)
+      for (int j = 0; j < 4; ++j)
+        for (int e = 0; e < M_N; ++e) printf("MTL %8lld unit %d %s\n", g_mtlbuf[j][e], 10 + j, g_mtl_names[e]);
+    ++g_mtl_launch;
+  }
+#endif
   if (warp == 2) {
     __syncwarp();
     tmem_dealloc_pair(tmem_base, 512);
@@ -653,7 +728,7 @@ cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
   const int pairs = int(std::min<int64_t>(n_units, (sms > 0 ? sms : 148) / 2));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(2 * pairs));
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(T::THREADS);
   cfg.dynamicSmemBytes = size_t(T::SMEM);
   cfg.stream = st;
   cudaLaunchAttribute at[2];

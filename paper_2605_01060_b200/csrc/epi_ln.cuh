@@ -64,8 +64,10 @@ struct LnNoOp {
 };
 
 // pass1_done() runs once the residual has been read for the last time (after pass 1).
-template <int BN, int HALF, bool PIPE = true, typename Res, typename Ready, typename Store, typename P1 = LnNoOp,
-          int NP = BN / HALF>
+// REMAP_LO > 0: accumulator columns [0, REMAP_LO) live at TMEM column REMAP_BASE + c instead of c (the fused
+// tail's split out-projection, mlp_tc.cu MLP_G0SPLIT).
+template <int BN, int HALF, bool PIPE = true, uint32_t REMAP_LO = 0, uint32_t REMAP_BASE = 0, typename Res,
+          typename Ready, typename Store, typename P1 = LnNoOp, int NP = BN / HALF>
 __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
                                             const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,
                                             int lane, float eps, Ready&& wait_ready, Store&& store,
@@ -75,12 +77,13 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
 #endif
   constexpr int NSTEP = HALF / 32;
   constexpr int NB = PIPE ? 2 : 1;
+  auto tcol = [](int c) { return uint32_t(c) < REMAP_LO ? REMAP_BASE + uint32_t(c) : uint32_t(c); };
   uint32_t r[NB][32];
   uint32_t rs[NB][16];
   load_res(0, rs[0]);
   wait_ready();
   LNT(0);
-  tmem_ld32(taddr + c_lo, r[0]);
+  tmem_ld32(taddr + tcol(c_lo), r[0]);
   float shift = 0.f;
   f32x2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f);
 #pragma unroll
@@ -88,12 +91,12 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
     const int cur = PIPE ? (k & 1) : 0;
     const int c = c_lo + 32 * k;
     if (!PIPE && k > 0) {
-      tmem_ld32(taddr + c, r[0]);
+      tmem_ld32(taddr + tcol(c), r[0]);
       load_res(k, rs[0]);
     }
     tmem_ld_wait_regs(r[cur]);
     if (PIPE && k + 1 < NSTEP) {
-      tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+      tmem_ld32(taddr + tcol(c + 32), r[cur ^ 1]);
       load_res(k + 1, rs[cur ^ 1]);
     }
     const uint32_t (&rr)[16] = rs[cur];
@@ -111,7 +114,7 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
       w[2 * i] = __float_as_uint(f2lo(v));
       w[2 * i + 1] = __float_as_uint(f2hi(v));
     }
-    tmem_st32(taddr + c, w);
+    tmem_st32(taddr + tcol(c), w);
   }
   tmem_st_wait();
   pass1_done();
@@ -151,14 +154,14 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   }
   const float rstd = rsqrtf(var + eps);
   const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);
-  tmem_ld32(taddr + c_lo, r[0]);
+  tmem_ld32(taddr + tcol(c_lo), r[0]);
 #pragma unroll
   for (int k = 0; k < NSTEP; ++k) {
     const int cur = PIPE ? (k & 1) : 0;
     const int c = c_lo + 32 * k;
-    if (!PIPE && k > 0) tmem_ld32(taddr + c, r[0]);
+    if (!PIPE && k > 0) tmem_ld32(taddr + tcol(c), r[0]);
     tmem_ld_wait_regs(r[cur]);
-    if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + c + 32, r[cur ^ 1]);
+    if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + tcol(c + 32), r[cur ^ 1]);
     uint32_t p[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {

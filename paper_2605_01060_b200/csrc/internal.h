@@ -94,6 +94,7 @@ struct MlpArgs {
   const CUtensorMap* tmW2;   // W2 [D x F], box mlp_w2_box_rows(D)
   const CUtensorMap* tmWo;   // nullptr, or Wo [D x D] (box mlp_w2_box_rows(D)): K6 fused as a prologue
   const CUtensorMap* tmX;    // X [M x D] load map (L2 prefetch of the K6 residual rows), when tmWo is set
+  const CUtensorMap* tmWo64 = nullptr;   // Wo [D x D], box 64 rows (d = 384: the split out-projection)
   int64_t M;
   int D, F;
   const float *b1, *b2, *gamma, *beta;       // FFN biases, LN_o
@@ -173,6 +174,7 @@ struct LayerW {
   float *bqkv, *bo, *ln1_g, *ln1_b, *b1, *b2, *ln2_g, *ln2_b;
   CUtensorMap tm_wqkv, tm_wo, tm_w1, tm_w2;
   CUtensorMap tm_wo_mlp, tm_w1_mlp, tm_w2_mlp;   // fused tail (mlp_tc.cu) views of Wo / W1 / W2
+  CUtensorMap tm_wo64;                            // Wo, 64-row boxes (split out-projection in the tail)
   uint16_t* wqkv_att = nullptr;       // W_qkv rows permuted into head-complete 192-row slices
   float* bqkv_att = nullptr;
   CUtensorMap tm_wqkv_att;

@@ -44,11 +44,17 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 #ifndef MLP_LN_PIPE
 #define MLP_LN_PIPE 1               // NP = 3: LN TMEM loads one step ahead too
 #endif
+#ifndef MLP_G0SPLIT
+// d = 384 with MLP_PINGPONG: the next unit's out-projection G0 starts under this unit's final LayerNorm:
+// its first 128 output columns (N = 128 MMAs) go to the idle H-chunk TMEM columns as soon as the O tile
+// and the first Wo stages are in; columns 128..383 (N = 256 MMAs) follow once the LN has drained Y.
+#define MLP_G0SPLIT 1
+#endif
 #ifndef MLP_STORE_DIRECT
 #define MLP_STORE_DIRECT 0          // 1: final LN output as 32-byte stores from registers (measured equal)
 #endif
 #ifndef MLP_PINGPONG
-#define MLP_PINGPONG 0              // 1: A tile and weight ring swap shared-memory regions every unit (measured neutral)
+#define MLP_PINGPONG 1              // A tile and weight ring swap shared-memory regions every unit
 #endif
 #ifndef MLP_PREFETCH
 #define MLP_PREFETCH 0              // L2 prefetch of the next unit's A rows (measured: no effect)
@@ -151,12 +157,13 @@ template <int D, bool OP>
 __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmWo,
-                  const __grid_constant__ CUtensorMap tmR, int M, int F, const float* __restrict__ b1,
+                  const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmWo64, int M, int F, const float* __restrict__ b1,
                   const float* __restrict__ b2, const float* __restrict__ gamma, const float* __restrict__ beta,
                   const float* __restrict__ bo, const float* __restrict__ gamma1, const float* __restrict__ beta1,
                   const uint16_t* __restrict__ xres, uint16_t* __restrict__ out, float eps) {
   using T = MlpCfg<D>;
   constexpr int EPI_WARPS = T::EPI_WARPS, NP = T::NP, HC = T::HC;
+  constexpr bool SPLIT = OP && MLP_PINGPONG && MLP_G0SPLIT && D == 384;   // G0 in column blocks 128 + 256
   constexpr int KB1 = T::KB1;
   constexpr int S1 = KB1 == 1 ? 1 : KB1 / 3;         // ring stages per W1 chunk
   constexpr int KPS = KB1 == 1 ? 1 : 3;              // W1 k-blocks per stage
@@ -286,6 +293,31 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
                              j * T::N2 + rank * T::B2_BOX, pol_w);
         }
       };
+      // SPLIT: G0's Wo stages -- cb0 (output columns 0..127, this CTA's 64 rows of each N = 128 MMA): 2 stages
+      // of 3 k-blocks; cb12 (columns 128..383, this CTA's 128 rows of each N = 256 MMA): 6 stages of 1
+      // k-block (16 KB of a 24 KB slot)
+      auto ring_wo_split = [&]() {
+        for (int i = 0; i < 2; ++i, ++sc) {
+          const int s = int(sc % RING);
+          const uint32_t ph = (sc / RING) & 1;
+          if (int(sc % 3) != p) continue;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * 3 * 64 * 128);
+          for (int j = 0; j < 3; ++j)
+            tma_load_2d_pair(sW + s * STAGE + j * 64 * 128, &tmWo64, full_c + uint32_t(s) * 8, (3 * i + j) * 64,
+                             rank * 64, pol_w);
+        }
+        for (int kb = 0; kb < KB1; ++kb, ++sc) {
+          const int s = int(sc % RING);
+          const uint32_t ph = (sc / RING) & 1;
+          if (int(sc % 3) != p) continue;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * 2 * 64 * 128);
+          for (int j = 0; j < 2; ++j)
+            tma_load_2d_pair(sW + s * STAGE + j * 64 * 128, &tmWo64, full_c + uint32_t(s) * 8, kb * 64,
+                             128 + rank * 128 + j * 64, pol_w);
+        }
+      };
       // A: this CTA's rows, once per unit.  Its k-blocks are split over the three producers (one
       // issuing thread completes ~one box per 500 cycles, and the load sits between the previous
       // unit's final-LN pass 1 and this unit's G0).  Box completions of producers 1 and 2 may reach
@@ -325,7 +357,8 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
           mbar_wait(a_empty, (ui & 1) ^ 1);
           mbar_wait(a_free, (ui & 1) ^ 1);
           if constexpr (OP) {
-            ring_wo(0, KB1);
+            if constexpr (SPLIT) ring_wo_split();
+            else ring_wo(0, KB1);
             if (p == 0) {
               for (int kb = 0; kb < KB1; ++kb) {
                 mbar_wait(&okb_free[kb], ui & 1);
@@ -420,16 +453,72 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
       __syncwarp();
       ++gc;
     };
+    // SPLIT: G0 column block 0 of unit j (N = 128 into the H-chunk columns): issued at the start (j = 0)
+    // or right after the previous unit's last G2, i.e. under its final LayerNorm
+    auto g0_cb0 = [&](int j) {
+      const uint64_t ad0 = umma_desc_sw128(smem_u32(region_a(j))), wd0 = umma_desc_sw128(smem_u32(region_w(j)));
+      MW(a_full, j & 1, 3);
+      MTL(M_AFULL, j);
+      tc_fence_after();
+      for (int i = 0; i < 2; ++i, ++sc) {
+        const int s = int(sc % RING);
+        MW(&full[s], (sc / RING) & 1, 2);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t bd0 = wd0 + uint64_t((s * STAGE) >> 4);
+          for (int jj = 0; jj < 3; ++jj) {
+            const int kb = 3 * i + jj;
+            const uint64_t ad = ad0 + uint64_t((kb * MBM * 128) >> 4);
+            const uint64_t bd = bd0 + uint64_t((jj * 64 * 128) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_bf16_pair(tmem_base + H_COL, ad + uint64_t(k * 2), bd + uint64_t(k * 2), idesc1, (kb | k) != 0);
+          }
+          tc_commit_pair_mc(&empty[s], 0x3);
+        }
+        __syncwarp();
+      }
+    };
+    if constexpr (SPLIT)
+      if (unit0 < n_units) g0_cb0(0);
     for (int u = unit0; u < n_units; u += units, ++ui) {
       a_desc0 = umma_desc_sw128(smem_u32(region_a(ui)));
       w_desc0 = umma_desc_sw128(smem_u32(region_w(ui)));
 #ifdef MLP_TL
       if (ui == 0 && blockIdx.x == 0 && lane == 0) g_mtl_t0 = clock64();
 #endif
-      MW(a_full, ui & 1, 3);
-      MTL(M_AFULL, ui);
-      tc_fence_after();
-      if constexpr (OP) {
+      if constexpr (!SPLIT) {
+        MW(a_full, ui & 1, 3);
+        MTL(M_AFULL, ui);
+        tc_fence_after();
+      }
+      if constexpr (SPLIT) {
+        // G0 columns 128..383 (N = 256) into Y[128, 384): the previous unit's final LN has drained Y
+        MW(y_empty, (ui & 1) ^ 1, 0);
+        tc_fence_after();
+        constexpr uint32_t idesc256 = umma_idesc_bf16(2 * MBM, 256);
+        for (int kb = 0; kb < KB1; ++kb, ++sc) {
+          const int s = int(sc % RING);
+          MW(&full[s], (sc / RING) & 1, 2);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = a_desc0 + uint64_t((kb * MBM * 128) >> 4);
+            const uint64_t bd = w_desc0 + uint64_t((s * STAGE) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_bf16_pair(tmem_base + 128, ad + uint64_t(k * 2), bd + uint64_t(k * 2), idesc256, (kb | k) != 0);
+            tc_commit_pair_mc(&empty[s], 0x3);
+            tc_commit_pair_mc(&okb_free[kb], 0x3);   // O k-block kb read by both column blocks
+          }
+          __syncwarp();
+        }
+        if (elect_one()) tc_commit_pair_mc(y0_full, 0x3);
+        __syncwarp();
+        MTL(M_G0ISS, ui);
+        MW(x1_ready, ui & 1, 1);                      // both CTAs' X1 written into A
+        MTL(M_X1R, ui);
+        tc_fence_after();
+      } else if constexpr (OP) {
         // G0: Y = O Wo^T (the previous unit's final LN has drained Y)
         MW(y_empty, (ui & 1) ^ 1, 0);
         tc_fence_after();
@@ -489,6 +578,13 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         if (c > 0) g2(c - 1, ui);
       }
       g2(NCH - 1, ui);
+      if constexpr (SPLIT) {
+        if (u + units < n_units) {
+          MW(h_empty, (hc & 1) ^ 1, 4);              // the GELU of the last chunk drained H
+          tc_fence_after();
+          g0_cb0(ui + 1);
+        }
+      }
     }
 #ifdef MLP_TRACE
     if (lane == 0 && blockIdx.x < 8)
@@ -545,7 +641,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         tc_fence_after();
         if (false)
 #endif
-        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE)>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE), SPLIT ? 128u : 0u, H_COL>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
                                 MTL(M_Y0, ui);
@@ -742,7 +838,9 @@ cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   const CUtensorMap& tmWo = OP ? *a.tmWo : *a.tmW2;
   const CUtensorMap& tmR = OP ? *a.tmX : *a.tmA;
-  return cudaLaunchKernelEx(&cfg, kern, *a.tmA, *a.tmW1, *a.tmW2, tmWo, tmR, int(a.M), a.F, a.b1, a.b2, a.gamma,
+  const CUtensorMap& tmWo64 = a.tmWo64 ? *a.tmWo64 : tmWo;
+  if (OP && MLP_PINGPONG && MLP_G0SPLIT && D == 384 && !a.tmWo64) return cudaErrorInvalidValue;
+  return cudaLaunchKernelEx(&cfg, kern, *a.tmA, *a.tmW1, *a.tmW2, tmWo, tmR, tmWo64, int(a.M), a.F, a.b1, a.b2, a.gamma,
                             a.beta, a.bo, a.gamma1, a.beta1, a.x, a.out, a.eps);
 }
 

@@ -211,6 +211,7 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       if (mlp_fused_supported(int(d), int(f))) {
         SURGE_TRY(make_tmap_bf16(&L.tm_wo_mlp, L.wo, d, d, mlp_w2_box_rows(int(d))));
         SURGE_TRY(make_tmap_bf16(&L.tm_w1_mlp, L.w1, f, d, 64));
+        SURGE_TRY(make_tmap_bf16(&L.tm_wo64, L.wo, d, d, 64));
         SURGE_TRY(make_tmap_bf16(&L.tm_w2_mlp, L.w2, d, f, mlp_w2_box_rows(int(d))));
       }
     }
@@ -373,8 +374,8 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     }
     if (tail_fused_ && mlp_fused_ && mlp_fused_supported(d, f)) {
       // K6 + K7 + K8 fused: X = LN_o(FFN(X1) + X1), X1 = LN_a(O Wo^T + bo + X) kept on chip
-      MlpArgs a{&tmO, &L.tm_w1_mlp, &L.tm_w2_mlp, &L.tm_wo_mlp, &tmX, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
-                L.bo, L.ln1_g, L.ln1_b, ws.X, ws.X, s_.eps};
+      MlpArgs a{&tmO, &L.tm_w1_mlp, &L.tm_w2_mlp, &L.tm_wo_mlp, &tmX, &L.tm_wo64, ntok, d, f, L.b1, L.b2, L.ln2_g,
+                L.ln2_b, L.bo, L.ln1_g, L.ln1_b, ws.X, ws.X, s_.eps};
       if (P) prof->begin(st, &ev);
       SURGE_TRY(launch_mlp(a, st));
       if (P) prof->end(KK_TAIL, st, ev, 2 * M * D * D + 4 * M * F * D, 2 * (D * D + 2 * F * D + 3 * M * D));
@@ -396,7 +397,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     k += fused ? 1 : 2;
     if (mlp_fused_ && mlp_fused_supported(d, f)) {
       // K7 + K8 fused: X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1), H stays on chip
-      MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, nullptr, nullptr, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
+      MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, nullptr, nullptr, nullptr, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
                 nullptr, nullptr, nullptr, nullptr, ws.X, s_.eps};
       if (P) prof->begin(st, &ev);
       SURGE_TRY(launch_mlp(a, st));

@@ -102,6 +102,7 @@ struct MlpArgs {
   const uint16_t* x;         // X (K6 residual rows; when tmWo is set)
   uint16_t* out;             // X [M x D] output (in place over x when tmWo is set)
   float eps;
+  const float* ln_host = nullptr;        // host copy [bo | gamma_a | beta_a | b2 | gamma_o | beta_o] (6 D)
 };
 bool mlp_fused_supported(int d, int ffn);
 inline uint32_t mlp_w2_box_rows(int d) { return uint32_t(d <= 256 ? d / 2 : d / 4); }
@@ -175,6 +176,7 @@ struct LayerW {
   CUtensorMap tm_wqkv, tm_wo, tm_w1, tm_w2;
   CUtensorMap tm_wo_mlp, tm_w1_mlp, tm_w2_mlp;   // fused tail (mlp_tc.cu) views of Wo / W1 / W2
   CUtensorMap tm_wo64;                            // Wo, 64-row boxes (split out-projection in the tail)
+  std::vector<float> ln_host;                     // host [bo | ln1_g | ln1_b | b2 | ln2_g | ln2_b] (tail kernel parameter)
   uint16_t* wqkv_att = nullptr;       // W_qkv rows permuted into head-complete 192-row slices
   float* bqkv_att = nullptr;
   CUtensorMap tm_wqkv_att;

@@ -50,6 +50,11 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 // and the first Wo stages are in; columns 128..383 (N = 256 MMAs) follow once the LN has drained Y.
 #define MLP_G0SPLIT 1
 #endif
+#ifndef MLP_LN_CPARAM
+// LayerNorm constants (bo, gamma_a, beta_a, b2, gamma_o, beta_o) as a __grid_constant__ kernel parameter:
+// uniform constant-cache loads instead of shared-memory loads in the LN epilogues (the LNs are MIO-bound)
+#define MLP_LN_CPARAM 0              // 1 measured slower (tail 392 -> 403 ms per 2M texts: LDC.64 per pair)
+#endif
 #ifndef MLP_STORE_DIRECT
 #define MLP_STORE_DIRECT 0          // 1: final LN output as 32-byte stores from registers (measured equal)
 #endif
@@ -65,6 +70,11 @@ constexpr int STAGE = 24 * 1024;    // 3 W1 k-blocks (64 rows x 128 B each) or 1
 #define MLP_EPI_WARPS 8   // d = 384: 8 or 12 (16 measured slower: tail 2148 -> 2344 ms/step, 96-register cap)
 #endif
 constexpr uint32_t H_COL = 384;     // TMEM column of the H chunk
+
+template <int D>
+struct MlpConsts {   // [bo | gamma_a | beta_a | b2 | gamma_o | beta_o], D floats each
+  float v[6 * D];
+};
 
 template <int D>
 struct MlpCfg {
@@ -157,7 +167,8 @@ template <int D, bool OP>
 __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmWo,
-                  const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmWo64, int M, int F, const float* __restrict__ b1,
+                  const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmWo64,
+                  const __grid_constant__ MlpConsts<D> lc, int M, int F, const float* __restrict__ b1,
                   const float* __restrict__ b2, const float* __restrict__ gamma, const float* __restrict__ beta,
                   const float* __restrict__ bo, const float* __restrict__ gamma1, const float* __restrict__ beta1,
                   const uint16_t* __restrict__ xres, uint16_t* __restrict__ out, float eps) {
@@ -616,7 +627,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
       uint8_t* const sA = region_a(ui);
       if constexpr (OP) {
         // ---- LN0 epilogue (K6): X1 = LN_a(Y + bo + X) -> bf16 into the A tile (swizzled K-major)
-        {
+        if constexpr (!MLP_LN_CPARAM) {
           constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
           float cv[PER];
 #pragma unroll
@@ -641,7 +652,10 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         tc_fence_after();
         if (false)
 #endif
-        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE), SPLIT ? 128u : 0u, H_COL>(t_row, hh * (D / NP), rg, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+        const float* c_b = MLP_LN_CPARAM ? lc.v : s_b2;
+        const float* c_g = MLP_LN_CPARAM ? lc.v + D : s_gamma;
+        const float* c_e = MLP_LN_CPARAM ? lc.v + 2 * D : s_beta;
+        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE), SPLIT ? 128u : 0u, H_COL>(t_row, hh * (D / NP), rg, c_b, c_g, c_e, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
                                 MTL(M_Y0, ui);
@@ -718,7 +732,12 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         }
       }
       // ---- LN epilogue: X2 = LN(Y + b2 + X1); output staged per warp in Hs (free after G2(last))
-      {
+      if constexpr (MLP_LN_CPARAM) {
+        ETR(0);
+        mbar_wait(y_full, ui & 1);            // Hs no longer read by the MMA
+        MTL(M_YFULL, ui);
+        ETR(7);
+      } else {
         constexpr int PER = (3 * D + EPI_WARPS * 32 - 1) / (EPI_WARPS * 32);
         float cv[PER];
 #pragma unroll
@@ -747,7 +766,10 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
       if (lane == 0) mbar_arrive(a_free);
       if (false)
 #endif
-      ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE)>(t_row, hh * (D / NP), ra, s_b2, s_gamma, s_beta, stats, q, hh, lane, eps,
+      const float* f_b = MLP_LN_CPARAM ? lc.v + 3 * D : s_b2;
+      const float* f_g = MLP_LN_CPARAM ? lc.v + 4 * D : s_gamma;
+      const float* f_e = MLP_LN_CPARAM ? lc.v + 5 * D : s_beta;
+      ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE)>(t_row, hh * (D / NP), ra, f_b, f_g, f_e, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();
@@ -839,8 +861,13 @@ cudaError_t launch_mlp_t(const MlpArgs& a, cudaStream_t st) {
   const CUtensorMap& tmWo = OP ? *a.tmWo : *a.tmW2;
   const CUtensorMap& tmR = OP ? *a.tmX : *a.tmA;
   const CUtensorMap& tmWo64 = a.tmWo64 ? *a.tmWo64 : tmWo;
+  MlpConsts<D> lc{};
+  if (MLP_LN_CPARAM) {
+    if (!a.ln_host) return cudaErrorInvalidValue;
+    for (int i = 0; i < 6 * D; ++i) lc.v[i] = a.ln_host[i];
+  }
   if (OP && MLP_PINGPONG && MLP_G0SPLIT && D == 384 && !a.tmWo64) return cudaErrorInvalidValue;
-  return cudaLaunchKernelEx(&cfg, kern, *a.tmA, *a.tmW1, *a.tmW2, tmWo, tmR, tmWo64, int(a.M), a.F, a.b1, a.b2, a.gamma,
+  return cudaLaunchKernelEx(&cfg, kern, *a.tmA, *a.tmW1, *a.tmW2, tmWo, tmR, tmWo64, lc, int(a.M), a.F, a.b1, a.b2, a.gamma,
                             a.beta, a.bo, a.gamma1, a.beta1, a.x, a.out, a.eps);
 }
 

@@ -221,7 +221,14 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
   cudaFree(dblob);
   if (e != cudaSuccess) return e;
   if (off != n) return cudaErrorInvalidValue;
-  return e2;
+  if (e2 != cudaSuccess) return e2;
+  // host copies of the LayerNorm constants: a kernel parameter of the fused tail (mlp_tc.cu MLP_LN_CPARAM)
+  for (LayerW& L : layers_) {
+    L.ln_host.resize(6 * d);
+    const float* src[6] = {L.bo, L.ln1_g, L.ln1_b, L.b2, L.ln2_g, L.ln2_b};
+    for (int i = 0; i < 6; ++i) SURGE_TRY(cudaMemcpy(L.ln_host.data() + i * d, src[i], d * 4, cudaMemcpyDeviceToHost));
+  }
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------------------------------ profiler
@@ -376,6 +383,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       // K6 + K7 + K8 fused: X = LN_o(FFN(X1) + X1), X1 = LN_a(O Wo^T + bo + X) kept on chip
       MlpArgs a{&tmO, &L.tm_w1_mlp, &L.tm_w2_mlp, &L.tm_wo_mlp, &tmX, &L.tm_wo64, ntok, d, f, L.b1, L.b2, L.ln2_g,
                 L.ln2_b, L.bo, L.ln1_g, L.ln1_b, ws.X, ws.X, s_.eps};
+      a.ln_host = L.ln_host.data();
       if (P) prof->begin(st, &ev);
       SURGE_TRY(launch_mlp(a, st));
       if (P) prof->end(KK_TAIL, st, ev, 2 * M * D * D + 4 * M * F * D, 2 * (D * D + 2 * F * D + 3 * M * D));
@@ -399,6 +407,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       // K7 + K8 fused: X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1), H stays on chip
       MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, nullptr, nullptr, nullptr, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
                 nullptr, nullptr, nullptr, nullptr, ws.X, s_.eps};
+      a.ln_host = L.ln_host.data();
       if (P) prof->begin(st, &ev);
       SURGE_TRY(launch_mlp(a, st));
       if (P) prof->end(KK_MLP, st, ev, 4 * M * F * D, 2 * (2 * F * D + 2 * M * D));

@@ -248,7 +248,14 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict
     }
   };
   int32_t t = a;
-  for (; t + 2 <= b; t += 2) tokens(std::integral_constant<int, 2>{}, t);
+#ifndef EMB_NT
+#define EMB_NT 2   // tokens per step (4: 113 registers, lower occupancy, measured slower)
+#endif
+  for (; t + EMB_NT <= b; t += EMB_NT) tokens(std::integral_constant<int, EMB_NT>{}, t);
+  if (EMB_NT > 2 && t + 2 <= b) {
+    tokens(std::integral_constant<int, 2>{}, t);
+    t += 2;
+  }
   if (t < b) tokens(std::integral_constant<int, 1>{}, t);
 }
 

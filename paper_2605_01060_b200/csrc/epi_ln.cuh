@@ -2,8 +2,10 @@
 // post-LN, biased variance, fp32 statistics), shared by the LN GEMM (gemm_tc.cu) and the fused MLP
 // (mlp_tc.cu) so both round identically.
 //
-// The accumulator row (BN fp32 columns in TMEM, lane = row) is split over two warps of the same
-// lane quadrant q, each owning columns [c_lo, c_lo + HALF), hh = which half.
+// The accumulator row (BN fp32 columns in TMEM, lane = row) is split over NP warps of the same lane
+// quadrant q (hh = the warp's part), interleaved in 32-column steps: step k of part hh covers columns
+// [32 (NP k + hh), +32), so after step k of every part the 32 NP columns [32 NP k, 32 NP (k + 1)) are done
+// (the fused tail lets its next MMAs chase the LN0 output k-block by k-block).
 //   pass 1: v = acc + bias + residual, written back to TMEM in place, shifted partial sums (the
 //           residual slice and TMEM load of step k+1 are in flight while step k is computed; the
 //           first residual slice is fetched before the accumulator is ready);
@@ -15,12 +17,12 @@
 
 namespace surge {
 
-// Residual source: load(k, rr) fills rr[16] = the 32 bf16 residual values of step k (columns
-// c_lo + 32 k ..), packed in pairs.  It is called one step ahead of use.
+// Residual source: load(col, rr) fills rr[16] = the 32 bf16 residual values of columns col .. col + 31,
+// packed in pairs.  It is called one step ahead of use.
 struct ResidualGlobal {
-  const uint16_t* rrow;   // this row, column c_lo
-  __device__ __forceinline__ void operator()(int k, uint32_t (&rr)[16]) const {
-    const uint4* p = reinterpret_cast<const uint4*>(rrow + 32 * k);
+  const uint16_t* rrow;   // this row, column 0
+  __device__ __forceinline__ void operator()(int col, uint32_t (&rr)[16]) const {
+    const uint4* p = reinterpret_cast<const uint4*>(rrow + col);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint4 v = p[i];
@@ -80,24 +82,26 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   auto tcol = [](int c) { return uint32_t(c) < REMAP_LO ? REMAP_BASE + uint32_t(c) : uint32_t(c); };
   uint32_t r[NB][32];
   uint32_t rs[NB][16];
-  load_res(0, rs[0]);
+  (void)c_lo;
+  auto lncol = [&](int k) { return 32 * (NP * k + hh); };   // columns of step k
+  load_res(lncol(0), rs[0]);
   wait_ready();
   LNT(0);
-  tmem_ld32(taddr + tcol(c_lo), r[0]);
+  tmem_ld32(taddr + tcol(lncol(0)), r[0]);
   float shift = 0.f;
   f32x2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < NSTEP; ++k) {
     const int cur = PIPE ? (k & 1) : 0;
-    const int c = c_lo + 32 * k;
+    const int c = lncol(k);
     if (!PIPE && k > 0) {
       tmem_ld32(taddr + tcol(c), r[0]);
-      load_res(k, rs[0]);
+      load_res(c, rs[0]);
     }
     tmem_ld_wait_regs(r[cur]);
     if (PIPE && k + 1 < NSTEP) {
-      tmem_ld32(taddr + tcol(c + 32), r[cur ^ 1]);
-      load_res(k + 1, rs[cur ^ 1]);
+      tmem_ld32(taddr + tcol(lncol(k + 1)), r[cur ^ 1]);
+      load_res(lncol(k + 1), rs[cur ^ 1]);
     }
     const uint32_t (&rr)[16] = rs[cur];
     if (k == 0) shift = __uint_as_float(r[cur][0]) + s_bias[c] + bf16lo(rr[0]);
@@ -154,14 +158,14 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   }
   const float rstd = rsqrtf(var + eps);
   const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);
-  tmem_ld32(taddr + tcol(c_lo), r[0]);
+  tmem_ld32(taddr + tcol(lncol(0)), r[0]);
 #pragma unroll
   for (int k = 0; k < NSTEP; ++k) {
     const int cur = PIPE ? (k & 1) : 0;
-    const int c = c_lo + 32 * k;
+    const int c = lncol(k);
     if (!PIPE && k > 0) tmem_ld32(taddr + tcol(c), r[0]);
     tmem_ld_wait_regs(r[cur]);
-    if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + tcol(c + 32), r[cur ^ 1]);
+    if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + tcol(lncol(k + 1)), r[cur ^ 1]);
     uint32_t p[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {

@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
         }
       } else {
         // LayerNorm over the full row (BN == N), two warps per row (column halves): epi_ln.cuh
-        const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + c_lo};
+        const ResidualGlobal rg{res + size_t(ok ? row : 0) * N};
         uint8_t* stg = sStg + (warp - 4) * T::STG_BUFS * 2048;
         ln_epilogue<BN, T::HALF>(taddr, c_lo, rg, s_bias, s_gamma, s_beta, stats + (it & 1) * 2 * BM, q, hh, lane,
                                  eps, [&] {

@@ -55,6 +55,12 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 // uniform constant-cache loads instead of shared-memory loads in the LN epilogues (the LNs are MIO-bound)
 #define MLP_LN_CPARAM 0              // 1 measured slower (tail 392 -> 403 ms per 2M texts: LDC.64 per pair)
 #endif
+#ifndef MLP_X1_CHASE
+// SPLIT: G1 of chunk 0 starts k-block by k-block as LN0's pass 2 (interleaved columns, epi_ln.cuh) completes
+// each 64-column block of X1, instead of after the whole LN0 (k-blocks 0, 1 also wait until the H columns
+// holding G0's first 128 output columns have been read)
+#define MLP_X1_CHASE 1
+#endif
 #ifndef MLP_STORE_DIRECT
 #define MLP_STORE_DIRECT 0          // 1: final LN output as 32-byte stores from registers (measured equal)
 #endif
@@ -138,9 +144,8 @@ __device__ const char* const g_mtl_names[M_N] = {"a_full(iss)", "g0_issued", "y0
 // 16-byte chunk j at (j ^ (r & 7)) * 16).
 struct ResidualSmemA {
   const uint8_t* sA;
-  int row, c_lo;
-  __device__ __forceinline__ void operator()(int k, uint32_t (&rr)[16]) const {
-    const int c = c_lo + 32 * k;
+  int row, c_lo;   // c_lo unused (the LN epilogue passes absolute columns)
+  __device__ __forceinline__ void operator()(int c, uint32_t (&rr)[16]) const {
     const uint8_t* base = sA + (c >> 6) * (MBM * 128) + row * 128;
     const int j0 = (c & 63) >> 3;
 #pragma unroll
@@ -175,6 +180,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
   using T = MlpCfg<D>;
   constexpr int EPI_WARPS = T::EPI_WARPS, NP = T::NP, HC = T::HC;
   constexpr bool SPLIT = OP && MLP_PINGPONG && MLP_G0SPLIT && D == 384;   // G0 in column blocks 128 + 256
+  constexpr bool CHASE = SPLIT && MLP_X1_CHASE && NP == 2;
   constexpr int KB1 = T::KB1;
   constexpr int S1 = KB1 == 1 ? 1 : KB1 / 3;         // ring stages per W1 chunk
   constexpr int KPS = KB1 == 1 ? 1 : 3;              // W1 k-blocks per stage
@@ -195,7 +201,8 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
   uint64_t* x1_ready = y0_full + 1;                          // leader (OP), 2 x EPI_WARPS: X1 in A
   uint64_t* xres_full = x1_ready + 1;                         // local (OP): X residual rows landed in A
   uint64_t* okb_free = xres_full + 1;                         // [KB1] both (OP): G0 done with O k-block kb
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(okb_free + KB1);
+  uint64_t* x1kb = okb_free + KB1;                            // [KB1] leader (OP), 2 x EPI_WARPS: X1 k-block kb in A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x1kb + KB1);
   uint8_t* const sR0 = smem + T::HEAD;                       // [KB1][128 x 128 B] (PINGPONG: region 0)
   uint8_t* sHs = sR0 + (MLP_PINGPONG ? T::REGION : T::A_BYTES);   // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
@@ -235,6 +242,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
     mbar_init(x1_ready, 2 * EPI_WARPS);
     mbar_init(xres_full, 1);
     for (int kb = 0; kb < KB1; ++kb) mbar_init(&okb_free[kb], 1);
+    for (int kb = 0; kb < KB1; ++kb) mbar_init(&x1kb[kb], 2 * EPI_WARPS);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -438,6 +446,10 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         MW(y_empty, (uiu & 1) ^ 1, 0);               // LN of the previous unit drained Y
         tc_fence_after();
       }
+      if (CHASE && c == 0) {
+        MW(x1_ready, uiu & 1, 1);                    // LN0 has read all of Y0 (G2 overwrites Y)
+        tc_fence_after();
+      }
       MW(hs_full, gc & 1, 1);                        // both CTAs' Hs(c) written
       tc_fence_after();
       for (int kb = 0; kb < 2; ++kb, ++sc) {
@@ -526,9 +538,11 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         if (elect_one()) tc_commit_pair_mc(y0_full, 0x3);
         __syncwarp();
         MTL(M_G0ISS, ui);
-        MW(x1_ready, ui & 1, 1);                      // both CTAs' X1 written into A
-        MTL(M_X1R, ui);
-        tc_fence_after();
+        if constexpr (!CHASE) {
+          MW(x1_ready, ui & 1, 1);                    // both CTAs' X1 written into A
+          MTL(M_X1R, ui);
+          tc_fence_after();
+        }
       } else if constexpr (OP) {
         // G0: Y = O Wo^T (the previous unit's final LN has drained Y)
         MW(y_empty, (ui & 1) ^ 1, 0);
@@ -565,6 +579,24 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
           const int s = int(sc % RING);
           MW(&full[s], (sc / RING) & 1, 2);
           tc_fence_after();
+          if (CHASE && c == 0) {
+            // chunk 0 chases LN0's pass 2: k-block kb once X1 k-block kb (and, for kb <= 1, the H reads) is done
+            for (int j = 0; j < KPS; ++j) {
+              const int kb = s2 * KPS + j;
+              MW(&x1kb[kb < 1 ? 1 : kb], ui & 1, 1);
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t ad = a_desc0 + uint64_t((kb * MBM * 128) >> 4);
+                const uint64_t bd = w_desc0 + uint64_t((s * STAGE + j * 64 * 128) >> 4);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  tc_mma_bf16_pair(tmem_base + H_COL, ad + uint64_t(k * 2), bd + uint64_t(k * 2), idesc1, (kb | k) != 0);
+                if (j == KPS - 1) tc_commit_pair_mc(&empty[s], 0x3);
+              }
+              __syncwarp();
+            }
+            if (s2 == 0) MTL(M_X1R, ui);
+          } else {
           if (elect_one()) {
             const uint64_t bd0 = w_desc0 + uint64_t((s * STAGE) >> 4);
             for (int j = 0; j < KPS; ++j) {
@@ -578,6 +610,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
             tc_commit_pair_mc(&empty[s], 0x3);
           }
           __syncwarp();
+          }
         }
         if (elect_one()) {
           tc_commit_pair_mc(h_full, 0x3);
@@ -668,6 +701,12 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
                                 for (int i = 0; i < 4; ++i)
                                   *reinterpret_cast<uint4*>(base + (((j0 + i) ^ (row_l & 7)) << 4)) =
                                       make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+                                if constexpr (CHASE) {   // X1 k-block col / 64: this warp's 32 columns are in
+                                  fence_proxy_async_smem();
+                                  tc_fence_before();
+                                  __syncwarp();
+                                  if (lane == 0) mbar_arrive_cluster_release(mapa_shared(smem_u32(&x1kb[col >> 6]), 0));
+                                }
                               });
         tc_fence_before();                     // Y reads done before G2(0) may accumulate into Y
         fence_proxy_async_smem();              // X1 (generic writes) -> visible to the MMA

@@ -68,10 +68,12 @@ struct LnNoOp {
 // pass1_done() runs once the residual has been read for the last time (after pass 1).
 // REMAP_LO > 0: accumulator columns [0, REMAP_LO) live at TMEM column REMAP_BASE + c instead of c (the fused
 // tail's split out-projection, mlp_tc.cu MLP_G0SPLIT).
-template <int BN, int HALF, bool PIPE = true, uint32_t REMAP_LO = 0, uint32_t REMAP_BASE = 0, typename Res,
-          typename Ready, typename Store, typename P1 = LnNoOp, int NP = BN / HALF>
-__device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const float* s_bias,
-                                            const float* s_gamma, const float* s_beta, float4* stats, int q, int hh,
+// CT = float: bias / gamma / beta as fp32 in shared memory; CT = uint16_t: as bf16 (the weight blob's own
+// precision, so the same values), half the shared-memory loads (the LN passes are MIO-bound).
+template <int BN, int HALF, bool PIPE = true, uint32_t REMAP_LO = 0, uint32_t REMAP_BASE = 0, typename CT = float,
+          typename Res, typename Ready, typename Store, typename P1 = LnNoOp, int NP = BN / HALF>
+__device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const CT* s_bias,
+                                            const CT* s_gamma, const CT* s_beta, float4* stats, int q, int hh,
                                             int lane, float eps, Ready&& wait_ready, Store&& store,
                                             P1&& pass1_done = P1{}) {
 #ifdef LN_TRACE
@@ -104,11 +106,24 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
       load_res(lncol(k + 1), rs[cur ^ 1]);
     }
     const uint32_t (&rr)[16] = rs[cur];
-    if (k == 0) shift = __uint_as_float(r[cur][0]) + s_bias[c] + bf16lo(rr[0]);
+    uint4 cb[4];                                        // CT = bf16: this step's 32 bias values
+    if constexpr (sizeof(CT) == 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cb[j] = reinterpret_cast<const uint4*>(s_bias + c)[j];
+    }
+    auto bias2 = [&](int i) -> float2 {                 // bias of columns c + 2i, c + 2i + 1
+      if constexpr (sizeof(CT) == 2) {
+        const uint32_t u = (&cb[i >> 2].x)[i & 3];
+        return make_float2(bf16lo(u), bf16hi(u));
+      } else {
+        return *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
+      }
+    };
+    if (k == 0) shift = __uint_as_float(r[cur][0]) + bias2(0).x + bf16lo(rr[0]);
     uint32_t w[32];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float2 bb = *reinterpret_cast<const float2*>(s_bias + c + 2 * i);
+      const float2 bb = bias2(i);
       const f32x2 v = fadd2(fadd2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])),
                                   f2(bb.x, bb.y)),
                             f2(bf16lo(rr[i]), bf16hi(rr[i])));
@@ -167,10 +182,25 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
     tmem_ld_wait_regs(r[cur]);
     if (PIPE && k + 1 < NSTEP) tmem_ld32(taddr + tcol(lncol(k + 1)), r[cur ^ 1]);
     uint32_t p[16];
+    uint4 cg[4], ce[4];
+    if constexpr (sizeof(CT) == 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cg[j] = reinterpret_cast<const uint4*>(s_gamma + c)[j];
+        ce[j] = reinterpret_cast<const uint4*>(s_beta + c)[j];
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float2 gg = *reinterpret_cast<const float2*>(s_gamma + c + 2 * i);
-      const float2 be = *reinterpret_cast<const float2*>(s_beta + c + 2 * i);
+      float2 gg, be;
+      if constexpr (sizeof(CT) == 2) {
+        const uint32_t ug = (&cg[i >> 2].x)[i & 3], ue = (&ce[i >> 2].x)[i & 3];
+        gg = make_float2(bf16lo(ug), bf16hi(ug));
+        be = make_float2(bf16lo(ue), bf16hi(ue));
+      } else {
+        gg = *reinterpret_cast<const float2*>(s_gamma + c + 2 * i);
+        be = *reinterpret_cast<const float2*>(s_beta + c + 2 * i);
+      }
       const f32x2 z = ffma2(f2(__uint_as_float(r[cur][2 * i]), __uint_as_float(r[cur][2 * i + 1])), k_rstd, k_off);
       const f32x2 y = ffma2(z, f2(gg.x, gg.y), f2(be.x, be.y));
       p[i] = pack_bf16x2(f2lo(y), f2hi(y));

@@ -61,6 +61,11 @@ constexpr int FC = 128;             // ff columns per chunk (H accumulator colum
 // holding G0's first 128 output columns have been read)
 #define MLP_X1_CHASE 1
 #endif
+#ifndef MLP_LN_BF16
+// LayerNorm constants staged in shared memory as bf16 (the weight blob's precision: the same values), half
+// the shared-memory loads of the MIO-bound LN passes
+#define MLP_LN_BF16 0               // 1 measured slower (tail 390 -> 398 ms per 2M texts: the unpacking costs more issue slots than the halved loads save)
+#endif
 #ifndef MLP_STORE_DIRECT
 #define MLP_STORE_DIRECT 0          // 1: final LN output as 32-byte stores from registers (measured equal)
 #endif
@@ -206,9 +211,15 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
   uint8_t* const sR0 = smem + T::HEAD;                       // [KB1][128 x 128 B] (PINGPONG: region 0)
   uint8_t* sHs = sR0 + (MLP_PINGPONG ? T::REGION : T::A_BYTES);   // [2][128 x 128 B]
   float4* stats = reinterpret_cast<float4*>(sHs + T::LN_STG); // LN only
-  float* s_b2 = reinterpret_cast<float*>(stats + NP * MBM);  // LN only
-  float* s_gamma = s_b2 + D;
-  float* s_beta = s_gamma + D;
+  using CT = std::conditional_t<MLP_LN_BF16 != 0, uint16_t, float>;   // LN constants in smem
+  static_assert(!(MLP_LN_BF16 && MLP_LN_CPARAM), "one LN-constant path");
+  CT* s_b2 = reinterpret_cast<CT*>(stats + NP * MBM);        // LN only
+  CT* s_gamma = s_b2 + D;
+  CT* s_beta = s_gamma + D;
+  auto to_ct = [](float v) -> CT {
+    if constexpr (sizeof(CT) == 2) return CT(pack_bf16x2(v, 0.f) & 0xffffu);
+    else return v;
+  };
   uint8_t* const sR1 = sHs + T::SCRATCH;                     // [RING][STAGE] (PINGPONG: region 1)
   // unit ui: A tile in region ui % 2, weight ring in the other (fixed roles without PINGPONG)
   auto region_a = [&](int ui) { return (MLP_PINGPONG && (ui & 1)) ? sR1 : sR0; };
@@ -671,7 +682,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < PER; ++i) {     // Hs idle: the previous unit's LN is done, chunk 0 not yet
             const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
-            if (k < 3 * D) s_b2[k] = cv[i];
+            if (k < 3 * D) s_b2[k] = to_ct(cv[i]);
           }
           asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
         }
@@ -685,10 +696,10 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
         tc_fence_after();
         if (false)
 #endif
-        const float* c_b = MLP_LN_CPARAM ? lc.v : s_b2;
-        const float* c_g = MLP_LN_CPARAM ? lc.v + D : s_gamma;
-        const float* c_e = MLP_LN_CPARAM ? lc.v + 2 * D : s_beta;
-        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE), SPLIT ? 128u : 0u, H_COL>(t_row, hh * (D / NP), rg, c_b, c_g, c_e, stats, q, hh, lane, eps,
+        const CT* c_b = MLP_LN_CPARAM ? reinterpret_cast<const CT*>(lc.v) : s_b2;
+        const CT* c_g = MLP_LN_CPARAM ? reinterpret_cast<const CT*>(lc.v + D) : s_gamma;
+        const CT* c_e = MLP_LN_CPARAM ? reinterpret_cast<const CT*>(lc.v + 2 * D) : s_beta;
+        ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE), SPLIT ? 128u : 0u, H_COL, CT>(t_row, hh * (D / NP), rg, c_b, c_g, c_e, stats, q, hh, lane, eps,
                               [&] {
                                 mbar_wait(y0_full, ui & 1);
                                 MTL(M_Y0, ui);
@@ -791,7 +802,7 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
           const int k = threadIdx.x - 128 + i * EPI_WARPS * 32;
-          if (k < 3 * D) s_b2[k] = cv[i];
+          if (k < 3 * D) s_b2[k] = to_ct(cv[i]);
         }
         asm volatile("bar.sync 5, %0;" ::"r"(EPI_WARPS * 32) : "memory");
       }
@@ -805,10 +816,10 @@ __global__ void __launch_bounds__(MlpCfg<D>::THREADS, 1)
       if (lane == 0) mbar_arrive(a_free);
       if (false)
 #endif
-      const float* f_b = MLP_LN_CPARAM ? lc.v + 3 * D : s_b2;
-      const float* f_g = MLP_LN_CPARAM ? lc.v + 4 * D : s_gamma;
-      const float* f_e = MLP_LN_CPARAM ? lc.v + 5 * D : s_beta;
-      ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE)>(t_row, hh * (D / NP), ra, f_b, f_g, f_e, stats, q, hh, lane, eps,
+      const CT* f_b = MLP_LN_CPARAM ? reinterpret_cast<const CT*>(lc.v + 3 * D) : s_b2;
+      const CT* f_g = MLP_LN_CPARAM ? reinterpret_cast<const CT*>(lc.v + 4 * D) : s_gamma;
+      const CT* f_e = MLP_LN_CPARAM ? reinterpret_cast<const CT*>(lc.v + 5 * D) : s_beta;
+      ln_epilogue<D, D / NP, (NP <= 2 || MLP_LN_PIPE), 0u, 0u, CT>(t_row, hh * (D / NP), ra, f_b, f_g, f_e, stats, q, hh, lane, eps,
                             [&] {
                               mbar_wait(y_full, ui & 1);
                               tc_fence_after();

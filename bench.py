@@ -51,6 +51,8 @@ def parse():
                     help="1: K4 QKV GEMM + K5 attention as one kernel (default); 0: separate kernels")
     ap.add_argument("--att-tc", type=int, default=0, choices=[0, 1],
                     help="fused QKV + attention with S and P V on tcgen05 (0: mma.sync attention epilogue)")
+    ap.add_argument("--ln-pair", type=int, default=1, choices=[0, 1],
+                    help="d in {768, 1024}: LN GEMMs as cluster pairs (0: fp32 pre-LN rows + LayerNorm kernel)")
     ap.add_argument("--mlp-fused", type=int, default=1, choices=[0, 1],
                     help="1: K7 FFN1+GELU and K8 FFN2+LN as one kernel (default); 0: separate GEMMs")
     ap.add_argument("--tail-fused", type=int, default=1, choices=[0, 1],
@@ -335,6 +337,7 @@ def main():
         h = N.surge_create(cfg, blob_dev, n_weights=n_w)
     N.surge_set_option(h, N.SURGE_OPT_ATT_FUSED, args.att_fused)
     N.surge_set_option(h, N.SURGE_OPT_ATT_TC, args.att_tc)
+    N.surge_set_option(h, N.SURGE_OPT_LN_PAIR, args.ln_pair)
     N.surge_set_option(h, N.SURGE_OPT_MLP_FUSED, args.mlp_fused)
     N.surge_set_option(h, N.SURGE_OPT_TAIL_FUSED, args.tail_fused)
     stream = torch.cuda.Stream(device=dev)

@@ -395,6 +395,11 @@ typedef struct {
  *     mma.sync in the GEMM epilogue.  Same bf16 Q/K/V/P values and softmax formula; the fp32
  *     accumulation order differs, so the two agree to rounding (not bit for bit). */
 #define SURGE_OPT_ATT_TC 5
+/*   SURGE_OPT_LN_PAIR (default 1; hidden size 768 or 1024): the out-projection and FFN2 GEMMs fuse their
+ *     residual + LayerNorm, a cluster of two CTAs splitting each row and exchanging the row statistics
+ *     through distributed shared memory; 0 = fp32 pre-LN rows to HBM + a row-LayerNorm kernel.  The fp32
+ *     summation order of the statistics differs between the two (agreement to rounding). */
+#define SURGE_OPT_LN_PAIR 6
 surge_status surge_set_option(surge_handle h, int32_t option, int64_t value);
 
 surge_status surge_profile_enable(surge_handle h, int32_t on);   /* on: clears counters */

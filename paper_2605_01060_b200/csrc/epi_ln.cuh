@@ -59,10 +59,34 @@ __device__ __forceinline__ void store_rows_32x32(uint8_t* stg, const uint32_t (&
   }
 }
 
+// The same 32 rows x 32 columns stored straight from registers: each lane writes its row's 64 bytes as
+// two 32-byte stores (STG.256, whole L2 sectors) -- no shared-memory transpose.
+__device__ __forceinline__ void store_row_64B(const uint32_t (&p)[16], int lane, uint16_t* out, int64_t row0,
+                                              int64_t rows, int ld, int col) {
+  if (row0 + lane < rows) {
+    uint16_t* dst = out + size_t(row0 + lane) * ld + col;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * i), "r"(p[8 * i]),
+                   "r"(p[8 * i + 1]), "r"(p[8 * i + 2]), "r"(p[8 * i + 3]), "r"(p[8 * i + 4]), "r"(p[8 * i + 5]),
+                   "r"(p[8 * i + 6]), "r"(p[8 * i + 7])
+                   : "memory");
+  }
+}
+
 // NP warps share a lane quadrant, each owning HALF = BN / NP columns (part hh).  PIPE: TMEM loads and
 // residual loads one step ahead (2 register buffers); !PIPE: one buffer (for register-limited kernels).
 struct LnNoOp {
   __device__ __forceinline__ void operator()() const {}
+};
+// Row statistics merge over the parts of one CTA (default) -- or, for a row split over a cluster of CTAs,
+// a publisher that also writes this part's (shift, S1, S2) into the peer CTAs' stats array and waits for
+// theirs (ln_pair.cu): part_off = index of this CTA's first part, NPM = parts in the merge.
+struct LnLocalMerge {
+  static constexpr int NPM = 0;   // 0: the CTA's own NP parts
+  __device__ __forceinline__ int part_off() const { return 0; }
+  __device__ __forceinline__ void publish(int, int, float4) const {}
+  __device__ __forceinline__ void wait() const {}
 };
 
 // pass1_done() runs once the residual has been read for the last time (after pass 1).
@@ -71,11 +95,13 @@ struct LnNoOp {
 // CT = float: bias / gamma / beta as fp32 in shared memory; CT = uint16_t: as bf16 (the weight blob's own
 // precision, so the same values), half the shared-memory loads (the LN passes are MIO-bound).
 template <int BN, int HALF, bool PIPE = true, uint32_t REMAP_LO = 0, uint32_t REMAP_BASE = 0, typename CT = float,
-          typename Res, typename Ready, typename Store, typename P1 = LnNoOp, int NP = BN / HALF>
+          typename Merge = LnLocalMerge, typename Res, typename Ready, typename Store, typename P1 = LnNoOp,
+          int NP = BN / HALF>
 __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res& load_res, const CT* s_bias,
                                             const CT* s_gamma, const CT* s_beta, float4* stats, int q, int hh,
                                             int lane, float eps, Ready&& wait_ready, Store&& store,
-                                            P1&& pass1_done = P1{}) {
+                                            P1&& pass1_done = P1{}, const Merge& merge = Merge{}) {
+  constexpr int NPM = Merge::NPM > 0 ? Merge::NPM : NP;   // parts in the statistics merge
 #ifdef LN_TRACE
   long long _lt = 0;
 #endif
@@ -139,12 +165,15 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
   pass1_done();
   LNT(1);
   const float S1 = f2lo(s1) + f2hi(s1), S2 = f2lo(s2) + f2hi(s2);
-  stats[hh * 128 + q * 32 + lane] = make_float4(shift, S1, S2, 0.f);
+  const float4 mine = make_float4(shift, S1, S2, 0.f);
+  stats[(merge.part_off() + hh) * 128 + q * 32 + lane] = mine;
+  merge.publish(merge.part_off() + hh, q * 32 + lane, mine);
   asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NP) : "memory");   // the NP warps of this quadrant
+  merge.wait();
   LNT(2);
   const float nh = float(HALF);
   float mean, var;
-  if constexpr (NP == 2) {
+  if constexpr (NPM == 2) {
     const float4 o = stats[(hh ^ 1) * 128 + q * 32 + lane];
     const float mean_a = shift + S1 / nh, m2_a = S2 - S1 * S1 / nh;
     const float mean_b = o.x + o.y / nh, m2_b = o.z - o.y * o.y / nh;
@@ -152,24 +181,24 @@ __device__ __forceinline__ void ln_epilogue(uint32_t taddr, int c_lo, const Res&
     mean = 0.5f * (mean_a + mean_b);
     var = fmaxf((m2_a + m2_b + dm * dm * (nh * 0.5f)) / float(BN), 0.f);
   } else {
-    // Chan's parallel merge of NP equal-size parts, in part order (identical in every warp)
-    float mp[NP], m2p[NP];
+    // Chan's parallel merge of NPM equal-size parts, in part order (identical in every warp and CTA)
+    float mp[NPM], m2p[NPM];
     float msum = 0.f;
 #pragma unroll
-    for (int i = 0; i < NP; ++i) {
+    for (int i = 0; i < NPM; ++i) {
       const float4 o = stats[i * 128 + q * 32 + lane];
       mp[i] = o.x + o.y / nh;
       m2p[i] = o.z - o.y * o.y / nh;
       msum += mp[i];
     }
-    mean = msum * (1.0f / NP);
+    mean = msum * (1.0f / NPM);
     float m2 = 0.f;
 #pragma unroll
-    for (int i = 0; i < NP; ++i) {
+    for (int i = 0; i < NPM; ++i) {
       const float dm = mp[i] - mean;
       m2 += m2p[i] + nh * dm * dm;
     }
-    var = fmaxf(m2 / float(BN), 0.f);
+    var = fmaxf(m2 / float(NPM * HALF), 0.f);
   }
   const float rstd = rsqrtf(var + eps);
   const f32x2 k_rstd = f2(rstd, rstd), k_off = f2(-mean * rstd, -mean * rstd);

@@ -82,6 +82,10 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st);
 // tensor-core MMAs with Q and P read from TMEM.  d = 384, d_h = 32 (MiniLM class); same arguments as
 // the EPI_QKV_ATTN GEMM (text-aligned tile records, permuted W_qkv with 96-row TMA boxes).
 bool qkv_attn_tc_supported(int d, int heads);
+// K6 / K8 with the LayerNorm fused for d in {768, 1024} (ln_pair.cu): a cluster of two CTAs splits the row,
+// statistics exchanged through distributed shared memory.  B = the weight with 64-row TMA boxes.
+bool ln_pair_supported(int d, int k);
+cudaError_t launch_ln_pair(const GemmArgs& g, cudaStream_t st);
 cudaError_t launch_qkv_attn_tc(const GemmArgs& g, cudaStream_t st);
 // LN GEMMs fuse the LayerNorm into the epilogue when the full row fits one CTA's TMEM (d in {64, 384});
 // otherwise they write fp32 pre-LN rows (EPI_BIAS_RES) and launch_layernorm finishes them.
@@ -176,6 +180,7 @@ struct LayerW {
   CUtensorMap tm_wqkv, tm_wo, tm_w1, tm_w2;
   CUtensorMap tm_wo_mlp, tm_w1_mlp, tm_w2_mlp;   // fused tail (mlp_tc.cu) views of Wo / W1 / W2
   CUtensorMap tm_wo64;                            // Wo, 64-row boxes (split out-projection in the tail)
+  CUtensorMap tm_wo_p64, tm_w2_p64;               // d in {768, 1024}: Wo / W2 with 64-row boxes (ln_pair.cu)
   std::vector<float> ln_host;                     // host [bo | ln1_g | ln1_b | b2 | ln2_g | ln2_b] (tail kernel parameter)
   uint16_t* wqkv_att = nullptr;       // W_qkv rows permuted into head-complete 192-row slices
   float* bqkv_att = nullptr;
@@ -243,6 +248,7 @@ class DeviceModel {
   // fused QKV + attention kernel on/off (on by default; off = separate K4 GEMM + K5 kernels)
   void set_att_fused(bool on) { att_fused_ = on; }
   void set_att_tc(bool on) { att_tc_ = on; }
+  void set_ln_pair(bool on) { ln_pair_ = on; }
   bool att_fused() const { return att_fused_; }
   // fused MLP kernel on/off (on by default; off = separate K7 GELU GEMM + K8 LN GEMM)
   void set_mlp_fused(bool on) { mlp_fused_ = on; }
@@ -258,6 +264,7 @@ class DeviceModel {
   ModelShape s_{};
   bool att_fused_ = true;
   bool att_tc_ = false;       // fused QKV + attention on tcgen05 where supported (qkv_attn_tc.cu)
+  bool ln_pair_ = true;       // d in {768, 1024}: LN GEMMs as cluster pairs (ln_pair.cu) instead of fp32 rows + LN kernel
   bool mlp_fused_ = true;
   bool tail_fused_ = true;
   int pooling_ = 0;

@@ -1,0 +1,270 @@
+// ln_pair.cu -- K6 / K8 for hidden sizes whose LayerNorm row does not fit one CTA's TMEM (d = 768, 1024:
+// the bge-base / bge-large classes):  C = LN(A B^T + b + R) * gamma + beta.
+//
+// A cluster of two CTAs (cta_group::1 each) shares a 128-row M tile and splits the d output columns: CTA r
+// owns columns [r d/2, (r+1) d/2) -- its accumulator (384 or 512 fp32 columns) fills its TMEM.  The row
+// statistics cross the pair through distributed shared memory: after its first LN pass each epilogue warp
+// writes its part's (shift, S1, S2) into both CTAs' stats arrays (st.shared::cluster) and arrives on the
+// peer's mbarrier (release.cluster); every warp then merges the four parts in the same order (Chan), so
+// both halves of a row are normalised with identical mean and variance.  The fp32 pre-LN rows never reach
+// HBM (the separate path writes them and runs a row-LayerNorm kernel: 4 + 4 + 2 bytes per element more).
+//
+// Warps: 0, 2, 3 TMA producers (A box + this CTA's B rows per k-block, ring of STAGES); 1 MMA issuer; 2
+// also allocates TMEM; 4..11 epilogue (epi_ln.cuh, 2 warps per lane quadrant).  Persistent over M tiles
+// (tile = cluster index, stride = number of clusters).  One accumulator: the epilogue of tile t and the
+// mainloop of tile t + 1 do not overlap (as in the d = 384 LN GEMM).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "epi_ln.cuh"
+#include "internal.h"
+
+namespace surge {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 128 + 32 * EPI_WARPS;
+
+template <int BNC>   // columns per CTA: 384 (d = 768) or 512 (d = 1024)
+struct LnPairCfg {
+  static constexpr int N_MMA = BNC / 256 >= 2 ? BNC / 256 : 2;   // 384: 2 x 192, 512: 2 x 256
+  static constexpr int MMA_N = BNC / N_MMA;
+  static constexpr int A_STAGE = BM * 128;                    // 16 KB
+  static constexpr int B_STAGE = BNC * 128;                   // 48 / 64 KB
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int HEAD = 1024;
+  static constexpr int STATS = 2 * 4 * BM * 16;               // [tile parity][4 parts][128 rows] float4
+  static constexpr int CONSTS = 3 * BNC * 4;                  // bias, gamma, beta of this CTA's columns
+  static constexpr int FIXED = HEAD + STATS + ((CONSTS + 1023) / 1024) * 1024;
+  static constexpr int STAGES = (227 * 1024 - FIXED) / STAGE;
+  static constexpr int SMEM = FIXED + STAGES * STAGE;
+  static_assert(STAGES >= 2, "ring");
+};
+
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// The peer's statistics: this part's (shift, S1, S2) also lands in the peer CTA's stats array (same smem
+// offset) and the warp arrives on the peer's `pstats`; wait() blocks on this CTA's own `pstats`.
+struct PairMerge {
+  static constexpr int NPM = 4;
+  int off;              // 2 * cluster rank
+  uint32_t peer_stats;  // shared::cluster address of the peer's stats array (this tile's slot)
+  uint32_t peer_bar;    // shared::cluster address of the peer's pstats barrier
+  uint64_t* my_bar;
+  uint32_t parity;
+  int lane;
+  __device__ __forceinline__ int part_off() const { return off; }
+  __device__ __forceinline__ void publish(int part, int row, float4 v) const {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(peer_stats + uint32_t((part * 128 + row) * 16)),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(peer_bar) : "memory");
+  }
+  __device__ __forceinline__ void wait() const { mbar_wait_acq_cluster(my_bar, parity); }
+};
+
+template <int BNC>
+__global__ void __launch_bounds__(THREADS, 1)
+    ln_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
+                   const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
+                   float eps) {
+  using T = LnPairCfg<BNC>;
+  constexpr int STAGES = T::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [STAGES]
+  uint64_t* empty = full + STAGES;                      // [STAGES]
+  uint64_t* tfull = empty + STAGES;                     // accumulator complete (commit)
+  uint64_t* tempty = tfull + 1;                         // accumulator drained (8 epilogue warps)
+  // [2] the peer's 8 epilogue warps published tile it's statistics (barrier it % 2): two barriers, so the peer
+  // (which may publish tile it + 1 before this CTA waits for tile it) can never complete a phase this CTA
+  // has not observed yet
+  uint64_t* pstats = tempty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pstats + 2);
+  float4* stats = reinterpret_cast<float4*>(smem + T::HEAD);                  // [2][4][128]
+  float* s_bias = reinterpret_cast<float*>(smem + T::HEAD + T::STATS);
+  float* s_gamma = s_bias + BNC;
+  float* s_beta = s_gamma + BNC;
+  uint8_t* sRing = smem + T::FIXED;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = int(cluster_ctarank());
+  const int n0 = rank * BNC;
+  const int t0 = int(blockIdx.x >> 1), dt = int(gridDim.x >> 1);
+  const int m_tiles = (M + BM - 1) / BM;
+  const int num_kb = K / 64;
+
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023u) != 0) __trap();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, EPI_WARPS);
+    mbar_init(&pstats[0], EPI_WARPS);
+    mbar_init(&pstats[1], EPI_WARPS);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  cluster_sync();                        // both CTAs' barriers initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ TMA producers
+      const int p = warp == 0 ? 0 : warp - 1;
+      const uint64_t pol_w = l2_policy_evict_last();
+      griddep_wait();
+      uint32_t c = 0;
+      constexpr int NBOX = 1 + BNC / 64;                  // A + this CTA's B rows in 64-row boxes
+      for (int t = t0; t < m_tiles; t += dt)
+        for (int kb = 0; kb < num_kb; ++kb, ++c) {
+          const int s = int(c % STAGES);
+          const uint32_t ph = (c / STAGES) & 1;
+          for (int b = 0; b < NBOX; ++b) {
+            if (int((c * NBOX + b) % 3) != p) continue;
+            mbar_wait(&empty[s], ph ^ 1);
+            if (b == 0) {
+              mbar_arrive_expect_tx(&full[s], uint32_t(T::STAGE));
+              tma_load_2d(sRing + s * T::STAGE, &tmA, &full[s], kb * 64, t * BM);
+            } else {
+              tma_load_2d_hint(sRing + s * T::STAGE + T::A_STAGE + (b - 1) * 64 * 128, &tmB, &full[s], kb * 64,
+                               n0 + (b - 1) * 64, pol_w);
+            }
+          }
+        }
+    }
+  } else if (warp == 1) {
+    griddep_launch_dependents();
+    // -------------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
+    const uint64_t r0 = umma_desc_sw128(smem_u32(sRing));
+    uint32_t c = 0;
+    int it = 0;
+    for (int t = t0; t < m_tiles; t += dt, ++it) {
+      mbar_wait(tempty, (it & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < num_kb; ++kb, ++c) {
+        const int s = int(c % STAGES);
+        mbar_wait(&full[s], (c / STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ad = r0 + uint64_t((s * T::STAGE) >> 4);
+          const uint64_t bd = r0 + uint64_t((s * T::STAGE + T::A_STAGE) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < T::N_MMA; ++j)
+              tc_mma_bf16(tmem_base + j * T::MMA_N, ad + uint64_t(k * 2),
+                          bd + uint64_t((j * T::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+          tc_commit(&empty[s]);
+          if (kb == num_kb - 1) tc_commit(tfull);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    griddep_wait();
+    // ------------------------------------------------------------------ epilogue (warps 4..11)
+    for (int i = threadIdx.x - 128; i < BNC; i += 32 * EPI_WARPS) {
+      s_bias[i] = bias[n0 + i];
+      s_gamma[i] = gamma[n0 + i];
+      s_beta[i] = beta[n0 + i];
+    }
+    asm volatile("bar.sync 5, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+    const int q = warp & 3, hh = (warp - 4) >> 2;
+    const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
+    const uint32_t peer_bar0 = mapa_shared(smem_u32(pstats), uint32_t(rank ^ 1));
+    int it = 0;
+    for (int t = t0; t < m_tiles; t += dt, ++it) {
+      const int row = t * BM + q * 32 + lane;
+      const bool ok = row < M;
+      float4* st = stats + (it & 1) * 4 * BM;
+      const PairMerge mg{2 * rank, mapa_shared(smem_u32(st), uint32_t(rank ^ 1)), peer_bar0 + uint32_t(8 * (it & 1)),
+                         &pstats[it & 1], uint32_t((it >> 1) & 1), lane};
+      const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + n0};
+      ln_epilogue<BNC, BNC / 2, true, 0u, 0u, float, PairMerge>(
+          taddr, 0, rg, s_bias, s_gamma, s_beta, st, q, hh, lane, eps,
+          [&] {
+            mbar_wait(tfull, it & 1);
+            tc_fence_after();
+          },
+          [&](const uint32_t (&p)[16], int col) { store_row_64B(p, lane, C, int64_t(t) * BM + q * 32, M, N, n0 + col); },
+          LnNoOp{}, mg);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();                        // no remote stats write / arrive may target an exited CTA
+  if (warp == 2) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+template <int BNC>
+cudaError_t launch_t(const GemmArgs& g, cudaStream_t st) {
+  using T = LnPairCfg<BNC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ln_pair_kernel<BNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t m_tiles = (g.M + BM - 1) / BM;
+  const int clusters = int(std::min<int64_t>(m_tiles, (sms > 0 ? sms : 148) / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(2 * clusters));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = size_t(T::SMEM);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, ln_pair_kernel<BNC>, *g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
+                            g.beta, g.C, g.eps);
+}
+
+}  // namespace
+
+bool ln_pair_supported(int d, int k) { return (d == 768 || d == 1024) && k % 64 == 0 && k > 0; }
+
+cudaError_t launch_ln_pair(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0) return cudaSuccess;
+  if (!ln_pair_supported(g.N, g.K)) return cudaErrorInvalidValue;
+  return g.N == 768 ? launch_t<384>(g, st) : launch_t<512>(g, st);
+}
+
+}  // namespace surge

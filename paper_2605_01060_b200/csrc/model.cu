@@ -208,6 +208,10 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(make_tmap_bf16(&L.tm_wo, L.wo, d, d, gemm_b_box_rows(int(d), int(d), ln_epi)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), ln_epi)));
+      if (ln_pair_supported(int(d), int(d))) {
+        SURGE_TRY(make_tmap_bf16(&L.tm_wo_p64, L.wo, d, d, 64));
+        SURGE_TRY(make_tmap_bf16(&L.tm_w2_p64, L.w2, d, f, 64));
+      }
       if (mlp_fused_supported(int(d), int(f))) {
         SURGE_TRY(make_tmap_bf16(&L.tm_wo_mlp, L.wo, d, d, mlp_w2_box_rows(int(d))));
         SURGE_TRY(make_tmap_bf16(&L.tm_w1_mlp, L.w1, f, d, 64));
@@ -394,15 +398,19 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     g.tmA = &tmO; g.tmB = &L.tm_wo; g.tmC = &smX1; g.tmR = &tmX; g.N = d; g.K = d; g.epi = EPI_BIAS_LN; g.bias = L.bo; g.res = ws.X;
     g.gamma = L.ln1_g; g.beta = L.ln1_b; g.C = ws.X1;
     if (P) prof->begin(st, &ev);
+    const bool pair = !fused && ln_pair_ && ln_pair_supported(d, d);
     if (fused) {
       SURGE_TRY(launch_gemm(g, st));
+    } else if (pair) {
+      g.tmB = &L.tm_wo_p64;
+      SURGE_TRY(launch_ln_pair(g, st));
     } else {
       g.epi = EPI_BIAS_RES; g.C = reinterpret_cast<uint16_t*>(ws.V);
       SURGE_TRY(launch_gemm(g, st));
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln1_g, L.ln1_b, s_.eps, ws.X1, st));
     }
     if (P) prof->end(KK_OUT_LN, st, ev, 2 * M * D * D, 2 * (M * D + D * D + 2 * M * D));
-    k += fused ? 1 : 2;
+    k += (fused || pair) ? 1 : 2;
     if (mlp_fused_ && mlp_fused_supported(d, f)) {
       // K7 + K8 fused: X = LN(GELU(X1 W1^T + b1) W2^T + b2 + X1), H stays on chip
       MlpArgs a{&tmX1, &L.tm_w1_mlp, &L.tm_w2_mlp, nullptr, nullptr, nullptr, ntok, d, f, L.b1, L.b2, L.ln2_g, L.ln2_b,
@@ -424,15 +432,19 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
     g.tmA = &tmH; g.tmB = &L.tm_w2; g.tmC = &smX; g.tmR = &tmX1; g.N = d; g.K = f; g.epi = EPI_BIAS_LN; g.bias = L.b2; g.res = ws.X1;
     g.gamma = L.ln2_g; g.beta = L.ln2_b; g.C = ws.X;
     if (P) prof->begin(st, &ev);
+    const bool pair2 = !fused && ln_pair_ && ln_pair_supported(d, f);
     if (fused) {
       SURGE_TRY(launch_gemm(g, st));
+    } else if (pair2) {
+      g.tmB = &L.tm_w2_p64;
+      SURGE_TRY(launch_ln_pair(g, st));
     } else {
       g.epi = EPI_BIAS_RES; g.C = reinterpret_cast<uint16_t*>(ws.V);
       SURGE_TRY(launch_gemm(g, st));
       SURGE_TRY(launch_layernorm(ws.V, ntok, d, L.ln2_g, L.ln2_b, s_.eps, ws.X, st));
     }
     if (P) prof->end(KK_FFN2, st, ev, 2 * M * D * F, 2 * (M * F + D * F + 2 * M * D));
-    k += fused ? 2 : 3;
+    k += (fused || pair2) ? 2 : 3;
   }
   if (P) prof->begin(st, &ev);
   SURGE_TRY(launch_meanpool_l2(ws.X, cu, n, tok0, d, static_cast<uint8_t*>(d_out) + size_t(s0) * d * out_elem_bytes(),

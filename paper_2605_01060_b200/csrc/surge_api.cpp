@@ -1324,6 +1324,10 @@ surge_status surge_set_option(surge_handle h, int32_t option, int64_t value) {
       if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
       c->model.set_att_fused(value != 0);
       return SURGE_OK;
+    case SURGE_OPT_LN_PAIR:
+      if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
+      c->model.set_ln_pair(value != 0);
+      return SURGE_OK;
     case SURGE_OPT_ATT_TC:
       if (value != 0 && value != 1) return SURGE_E_INVALID_ARG;
       c->model.set_att_tc(value != 0);

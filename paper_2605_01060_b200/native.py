@@ -78,6 +78,7 @@ SURGE_OPT_MLP_FUSED = 2
 SURGE_OPT_TAIL_FUSED = 3
 SURGE_OPT_POOLING = 4
 SURGE_OPT_ATT_TC = 5
+SURGE_OPT_LN_PAIR = 6
 SURGE_POOL_MEAN, SURGE_POOL_CLS = 0, 1
 SURGE_F32, SURGE_BF16 = 0, 1
 SURGE_BMAX_LABEL, SURGE_BMAX_SPLIT, SURGE_BMAX_PREFLUSH = 0, 1, 2

@@ -29,15 +29,15 @@ constexpr int BM = 128;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 
-template <int BNC>   // columns per CTA: 384 (d = 768) or 512 (d = 1024)
+template <int BNC, int CL>   // columns per CTA (d / CL), CTAs per cluster
 struct LnPairCfg {
-  static constexpr int N_MMA = BNC / 256 >= 2 ? BNC / 256 : 2;   // 384: 2 x 192, 512: 2 x 256
+  static constexpr int N_MMA = BNC <= 256 ? 1 : 2;            // 192 / 256: one MMA, 384: 2 x 192, 512: 2 x 256
   static constexpr int MMA_N = BNC / N_MMA;
   static constexpr int A_STAGE = BM * 128;                    // 16 KB
   static constexpr int B_STAGE = BNC * 128;                   // 48 / 64 KB
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int HEAD = 1024;
-  static constexpr int STATS = 2 * 4 * BM * 16;               // [tile parity][4 parts][128 rows] float4
+  static constexpr int STATS = 2 * 2 * CL * BM * 16;          // [tile parity][2 CL parts][128 rows] float4
   static constexpr int CONSTS = 3 * BNC * 4;                  // bias, gamma, beta of this CTA's columns
   static constexpr int FIXED = HEAD + STATS + ((CONSTS + 1023) / 1024) * 1024;
   static constexpr int STAGES = (227 * 1024 - FIXED) / STAGE;
@@ -55,34 +55,45 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t pa
       : "memory");
 }
 
-// The peer's statistics: this part's (shift, S1, S2) also lands in the peer CTA's stats array (same smem
-// offset) and the warp arrives on the peer's `pstats`; wait() blocks on this CTA's own `pstats`.
+// The peers' statistics: this part's (shift, S1, S2) also lands in every peer CTA's stats array (same
+// smem offset) and the warp arrives on each peer's `pstats`; wait() blocks on this CTA's own `pstats`.
+template <int CL>
 struct PairMerge {
-  static constexpr int NPM = 4;
+  static constexpr int NPM = 2 * CL;
   int off;              // 2 * cluster rank
-  uint32_t peer_stats;  // shared::cluster address of the peer's stats array (this tile's slot)
-  uint32_t peer_bar;    // shared::cluster address of the peer's pstats barrier
+  uint32_t stats_cta;   // this CTA's stats slot (shared::cta address)
+  uint32_t bar_cta;     // this tile's pstats barrier (shared::cta address) in every CTA
   uint64_t* my_bar;
   uint32_t parity;
-  int lane;
+  int lane, rank;
   __device__ __forceinline__ int part_off() const { return off; }
   __device__ __forceinline__ void publish(int part, int row, float4 v) const {
-    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(peer_stats + uint32_t((part * 128 + row) * 16)),
-                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                 : "memory");
+#pragma unroll
+    for (int pr = 1; pr < CL; ++pr) {
+      const uint32_t peer = uint32_t((rank + pr) % CL);
+      asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                       mapa_shared(stats_cta + uint32_t((part * 128 + row) * 16), peer)),
+                   "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                   : "memory");
+    }
     __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(peer_bar) : "memory");
+    if (lane == 0)
+#pragma unroll
+      for (int pr = 1; pr < CL; ++pr)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                         mapa_shared(bar_cta, uint32_t((rank + pr) % CL)))
+                     : "memory");
   }
   __device__ __forceinline__ void wait() const { mbar_wait_acq_cluster(my_bar, parity); }
 };
 
-template <int BNC>
+template <int BNC, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
     ln_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, const float* __restrict__ bias, const uint16_t* __restrict__ res,
                    const float* __restrict__ gamma, const float* __restrict__ beta, uint16_t* __restrict__ C,
                    float eps) {
-  using T = LnPairCfg<BNC>;
+  using T = LnPairCfg<BNC, CL>;
   constexpr int STAGES = T::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [STAGES]
@@ -94,7 +105,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // has not observed yet
   uint64_t* pstats = tempty + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pstats + 2);
-  float4* stats = reinterpret_cast<float4*>(smem + T::HEAD);                  // [2][4][128]
+  float4* stats = reinterpret_cast<float4*>(smem + T::HEAD);                  // [2][2 CL][128]
   float* s_bias = reinterpret_cast<float*>(smem + T::HEAD + T::STATS);
   float* s_gamma = s_bias + BNC;
   float* s_beta = s_gamma + BNC;
@@ -103,7 +114,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = int(cluster_ctarank());
   const int n0 = rank * BNC;
-  const int t0 = int(blockIdx.x >> 1), dt = int(gridDim.x >> 1);
+  const int t0 = int(blockIdx.x) / CL, dt = int(gridDim.x) / CL;
   const int m_tiles = (M + BM - 1) / BM;
   const int num_kb = K / 64;
 
@@ -117,8 +128,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, EPI_WARPS);
-    mbar_init(&pstats[0], EPI_WARPS);
-    mbar_init(&pstats[1], EPI_WARPS);
+    mbar_init(&pstats[0], (CL - 1) * EPI_WARPS);
+    mbar_init(&pstats[1], (CL - 1) * EPI_WARPS);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -195,16 +206,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("bar.sync 5, %0;" ::"r"(32 * EPI_WARPS) : "memory");
     const int q = warp & 3, hh = (warp - 4) >> 2;
     const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16);
-    const uint32_t peer_bar0 = mapa_shared(smem_u32(pstats), uint32_t(rank ^ 1));
+
     int it = 0;
     for (int t = t0; t < m_tiles; t += dt, ++it) {
       const int row = t * BM + q * 32 + lane;
       const bool ok = row < M;
-      float4* st = stats + (it & 1) * 4 * BM;
-      const PairMerge mg{2 * rank, mapa_shared(smem_u32(st), uint32_t(rank ^ 1)), peer_bar0 + uint32_t(8 * (it & 1)),
-                         &pstats[it & 1], uint32_t((it >> 1) & 1), lane};
+      float4* st = stats + (it & 1) * 2 * CL * BM;
+      const PairMerge<CL> mg{2 * rank, smem_u32(st), smem_u32(&pstats[it & 1]), &pstats[it & 1],
+                             uint32_t((it >> 1) & 1), lane, rank};
       const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + n0};
-      ln_epilogue<BNC, BNC / 2, true, 0u, 0u, float, PairMerge>(
+      ln_epilogue<BNC, BNC / 2, true, 0u, 0u, float, PairMerge<CL>>(
           taddr, 0, rg, s_bias, s_gamma, s_beta, st, q, hh, lane, eps,
           [&] {
             mbar_wait(tfull, it & 1);
@@ -225,12 +236,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int BNC>
+template <int BNC, int CL>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t st) {
-  using T = LnPairCfg<BNC>;
+  using T = LnPairCfg<BNC, CL>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ln_pair_kernel<BNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(ln_pair_kernel<BNC, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -238,22 +249,22 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t m_tiles = (g.M + BM - 1) / BM;
-  const int clusters = int(std::min<int64_t>(m_tiles, (sms > 0 ? sms : 148) / 2));
+  const int clusters = int(std::min<int64_t>(m_tiles, (sms > 0 ? sms : 148) / CL));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(2 * clusters));
+  cfg.gridDim = dim3(unsigned(CL * clusters));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = size_t(T::SMEM);
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, ln_pair_kernel<BNC>, *g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
+  return cudaLaunchKernelEx(&cfg, ln_pair_kernel<BNC, CL>, *g.tmA, *g.tmB, int(g.M), g.N, g.K, g.bias, g.res, g.gamma,
                             g.beta, g.C, g.eps);
 }
 
@@ -264,7 +275,14 @@ bool ln_pair_supported(int d, int k) { return (d == 768 || d == 1024) && k % 64 
 cudaError_t launch_ln_pair(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0) return cudaSuccess;
   if (!ln_pair_supported(g.N, g.K)) return cudaErrorInvalidValue;
-  return g.N == 768 ? launch_t<384>(g, st) : launch_t<512>(g, st);
+#ifndef LN_PAIR_CL768
+#define LN_PAIR_CL768 2     // 4 measured 2x slower
+#endif
+#ifndef LN_PAIR_CL1024
+#define LN_PAIR_CL1024 2   // 4-CTA clusters (256 columns, 4 stages) measured 1.7x slower
+#endif
+  if (g.N == 768) return launch_t<768 / LN_PAIR_CL768, LN_PAIR_CL768>(g, st);
+  return launch_t<1024 / LN_PAIR_CL1024, LN_PAIR_CL1024>(g, st);
 }
 
 }  // namespace surge

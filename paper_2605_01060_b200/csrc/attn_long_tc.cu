@@ -1,0 +1,271 @@
+// attn_long_tc.cu -- K5 for texts of 65..512 tokens at d_h = 64 (the bge classes' long-text workload,
+// SURVEY.md §8(f) N1; reading R10: softmax(q k^T / sqrt(d_h)) v over the text's own tokens) with both
+// products on the tcgen05 tensor cores.  One CTA per (text, head); the text's K and V rows of the head stay
+// in shared memory (TMA boxes of 128 rows x 64 bf16 from the QKV buffer, 128-byte swizzle) while its
+// 128-row query tiles go through:
+//   S = Q K^T     tcgen05 M = 128, N = L (the text length rounded up to 64, <= 512: the whole row of S
+//                 fits TMEM, so the softmax is exact in one pass -- no online rescaling), K = 64;
+//   softmax       8 warps, two per TMEM lane quadrant, each over half of the row's columns (keys >= len
+//                 masked); row max and row sum exchanged through shared memory; exp2 form with the row
+//                 max, P (bf16) written over the columns of S already read (P_A at [0, L/4), P_B at
+//                 [L/2, 3L/4));
+//   O = P V       tcgen05 M = 128, N = 64, K = L, A = P read from TMEM, B = V as stored (MN-major);
+//   O / rowsum -> bf16 -> global O (128 bytes per row), rows < len.
+// TMEM: 512 columns, S in [0, L), O in [3L/4, 3L/4 + 64).  Layouts as in qkv_attn_tc.cu (checked by
+// scripts/microbench/ts_attn_check.cu).  Same bf16 Q/K/V/P values and softmax formula as the mma.sync
+// kernels (attn_tile.cuh); fp32 accumulation order differs (reading R21).
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace surge {
+
+namespace {
+
+constexpr int DH = 64;
+constexpr int BM = 128;
+constexpr int THREADS = 320;          // warp 0 control (TMA + MMA), warp 1 TMEM, warps 2..9 softmax / O
+constexpr int OFF_Q = 1024;           // after the barriers and the max / sum exchange
+// Two size classes, launched over the same text list (a CTA whose text is of the other class exits at
+// once): texts of <= 256 tokens use 256 TMEM columns and 81 KB of shared memory, so two CTAs share an SM
+// and hide each other's load / softmax latency; longer texts take the whole TMEM (one CTA per SM).
+template <int LMAX>
+struct LongCfg {
+  static constexpr int OFF_K = OFF_Q + BM * 128;
+  static constexpr int OFF_V = OFF_K + LMAX * 128;
+  static constexpr int SMEM = OFF_V + LMAX * 128;   // 81 / 145 KB
+};
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+template <int LMAX>
+__global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
+    attn_long_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ cu,
+                        const int32_t* __restrict__ d_long, int32_t tok0, int d, uint16_t* __restrict__ out,
+                        float qscale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* q_full = kv_full + 1;
+  uint64_t* q_empty = q_full + 1;     // S(qt) retired: the Q tile may be reloaded (commit)
+  uint64_t* s_full = q_empty + 1;     // commit
+  uint64_t* p_ready = s_full + 1;     // 8 softmax warps
+  uint64_t* o_full = p_ready + 1;     // commit
+  uint64_t* o_empty = o_full + 1;     // 4 warps (part 0) have read O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  float* xmax = reinterpret_cast<float*>(smem + 256);   // [2 parts][128 rows]
+  float* xsum = xmax + 2 * BM;                          // [2 parts][128 rows]
+  uint8_t* sQ = smem + OFF_Q;
+  uint8_t* sK = smem + LongCfg<LMAX>::OFF_K;
+  uint8_t* sV = smem + LongCfg<LMAX>::OFF_V;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int text = __ldg(d_long + blockIdx.x), head = int(blockIdx.y);
+  const int ta = __ldg(cu + text) - tok0, len = __ldg(cu + text + 1) - __ldg(cu + text);
+  const int L = (len + 63) & ~63;                       // <= 512 (the caller checks max_len)
+  const int nq = (len + BM - 1) / BM;
+  if (L > LMAX || (LMAX > 256 && L <= 256)) return;     // the other size class's text
+
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023u) != 0) __trap();
+    tma_prefetch_desc(&tmQKV);
+    mbar_init(kv_full, 1);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_ready, 8);
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, LMAX);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t O_COL = uint32_t(3 * L / 4);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ control: TMA + MMA (one thread)
+    if (lane == 0) {
+      griddep_wait();
+      const int nkv = (L + BM - 1) / BM;
+      mbar_arrive_expect_tx(kv_full, uint32_t(2 * nkv * BM * 128));
+      for (int j = 0; j < nkv; ++j) {
+        tma_load_2d(sK + j * BM * 128, &tmQKV, kv_full, d + head * DH, ta + j * BM);
+        tma_load_2d(sV + j * BM * 128, &tmQKV, kv_full, 2 * d + head * DH, ta + j * BM);
+      }
+      const uint64_t qd = umma_desc_sw128(smem_u32(sQ)), kd = umma_desc_sw128(smem_u32(sK)),
+                     vd = umma_desc_sw128(smem_u32(sV));
+      const uint32_t id_pv = umma_idesc_bf16(BM, DH) | (1u << 16);   // B = V MN-major (as stored)
+      for (int qt = 0; qt < nq; ++qt) {
+        if (qt > 0) mbar_wait(q_empty, (qt - 1) & 1);  // S(qt-1) has read the previous Q tile
+        mbar_arrive_expect_tx(q_full, uint32_t(BM * 128));
+        tma_load_2d(sQ, &tmQKV, q_full, head * DH, ta + qt * BM);
+        mbar_wait(q_full, qt & 1);
+        if (qt == 0) mbar_wait(kv_full, 0);
+        if (qt > 0) mbar_wait(o_empty, (qt - 1) & 1);  // O(qt-1) read: S / P / O columns may be rewritten
+        tc_fence_after();
+        // S = Q K^T: N = L in blocks of <= 256 columns, K = 64 (4 steps)
+        for (int n0 = 0; n0 < L; n0 += 256) {
+          const int nn = L - n0 < 256 ? L - n0 : 256;
+          const uint32_t id_s = umma_idesc_bf16(BM, uint32_t(nn));
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k)
+            tc_mma_bf16(tmem + uint32_t(n0), qd + uint64_t(k * 2), kd + uint64_t((n0 * 128) >> 4) + uint64_t(k * 2), id_s,
+                        k);
+        }
+        tc_commit(s_full);
+        tc_commit(q_empty);
+        mbar_wait(p_ready, qt & 1);
+        tc_fence_after();
+        // O = P V: K = L keys in steps of 16; P_A (keys < L/2) at column 0, P_B at column L/2
+        for (int k = 0; k < L / 16; ++k) {
+          const int kk = k < L / 32 ? k : k - L / 32;
+          const uint32_t pa = tmem + (k < L / 32 ? 0u : uint32_t(L / 2)) + uint32_t(8 * kk);
+          mma_ts(tmem + O_COL, pa, vd + uint64_t((k * 16 * 128) >> 4), id_pv, k);
+        }
+        tc_commit(o_full);
+      }
+    }
+  } else if (warp >= 2) {
+    // ------------------------------------------------------------------ softmax + O (warps 2..9)
+    const int q = warp & 3, hh = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t tl = tmem + (uint32_t(q * 32) << 16);
+    const int half = L / 2, c0 = hh * half;
+    const float qs = qscale;
+    for (int qt = 0; qt < nq; ++qt) {
+      mbar_wait(s_full, qt & 1);
+      tc_fence_after();
+      float m = -INFINITY;
+      for (int cc = 0; cc < half; cc += 32) {          // row max over this part's valid keys
+        uint32_t sv[32];
+        tmem_ld32(tl + uint32_t(c0 + cc), sv);
+        tmem_ld_wait_regs(sv);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c0 + cc + i < len) m = fmaxf(m, __uint_as_float(sv[i]));
+      }
+      xmax[hh * BM + r] = m;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // the two warps of this quadrant
+      m = fmaxf(m, xmax[(hh ^ 1) * BM + r]);
+      const float mq = m * qs;                          // len >= 1: finite for every row of the tile
+      float l = 0.f;
+      for (int cc = 0; cc < half; cc += 32) {          // P = 2^(s q - m q) (0 past the text), bf16, over S
+        uint32_t sv[32], pk[16];
+        tmem_ld32(tl + uint32_t(c0 + cc), sv);
+        tmem_ld_wait_regs(sv);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int key = c0 + cc + 2 * i;
+          const float e0 = key < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i]), qs, -mq)) : 0.f;
+          const float e1 = key + 1 < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i + 1]), qs, -mq)) : 0.f;
+          l += e0 + e1;
+          pk[i] = pack_bf16x2(e0, e1);
+        }
+        tmem_st16(tl + uint32_t(c0 + cc / 2), pk);      // P of keys c0 + cc .. : S columns already read
+      }
+      xsum[hh * BM + r] = l;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      if (hh == 0) {
+        const float il = __frcp_rn(l + xsum[BM + r]);
+        mbar_wait(o_full, qt & 1);
+        tc_fence_after();
+        uint32_t o[32], o2[32];
+        tmem_ld32(tl + O_COL, o);
+        tmem_ld32(tl + O_COL + 32, o2);
+        tmem_ld_wait_regs(o);
+        tmem_ld_wait_regs(o2);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty);
+        const int row = qt * BM + r;
+        if (row < len) {
+          uint16_t* dst = out + size_t(ta + row) * d + head * DH;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const uint32_t (&src)[32] = h2 ? o2 : o;
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              pk[i] = pack_bf16x2(__uint_as_float(src[2 * i]) * il, __uint_as_float(src[2 * i + 1]) * il);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 32 * h2 + 16 * i),
+                           "r"(pk[8 * i]), "r"(pk[8 * i + 1]), "r"(pk[8 * i + 2]), "r"(pk[8 * i + 3]),
+                           "r"(pk[8 * i + 4]), "r"(pk[8 * i + 5]), "r"(pk[8 * i + 6]), "r"(pk[8 * i + 7])
+                           : "memory");
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem, LMAX);
+  }
+}
+
+}  // namespace
+
+bool attn_long_tc_supported(int head_dim) { return head_dim == DH; }
+
+bool attn_long_tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SURGE_ATT_LONG_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+cudaError_t launch_attn_long_tc(const uint16_t* qkv, const int32_t* cu, const int32_t* d_long, int32_t n_long,
+                                int32_t tok0, int32_t ntok, int heads, uint16_t* out, cudaStream_t st) {
+  if (n_long <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_long_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         LongCfg<256>::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_long_tc_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, LongCfg<512>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int d = heads * DH;
+  CUtensorMap tm;
+  cudaError_t e = make_tmap_bf16(&tm, qkv, uint64_t(ntok), uint64_t(3 * d), BM);
+  if (e != cudaSuccess) return e;
+  const float qscale = 1.4426950408889634f / sqrtf(float(DH));
+  attn_long_tc_kernel<256><<<dim3(unsigned(n_long), unsigned(heads)), THREADS, LongCfg<256>::SMEM, st>>>(
+      tm, cu, d_long, tok0, d, out, qscale);
+  attn_long_tc_kernel<512><<<dim3(unsigned(n_long), unsigned(heads)), THREADS, LongCfg<512>::SMEM, st>>>(
+      tm, cu, d_long, tok0, d, out, qscale);
+  return cudaGetLastError();
+}
+
+}  // namespace surge

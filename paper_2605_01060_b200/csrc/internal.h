@@ -85,6 +85,12 @@ bool qkv_attn_tc_supported(int d, int heads);
 // K6 / K8 with the LayerNorm fused for d in {768, 1024} (ln_pair.cu): a cluster of two CTAs splits the row,
 // statistics exchanged through distributed shared memory.  B = the weight with 64-row TMA boxes.
 bool ln_pair_supported(int d, int k);
+// K5 for texts of 65..512 tokens at d_h = 64 on tcgen05 (attn_long_tc.cu): one CTA per (text, head), K / V
+// of the text resident, S row in TMEM; replaces attention_long_kernel (env SURGE_ATT_LONG_TC=0 restores it).
+bool attn_long_tc_supported(int head_dim);
+bool attn_long_tc_enabled();
+cudaError_t launch_attn_long_tc(const uint16_t* qkv, const int32_t* cu, const int32_t* d_long, int32_t n_long,
+                                int32_t tok0, int32_t ntok, int heads, uint16_t* out, cudaStream_t st);
 cudaError_t launch_ln_pair(const GemmArgs& g, cudaStream_t st);
 cudaError_t launch_qkv_attn_tc(const GemmArgs& g, cudaStream_t st);
 // LN GEMMs fuse the LayerNorm into the epilogue when the full row fits one CTA's TMEM (d in {64, 384});

@@ -793,7 +793,10 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
         lattr_##DH = true;                                                                                   \
       }                                                                                                      \
       if (max_len > 512) return cudaErrorInvalidValue;                                                       \
-      if (n_long > 0)                                                                                        \
+      if (n_long > 0 && attn_long_tc_enabled() && attn_long_tc_supported(DH)) {                             \
+        cudaError_t e_ = launch_attn_long_tc(qkv, cu, d_long, n_long, tok0, ntok, heads, out, st);            \
+        if (e_ != cudaSuccess) return e_;                                                                    \
+      } else if (n_long > 0)                                                                                 \
         attention_long_kernel<DH><<<dim3(unsigned(n_long), unsigned(heads)), LA::WARPS * 32, LA::smem(max_len), \
                                     st>>>(qkv, cu, d_long, tok0, heads, out, qscale, LA::kv_rows(max_len));  \
     } else if (max_len > ATT_SHORT) {   /* list of long texts unknown: scalar per-(text, head) kernel */    \

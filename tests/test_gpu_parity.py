@@ -667,3 +667,21 @@ def test_ln_pair_vs_separate_layernorm_and_oracle(N, enc, n_texts):
     T = texts_of(ids, lens)
     rows = sorted({0, len(lens) - 1, *rng.integers(0, len(lens), size=8).tolist()})
     compare(pair[rows], np.stack([E.encode_text(T[i]) for i in rows]))
+
+
+def test_long_text_attention_tcgen05_vs_oracle(N):
+    """Texts of 65..512 tokens at d_h = 64 (bge-base): the long-text attention on tcgen05 (attn_long_tc.cu: one
+    CTA per (text, head), the text's whole S row in TMEM, exact one-pass softmax) -- every query-tile / key-block
+    edge length (65, 127/128/129, 191/192, 255/256/257, 320, 383/384, 447/448, 511/512) plus short texts in the
+    same chunks (they take the short-text kernel); every row vs the fp64 oracle under the gate."""
+    ecfg = ENCODERS["bgebase"]
+    w = make_weights(ecfg, seed=1234)
+    rng = np.random.default_rng(17)
+    lens = np.array([65, 127, 128, 129, 191, 192, 255, 256, 257, 320, 383, 384, 447, 448, 511, 512, 9, 40, 64, 70],
+                    dtype=np.int32)
+    ids = rng.integers(1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
+    got = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096)
+    E = oenc.Encoder(ecfg, w)
+    T = texts_of(ids, lens)
+    c, a = compare(got, np.stack([E.encode_text(t) for t in T]))
+    print(f"long-text tcgen05 attention vs oracle, {len(T)} rows: min cos {c:.6f}, max|d| {a:.3g}")

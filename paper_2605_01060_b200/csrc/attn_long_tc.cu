@@ -1,4 +1,4 @@
-// attn_long_tc.cu -- K5 for texts of 65..512 tokens at d_h = 64 (the bge classes' long-text workload,
+// attn_long_tc.cu -- K5 for texts of 129..512 tokens at d_h = 64 (the bge classes' long-text workload,
 // SURVEY.md §8(f) N1; reading R10: softmax(q k^T / sqrt(d_h)) v over the text's own tokens) with both
 // products on the tcgen05 tensor cores.  One CTA per (text, head); the text's K and V rows of the head stay
 // in shared memory (TMA boxes of 128 rows x 64 bf16 from the QKV buffer, 128-byte swizzle) while its
@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
   const int ta = __ldg(cu + text) - tok0, len = __ldg(cu + text + 1) - __ldg(cu + text);
   const int L = (len + 63) & ~63;                       // <= 512 (the caller checks max_len)
   const int nq = (len + BM - 1) / BM;
-  if (L > LMAX || (LMAX > 256 && L <= 256)) return;     // the other size class's text
+  // texts <= 128 tokens: the mma.sync kernel (same arithmetic as the fused QKV + attention epilogue);
+  // otherwise the other size class's text
+  if (len <= BM || L > LMAX || (LMAX > 256 && L <= 256)) return;
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -236,10 +238,13 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
 
 bool attn_long_tc_supported(int head_dim) { return head_dim == DH; }
 
+// Off by default: one (text, head) per CTA with its loads, both MMAs, the softmax and the stores in series
+// measured slower than the mma.sync kernel on the C4 workload (bge-large long texts: attention 3.20 s vs
+// 2.71 s per 100K texts); SURGE_ATT_LONG_TC=1 selects it.
 bool attn_long_tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("SURGE_ATT_LONG_TC");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

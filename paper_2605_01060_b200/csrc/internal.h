@@ -86,7 +86,7 @@ bool qkv_attn_tc_supported(int d, int heads);
 // statistics exchanged through distributed shared memory.  B = the weight with 64-row TMA boxes.
 bool ln_pair_supported(int d, int k);
 // K5 for texts of 65..512 tokens at d_h = 64 on tcgen05 (attn_long_tc.cu): one CTA per (text, head), K / V
-// of the text resident, S row in TMEM; replaces attention_long_kernel (env SURGE_ATT_LONG_TC=0 restores it).
+// of the text resident, S row in TMEM; texts > 128 tokens, off by default (env SURGE_ATT_LONG_TC=1).
 bool attn_long_tc_supported(int head_dim);
 bool attn_long_tc_enabled();
 cudaError_t launch_attn_long_tc(const uint16_t* qkv, const int32_t* cu, const int32_t* d_long, int32_t n_long,

@@ -519,7 +519,7 @@ struct LongAtt {
 template <int DH>
 __global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel(
     const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu, const int32_t* __restrict__ texts,
-    int32_t tok0, int heads, uint16_t* __restrict__ out, float qscale, int kv_rows) {
+    int32_t tok0, int heads, uint16_t* __restrict__ out, float qscale, int kv_rows, int max_handled) {
   using A = LongAtt<DH>;
   constexpr int LDS = A::LDS, CH = A::CH;
   extern __shared__ __align__(16) uint16_t att_sm[];
@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel
   const int h = blockIdx.y;
   const int d = heads * DH, ld = 3 * d;
   const int32_t a = cu[txt] - tok0, len = cu[txt + 1] - cu[txt];
+  if (len > max_handled) return;                 // left to the tcgen05 long-text kernel (attn_long_tc.cu)
   const int nt = (len + 15) >> 4;
   for (int i = tid; i < len * CH; i += blockDim.x) {
     const int r = i / CH, c = i - r * CH;
@@ -793,12 +794,18 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
         lattr_##DH = true;                                                                                   \
       }                                                                                                      \
       if (max_len > 512) return cudaErrorInvalidValue;                                                       \
-      if (n_long > 0 && attn_long_tc_enabled() && attn_long_tc_supported(DH)) {                             \
+      /* texts of 65..128 tokens keep the mma.sync arithmetic of the fused QKV + attention epilogue (a     \
+         text's bits must not depend on its chunk's other texts); longer ones go to tcgen05 (d_h = 64) */   \
+      const bool tc_ = attn_long_tc_enabled() && attn_long_tc_supported(DH) && max_len > ATT_TILE_ROWS;     \
+      if (n_long > 0 && tc_) {                                                                              \
         cudaError_t e_ = launch_attn_long_tc(qkv, cu, d_long, n_long, tok0, ntok, heads, out, st);            \
         if (e_ != cudaSuccess) return e_;                                                                    \
-      } else if (n_long > 0)                                                                                 \
-        attention_long_kernel<DH><<<dim3(unsigned(n_long), unsigned(heads)), LA::WARPS * 32, LA::smem(max_len), \
-                                    st>>>(qkv, cu, d_long, tok0, heads, out, qscale, LA::kv_rows(max_len));  \
+      }                                                                                                      \
+      if (n_long > 0)                                                                                        \
+        attention_long_kernel<DH><<<dim3(unsigned(n_long), unsigned(heads)), LA::WARPS * 32,                  \
+                                    LA::smem(tc_ ? ATT_TILE_ROWS : max_len), st>>>(                          \
+            qkv, cu, d_long, tok0, heads, out, qscale, LA::kv_rows(tc_ ? ATT_TILE_ROWS : max_len),            \
+            tc_ ? ATT_TILE_ROWS : 1 << 30);                                                                   \
     } else if (max_len > ATT_SHORT) {   /* list of long texts unknown: scalar per-(text, head) kernel */    \
       constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \
       attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W1), W1 * 32, 0, st>>>(                       \

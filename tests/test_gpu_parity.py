@@ -7,6 +7,8 @@ Gates (BASELINE.json north star):
   self-invariance: identical embeddings across SuperBatch compositions, PBP mode, the
              device-level path, and rank splits (world_size 2 on one GPU).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -246,7 +248,7 @@ def test_larger_encoder_classes_sample(N, enc, length_model):
         compare(got[key][rows], np.stack([E.encode_text(T[i]) for i in rows]))
 
 
-def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True, tail_fused=True, att_tc=True,
+def _packed_encode(N, ecfg, w, lens, ids, fused, chunk_tokens=0, mlp_fused=True, tail_fused=True, att_tc=False,
                    ln_pair=True):
     h = N.surge_create(N.make_config(ecfg, 1000, 5000, chunk_tokens=chunk_tokens), pack_blob(ecfg, w))
     try:
@@ -670,7 +672,7 @@ def test_ln_pair_vs_separate_layernorm_and_oracle(N, enc, n_texts):
 
 
 def test_long_text_attention_tcgen05_vs_oracle(N):
-    """Texts of 65..512 tokens at d_h = 64 (bge-base): the long-text attention on tcgen05 (attn_long_tc.cu: one
+    """Texts of 65..512 tokens at d_h = 64 (bge-base): texts > 128 tokens take the long-text attention on tcgen05 (attn_long_tc.cu: one
     CTA per (text, head), the text's whole S row in TMEM, exact one-pass softmax) -- every query-tile / key-block
     edge length (65, 127/128/129, 191/192, 255/256/257, 320, 383/384, 447/448, 511/512) plus short texts in the
     same chunks (they take the short-text kernel); every row vs the fp64 oracle under the gate."""
@@ -680,7 +682,24 @@ def test_long_text_attention_tcgen05_vs_oracle(N):
     lens = np.array([65, 127, 128, 129, 191, 192, 255, 256, 257, 320, 383, 384, 447, 448, 511, 512, 9, 40, 64, 70],
                     dtype=np.int32)
     ids = rng.integers(1000, ecfg.vocab_size, size=int(lens.sum())).astype(np.int32)
-    got = _packed_encode(N, ecfg, w, lens, ids, True, chunk_tokens=4096)
+    import subprocess
+    import sys
+    import tempfile
+    # the kernel is selected by SURGE_ATT_LONG_TC=1 (read once per process): encode in a child process
+    with tempfile.TemporaryDirectory() as td:
+        np.save(f"{td}/lens.npy", lens)
+        np.save(f"{td}/ids.npy", ids)
+        code = ("import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+                "import test_gpu_parity as T\n"
+                "from paper_2605_01060_b200 import native as N\n"
+                "from synth.configs import ENCODERS\nfrom synth.weights import make_weights\n"
+                "e = ENCODERS['bgebase']; w = make_weights(e, seed=1234)\n"
+                "out = T._packed_encode(N, e, w, np.load(%r), np.load(%r), True, chunk_tokens=4096)\n"
+                "np.save(%r, out)\n") % (os.path.dirname(__file__), os.path.dirname(os.path.dirname(__file__)),
+                                          f"{td}/lens.npy", f"{td}/ids.npy", f"{td}/out.npy")
+        env = dict(os.environ, SURGE_ATT_LONG_TC="1")
+        subprocess.run([sys.executable, "-c", code], check=True, env=env)
+        got = np.load(f"{td}/out.npy")
     E = oenc.Encoder(ecfg, w)
     T = texts_of(ids, lens)
     c, a = compare(got, np.stack([E.encode_text(t) for t in T]))

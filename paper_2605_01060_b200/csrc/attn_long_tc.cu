@@ -16,6 +16,7 @@
 // kernels (attn_tile.cuh); fp32 accumulation order differs (reading R21).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -234,6 +235,258 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
   }
 }
 
+// Texts of 129..256 tokens: a persistent CTA per SM works through its (text, head) items as a pipeline of
+// elements e = (item, 128-row query tile), two in flight: TMEM regions of 256 columns alternate by e % 2
+// (S / P / O of element e), the K/V tiles of consecutive items alternate between two shared-memory buffers
+// (the next item's K/V load under the current item's work), and the single MMA thread issues S(e + 1)
+// before it waits for the softmax of e to issue PV(e) -- so the softmax of one element runs under the
+// tensor work (and loads) of its neighbours instead of in series with them.
+constexpr int PIPE_OFF_Q = 2048;
+constexpr int PIPE_OFF_KV = PIPE_OFF_Q + BM * 128;                 // [2 buffers][K 256 rows | V 256 rows]
+constexpr int PIPE_KV = 2 * 256 * 128;                             // 64 KB per buffer
+constexpr int PIPE_SMEM = PIPE_OFF_KV + 2 * PIPE_KV;              // 146 KB
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_long_pipe_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ cu,
+                          const int32_t* __restrict__ d_long, int32_t n_items, int heads, int32_t tok0, int d,
+                          uint16_t* __restrict__ out, float qscale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem);   // [2] per KV buffer
+  uint64_t* kv_free = kv_full + 2;     // [2] commit after the item's last PV
+  uint64_t* q_full = kv_free + 2;
+  uint64_t* q_empty = q_full + 1;      // commit after S(e)
+  uint64_t* s_full = q_empty + 1;      // [2] per TMEM region
+  uint64_t* p_ready = s_full + 2;      // [2] 8 warps
+  uint64_t* o_full = p_ready + 2;      // [2] commit
+  uint64_t* o_empty = o_full + 2;      // [2] 4 warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  float* xmax = reinterpret_cast<float*>(smem + 256);   // [2 regions][2 parts][128]
+  float* xsum = xmax + 4 * BM;                          // [2 regions][2 parts][128]
+  uint8_t* sQ = smem + PIPE_OFF_Q;
+  uint8_t* sKV = smem + PIPE_OFF_KV;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // item i (of this CTA's list): global item blockIdx.x + i gridDim.x, text d_long[g / heads], head g % heads;
+  // only texts of 129..256 tokens are this kernel's
+  auto item_of = [&](int g, int& ta, int& len, int& head) -> bool {
+    const int text = __ldg(d_long + g / heads);
+    head = g % heads;
+    ta = __ldg(cu + text) - tok0;
+    len = __ldg(cu + text + 1) - __ldg(cu + text);
+    return len > BM && len <= 256;
+  };
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023u) != 0) __trap();
+    tma_prefetch_desc(&tmQKV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_free[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_ready[i], 8);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      griddep_wait();
+      const uint32_t id_pv = umma_idesc_bf16(BM, DH) | (1u << 16);
+      const uint64_t qd = umma_desc_sw128(smem_u32(sQ));
+      // the CTA's valid items, walked twice in step: `ld` = next item whose K/V to load, `e` elements
+      int g_ld = int(blockIdx.x), n_ld = 0;            // loads issued (items)
+      auto load_next = [&]() -> bool {                 // K/V of the next valid item into buffer n_ld % 2
+        int ta, len, head;
+        for (; g_ld < n_items; g_ld += int(gridDim.x)) {
+          if (!item_of(g_ld, ta, len, head)) continue;
+          const int b = n_ld & 1;
+          if (n_ld >= 2) mbar_wait(&kv_free[b], ((n_ld - 2) >> 1) & 1);   // item n_ld - 2's last PV retired
+          uint8_t* kv = sKV + b * PIPE_KV;
+          mbar_arrive_expect_tx(&kv_full[b], uint32_t(2 * 2 * BM * 128));
+          for (int j = 0; j < 2; ++j) {
+            tma_load_2d(kv + j * BM * 128, &tmQKV, &kv_full[b], d + head * DH, ta + j * BM);
+            tma_load_2d(kv + 256 * 128 + j * BM * 128, &tmQKV, &kv_full[b], 2 * d + head * DH, ta + j * BM);
+          }
+          g_ld += int(gridDim.x);
+          ++n_ld;
+          return true;
+        }
+        return false;
+      };
+      load_next();
+      load_next();
+      // element e = (item n_it, query tile qt); S(e) issued one element ahead of PV(e)
+      int g_it = int(blockIdx.x), n_it = -1, ta = 0, len = 0, head = 0, qt = 1, e = 0;
+      auto next_elem = [&]() -> bool {                 // advance (n_it, qt) to the next element
+        if (n_it >= 0 && qt + 1 < 2) {
+          ++qt;
+          return true;
+        }
+        for (; g_it < n_items; g_it += int(gridDim.x))
+          if (item_of(g_it, ta, len, head)) {
+            g_it += int(gridDim.x);
+            ++n_it;
+            qt = 0;
+            return true;
+          }
+        return false;
+      };
+      struct El { int n_it, ta, len, head, qt; };
+      auto issue_s = [&](int ee, const El& x) {       // S(ee) = Q K^T into TMEM region ee % 2
+        const int rg = ee & 1;
+        if (ee > 0) mbar_wait(q_empty, (ee - 1) & 1);  // S(ee-1) has read the Q buffer
+        mbar_arrive_expect_tx(q_full, uint32_t(BM * 128));
+        tma_load_2d(sQ, &tmQKV, q_full, x.head * DH, x.ta + x.qt * BM);
+        mbar_wait(q_full, ee & 1);
+        if (x.qt == 0) mbar_wait(&kv_full[x.n_it & 1], (x.n_it >> 1) & 1);
+        if (ee >= 2) mbar_wait(&o_empty[rg], ((ee - 2) >> 1) & 1);   // region's previous element drained
+        tc_fence_after();
+        const int L = (x.len + 63) & ~63;
+        const uint64_t kd = umma_desc_sw128(smem_u32(sKV + (x.n_it & 1) * PIPE_KV));
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k)
+          tc_mma_bf16(tmem + uint32_t(256 * rg), qd + uint64_t(k * 2), kd + uint64_t(k * 2), umma_idesc_bf16(BM, uint32_t(L)),
+                      k);
+        tc_commit(&s_full[rg]);
+        tc_commit(q_empty);
+      };
+      auto issue_pv = [&](int ee, const El& x) {
+        const int rg = ee & 1;
+        mbar_wait(&p_ready[rg], (ee >> 1) & 1);
+        tc_fence_after();
+        const int L = (x.len + 63) & ~63;
+        const uint64_t vd = umma_desc_sw128(smem_u32(sKV + (x.n_it & 1) * PIPE_KV + 256 * 128));
+        const uint32_t base = tmem + uint32_t(256 * rg);
+        for (int k = 0; k < L / 16; ++k) {
+          const int kk = k < L / 32 ? k : k - L / 32;
+          const uint32_t pa = base + (k < L / 32 ? 0u : uint32_t(L / 2)) + uint32_t(8 * kk);
+          mma_ts(base + uint32_t(3 * L / 4), pa, vd + uint64_t((k * 16 * 128) >> 4), id_pv, k);
+        }
+        tc_commit(&o_full[rg]);
+        if (x.qt == 1) {                               // the item's last query tile: its K/V buffer is free
+          tc_commit(&kv_free[x.n_it & 1]);
+          load_next();
+        }
+      };
+      El cur{}, nxt{};
+      bool have = next_elem();
+      if (have) cur = El{n_it, ta, len, head, qt};
+      if (have) issue_s(0, cur);
+      for (e = 0; have; ++e) {
+        const bool more = next_elem();
+        if (more) {
+          nxt = El{n_it, ta, len, head, qt};
+          issue_s(e + 1, nxt);
+        }
+        issue_pv(e, cur);
+        cur = nxt;
+        have = more;
+      }
+    }
+  } else if (warp >= 2) {
+    // ------------------------------------------------------------------ softmax + O (warps 2..9)
+    const int q = warp & 3, hh = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const float qs = qscale;
+    int e = 0;
+    for (int g = int(blockIdx.x); g < n_items; g += int(gridDim.x)) {
+      int ta, len, head;
+      if (!item_of(g, ta, len, head)) continue;
+      const int L = (len + 63) & ~63, half = L / 2, c0 = hh * half;
+      for (int qt = 0; qt < 2; ++qt, ++e) {
+        const int rg = e & 1;
+        const uint32_t tl = tmem + uint32_t(256 * rg) + (uint32_t(q * 32) << 16);
+        float* xm = xmax + rg * 2 * BM;
+        float* xs = xsum + rg * 2 * BM;
+        mbar_wait(&s_full[rg], (e >> 1) & 1);
+        tc_fence_after();
+        float m = -INFINITY;
+        for (int cc = 0; cc < half; cc += 32) {
+          uint32_t sv[32];
+          tmem_ld32(tl + uint32_t(c0 + cc), sv);
+          tmem_ld_wait_regs(sv);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + cc + i < len) m = fmaxf(m, __uint_as_float(sv[i]));
+        }
+        xm[hh * BM + r] = m;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        m = fmaxf(m, xm[(hh ^ 1) * BM + r]);
+        const float mq = m * qs;
+        float l = 0.f;
+        for (int cc = 0; cc < half; cc += 32) {
+          uint32_t sv[32], pk[16];
+          tmem_ld32(tl + uint32_t(c0 + cc), sv);
+          tmem_ld_wait_regs(sv);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int key = c0 + cc + 2 * i;
+            const float e0 = key < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i]), qs, -mq)) : 0.f;
+            const float e1 = key + 1 < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i + 1]), qs, -mq)) : 0.f;
+            l += e0 + e1;
+            pk[i] = pack_bf16x2(e0, e1);
+          }
+          tmem_st16(tl + uint32_t(c0 + cc / 2), pk);
+        }
+        xs[hh * BM + r] = l;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_ready[rg]);
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        if (hh == 0) {
+          const float il = __frcp_rn(l + xs[BM + r]);
+          mbar_wait(&o_full[rg], (e >> 1) & 1);
+          tc_fence_after();
+          uint32_t o[32], o2[32];
+          tmem_ld32(tl + uint32_t(3 * L / 4), o);
+          tmem_ld32(tl + uint32_t(3 * L / 4 + 32), o2);
+          tmem_ld_wait_regs(o);
+          tmem_ld_wait_regs(o2);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_empty[rg]);
+          const int row = qt * BM + r;
+          if (row < len) {
+            uint16_t* dst = out + size_t(ta + row) * d + head * DH;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const uint32_t (&src)[32] = h2 ? o2 : o;
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                pk[i] = pack_bf16x2(__uint_as_float(src[2 * i]) * il, __uint_as_float(src[2 * i + 1]) * il);
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+                asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 32 * h2 + 16 * i),
+                             "r"(pk[8 * i]), "r"(pk[8 * i + 1]), "r"(pk[8 * i + 2]), "r"(pk[8 * i + 3]),
+                             "r"(pk[8 * i + 4]), "r"(pk[8 * i + 5]), "r"(pk[8 * i + 6]), "r"(pk[8 * i + 7])
+                             : "memory");
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
 
 bool attn_long_tc_supported(int head_dim) { return head_dim == DH; }
@@ -259,6 +512,8 @@ cudaError_t launch_attn_long_tc(const uint16_t* qkv, const int32_t* cu, const in
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(attn_long_tc_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, LongCfg<512>::SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_long_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PIPE_SMEM);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   const int d = heads * DH;
@@ -266,8 +521,20 @@ cudaError_t launch_attn_long_tc(const uint16_t* qkv, const int32_t* cu, const in
   cudaError_t e = make_tmap_bf16(&tm, qkv, uint64_t(ntok), uint64_t(3 * d), BM);
   if (e != cudaSuccess) return e;
   const float qscale = 1.4426950408889634f / sqrtf(float(DH));
-  attn_long_tc_kernel<256><<<dim3(unsigned(n_long), unsigned(heads)), THREADS, LongCfg<256>::SMEM, st>>>(
-      tm, cu, d_long, tok0, d, out, qscale);
+#ifndef ATT_LONG_PIPE
+#define ATT_LONG_PIPE 1
+#endif
+  if (ATT_LONG_PIPE) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = int64_t(n_long) * heads;
+    attn_long_pipe_kernel<<<unsigned(std::min<int64_t>(items, sms > 0 ? sms : 148)), THREADS, PIPE_SMEM, st>>>(
+        tm, cu, d_long, int32_t(items), heads, tok0, d, out, qscale);
+  } else {
+    attn_long_tc_kernel<256><<<dim3(unsigned(n_long), unsigned(heads)), THREADS, LongCfg<256>::SMEM, st>>>(
+        tm, cu, d_long, tok0, d, out, qscale);
+  }
   attn_long_tc_kernel<512><<<dim3(unsigned(n_long), unsigned(heads)), THREADS, LongCfg<512>::SMEM, st>>>(
       tm, cu, d_long, tok0, d, out, qscale);
   return cudaGetLastError();

@@ -11,6 +11,12 @@ for tool in memcheck racecheck synccheck; do
     python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|smoke ok' gpurun_out/sanitize_$tool.log | tr '\n' ' ')"
 done
+# the round-2 kernels (tcgen05 QKV + attention, cluster-pair LN GEMMs, long-text tcgen05 attention)
+for tool in memcheck synccheck; do
+  SURGE_ATT_LONG_TC=1 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --target-processes all \
+    python scripts/sanitize_new_kernels.py > gpurun_out/sanitize_new_$tool.log 2>&1
+  echo "new kernels $tool rc=$? $(grep -E 'ERROR SUMMARY|new kernels ok' gpurun_out/sanitize_new_$tool.log | tr '\n' ' ')"
+done
 TSAN=$(gcc -print-file-name=libtsan.so)
 SURGE_BUILD_OUT=varlib/tsan.so SURGE_BUILD_DIR=varlib/_b_tsan NVCC_EXTRA="-Xcompiler -fsanitize=thread,-g" \
   NVCC_LINK_EXTRA="-Xcompiler -fsanitize=thread" python paper_2605_01060_b200/build.py -f > /dev/null

@@ -61,6 +61,8 @@ def parse():
                     help="what B_max does (include/surge.h SURGE_BMAX_*): literal Alg.1 (default), "
                          "split oversized partitions (P:1271), or flush before them (P:304/P:308)")
     ap.add_argument("--b-min", type=int, default=0, help="override the workload's B_min (B_max = 5 B_min)")
+    ap.add_argument("--b-max", type=int, default=0, help="override B_max (after --b-min)")
+    ap.add_argument("--sigma", type=float, default=0.0, help="override the log-normal sigma of partition sizes")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -170,11 +172,14 @@ def run_host_only(args, world, rank):
                           "superbatches": len(sbs), "peak_buffered_texts": peak, "plan_s": dt,
                           "texts_per_rank": [int(x[0]) for x in per_rank],
                           "tokens_per_rank": [int(x[1]) for x in per_rank],
-                          "n_texts": wl.n_texts, "n_tokens": wl.n_tokens}), flush=True)
+                          "n_texts": wl.n_texts, "n_tokens": wl.n_tokens, "sigma": wl.cfg.sigma,
+                          "b_min": wl.cfg.b_min, "b_max": wl.cfg.b_max,
+                          "max_superbatch_texts": max((int(wl.sizes[a:b].sum()) for a, b, _ in sbs), default=0)}),
+              flush=True)
 
 
 def workload_cfg(args):
-    """BASELINE.json workload named by --workload, with the optional N / P / B_min overrides."""
+    """BASELINE.json workload named by --workload, with the optional N / P / sigma / B_min / B_max overrides."""
     from dataclasses import replace
     wcfg = WORKLOADS[args.workload]
     kw = {}
@@ -184,7 +189,14 @@ def workload_cfg(args):
         kw["n_partitions"] = args.n_partitions
     if args.b_min:
         kw.update(b_min=args.b_min, b_max=5 * args.b_min)      # B_max = 5 B_min
-    return replace(wcfg, **kw) if kw else wcfg
+    if args.b_max:
+        kw["b_max"] = args.b_max
+    if args.sigma:
+        kw["sigma"] = args.sigma
+    w = replace(wcfg, **kw) if kw else wcfg
+    if not 0 < w.b_min <= w.b_max:
+        sys.exit(f"bench.py: need 0 < B_min <= B_max (got {w.b_min}, {w.b_max})")
+    return w
 
 
 def _oracle_flops_per_text(ecfg, l: int) -> float:

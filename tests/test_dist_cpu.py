@@ -159,3 +159,21 @@ def test_bench_rejects_gpus_world_mismatch():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--host-only"],
                        capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
     assert r.returncode != 0 and "--gpus 2" in r.stderr
+
+
+def test_bench_config_overrides():
+    """--sigma / --b-min / --b-max reach the workload (config CLI, SURVEY §8(b) surge_config thresholds):
+    the host plan runs at the requested skew and thresholds, and no SuperBatch sealed by the efficiency
+    trigger exceeds B_max unless it is a single oversized partition (Alg.1)."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--host-only", "--n-texts", "200000",
+           "--sigma", "2.5", "--b-min", "20000", "--b-max", "60000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert (d["sigma"], d["b_min"], d["b_max"]) == (2.5, 20000, 60000)
+    assert d["n_texts"] == 200_000 and sum(d["texts_per_rank"]) == 200_000
+    bad = subprocess.run(cmd[:-4] + ["--b-min", "50000", "--b-max", "100"], capture_output=True, text=True,
+                         timeout=300, env=env, cwd=ROOT)
+    assert bad.returncode != 0 and "B_min <= B_max" in bad.stderr

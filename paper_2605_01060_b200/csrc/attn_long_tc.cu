@@ -29,16 +29,17 @@ namespace {
 constexpr int DH = 64;
 constexpr int BM = 128;
 constexpr int THREADS = 320;          // warp 0 control (TMA + MMA), warp 1 TMEM, warps 2..9 softmax / O
-constexpr int OFF_Q = 1024;           // after the barriers and the max / sum exchange
+constexpr int OFF_Q = 3072;           // after the barriers (< 256) and the max / sum exchange ([256, 2304))
 // Two size classes, launched over the same text list (a CTA whose text is of the other class exits at
 // once): texts of <= 256 tokens use 256 TMEM columns and 81 KB of shared memory, so two CTAs share an SM
 // and hide each other's load / softmax latency; longer texts take the whole TMEM (one CTA per SM).
 template <int LMAX>
 struct LongCfg {
-  static constexpr int OFF_K = OFF_Q + BM * 128;
+  static constexpr int OFF_K = OFF_Q + 2 * BM * 128;   // two Q buffers (query tile qt: buffer qt % 2)
   static constexpr int OFF_V = OFF_K + LMAX * 128;
-  static constexpr int SMEM = OFF_V + LMAX * 128;   // 81 / 145 KB
+  static constexpr int SMEM = OFF_V + LMAX * 128;   // 99 / 163 KB
 };
+static_assert(OFF_Q >= 256 + 2 * 2 * BM * 4 && OFF_Q % 1024 == 0, "Q tiles after the max / sum exchange arrays");
 
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -63,9 +64,9 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
                         float qscale) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* q_full = kv_full + 1;
-  uint64_t* q_empty = q_full + 1;     // S(qt) retired: the Q tile may be reloaded (commit)
-  uint64_t* s_full = q_empty + 1;     // commit
+  uint64_t* q_full = kv_full + 1;     // [2] per Q buffer
+  uint64_t* q_empty = q_full + 2;     // [2] S(qt) retired: its Q buffer may be reloaded (commit)
+  uint64_t* s_full = q_empty + 2;     // commit
   uint64_t* p_ready = s_full + 1;     // 8 softmax warps
   uint64_t* o_full = p_ready + 1;     // commit
   uint64_t* o_empty = o_full + 1;     // 4 warps (part 0) have read O
@@ -89,8 +90,10 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
     if ((smem_u32(smem) & 1023u) != 0) __trap();
     tma_prefetch_desc(&tmQKV);
     mbar_init(kv_full, 1);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(p_ready, 8);
     mbar_init(o_full, 1);
@@ -117,14 +120,18 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
         tma_load_2d(sK + j * BM * 128, &tmQKV, kv_full, d + head * DH, ta + j * BM);
         tma_load_2d(sV + j * BM * 128, &tmQKV, kv_full, 2 * d + head * DH, ta + j * BM);
       }
-      const uint64_t qd = umma_desc_sw128(smem_u32(sQ)), kd = umma_desc_sw128(smem_u32(sK)),
-                     vd = umma_desc_sw128(smem_u32(sV));
+      const uint64_t kd = umma_desc_sw128(smem_u32(sK)), vd = umma_desc_sw128(smem_u32(sV));
       const uint32_t id_pv = umma_idesc_bf16(BM, DH) | (1u << 16);   // B = V MN-major (as stored)
+      auto load_q = [&](int qt) {                      // query tile qt -> Q buffer qt % 2
+        if (qt >= 2) mbar_wait(&q_empty[qt & 1], ((qt - 2) >> 1) & 1);   // S(qt - 2) has read it
+        mbar_arrive_expect_tx(&q_full[qt & 1], uint32_t(BM * 128));
+        tma_load_2d(sQ + (qt & 1) * BM * 128, &tmQKV, &q_full[qt & 1], head * DH, ta + qt * BM);
+      };
+      load_q(0);
       for (int qt = 0; qt < nq; ++qt) {
-        if (qt > 0) mbar_wait(q_empty, (qt - 1) & 1);  // S(qt-1) has read the previous Q tile
-        mbar_arrive_expect_tx(q_full, uint32_t(BM * 128));
-        tma_load_2d(sQ, &tmQKV, q_full, head * DH, ta + qt * BM);
-        mbar_wait(q_full, qt & 1);
+        if (qt + 1 < nq) load_q(qt + 1);               // the next tile's Q loads under this tile's work
+        const uint64_t qd = umma_desc_sw128(smem_u32(sQ + (qt & 1) * BM * 128));
+        mbar_wait(&q_full[qt & 1], (qt >> 1) & 1);
         if (qt == 0) mbar_wait(kv_full, 0);
         if (qt > 0) mbar_wait(o_empty, (qt - 1) & 1);  // O(qt-1) read: S / P / O columns may be rewritten
         tc_fence_after();
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
                         k);
         }
         tc_commit(s_full);
-        tc_commit(q_empty);
+        tc_commit(&q_empty[qt & 1]);
         mbar_wait(p_ready, qt & 1);
         tc_fence_after();
         // O = P V: K = L keys in steps of 16; P_A (keys < L/2) at column 0, P_B at column L/2
@@ -160,33 +167,50 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
     for (int qt = 0; qt < nq; ++qt) {
       mbar_wait(s_full, qt & 1);
       tc_fence_after();
-      float m = -INFINITY;
-      for (int cc = 0; cc < half; cc += 32) {          // row max over this part's valid keys
-        uint32_t sv[32];
-        tmem_ld32(tl + uint32_t(c0 + cc), sv);
-        tmem_ld_wait_regs(sv);
+      constexpr int NB = LMAX <= 256 ? 1 : 4;         // (two CTAs per SM at LMAX 256: 96 registers)
+      // the part's half row in batches of 32 NB columns (NB loads, one wait; loads clamped into the row,
+      // columns past the half masked): the max, then P = 2^(s q - m q) (0 past the text), bf16, over S
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      for (int cb = 0; cb < half; cb += 32 * NB) {
+        uint32_t sv[NB][32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + cc + i < len) m = fmaxf(m, __uint_as_float(sv[i]));
+        for (int j = 0; j < NB; ++j) tmem_ld32(tl + uint32_t(min(c0 + cb + 32 * j, L - 32)), sv[j]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            asm volatile("" : "+r"(sv[j][i]));
+            const int c = cb + 32 * j + i;
+            if (c < half && c0 + c < len) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(sv[j][i]));
+          }
       }
+      float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       xmax[hh * BM + r] = m;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");   // the two warps of this quadrant
       m = fmaxf(m, xmax[(hh ^ 1) * BM + r]);
       const float mq = m * qs;                          // len >= 1: finite for every row of the tile
       float l = 0.f;
-      for (int cc = 0; cc < half; cc += 32) {          // P = 2^(s q - m q) (0 past the text), bf16, over S
-        uint32_t sv[32], pk[16];
-        tmem_ld32(tl + uint32_t(c0 + cc), sv);
-        tmem_ld_wait_regs(sv);
+      for (int cb = 0; cb < half; cb += 32 * NB) {
+        uint32_t sv[NB][32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int key = c0 + cc + 2 * i;
-          const float e0 = key < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i]), qs, -mq)) : 0.f;
-          const float e1 = key + 1 < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i + 1]), qs, -mq)) : 0.f;
-          l += e0 + e1;
-          pk[i] = pack_bf16x2(e0, e1);
+        for (int j = 0; j < NB; ++j) tmem_ld32(tl + uint32_t(min(c0 + cb + 32 * j, L - 32)), sv[j]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            asm volatile("" : "+r"(sv[j][2 * i]), "+r"(sv[j][2 * i + 1]));
+            const int c = cb + 32 * j + 2 * i, key = c0 + c;
+            const float e0 = (c < half && key < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i]), qs, -mq)) : 0.f;
+            const float e1 = (c + 1 < half && key + 1 < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i + 1]), qs, -mq)) : 0.f;
+            l += e0 + e1;
+            pk[i] = pack_bf16x2(e0, e1);
+          }
+          // P of columns c0 + cb + 32 j.. lands on S columns c0 + (cb + 32 j) / 2.. (already read)
+          if (cb + 32 * j < half) tmem_st16(tl + uint32_t(c0 + (cb + 32 * j) / 2), pk);
         }
-        tmem_st16(tl + uint32_t(c0 + cc / 2), pk);      // P of keys c0 + cc .. : S columns already read
       }
       xsum[hh * BM + r] = l;
       tmem_st_wait();
@@ -241,10 +265,11 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
 // (the next item's K/V load under the current item's work), and the single MMA thread issues S(e + 1)
 // before it waits for the softmax of e to issue PV(e) -- so the softmax of one element runs under the
 // tensor work (and loads) of its neighbours instead of in series with them.
-constexpr int PIPE_OFF_Q = 2048;
-constexpr int PIPE_OFF_KV = PIPE_OFF_Q + BM * 128;                 // [2 buffers][K 256 rows | V 256 rows]
+constexpr int PIPE_OFF_Q = 5120;   // [2 buffers] Q tile of an element, after the max / sum exchange ([256, 4352))
+constexpr int PIPE_OFF_KV = PIPE_OFF_Q + 2 * BM * 128;             // [2 buffers][K 256 rows | V 256 rows]
 constexpr int PIPE_KV = 2 * 256 * 128;                             // 64 KB per buffer
-constexpr int PIPE_SMEM = PIPE_OFF_KV + 2 * PIPE_KV;              // 146 KB
+constexpr int PIPE_SMEM = PIPE_OFF_KV + 2 * PIPE_KV;              // 165 KB
+static_assert(PIPE_OFF_Q >= 256 + 2 * 4 * BM * 4 && PIPE_OFF_Q % 1024 == 0, "Q tiles after the exchange arrays");
 
 __global__ void __launch_bounds__(THREADS, 1)
     attn_long_pipe_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ cu,
@@ -253,9 +278,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem);   // [2] per KV buffer
   uint64_t* kv_free = kv_full + 2;     // [2] commit after the item's last PV
-  uint64_t* q_full = kv_free + 2;
-  uint64_t* q_empty = q_full + 1;      // commit after S(e)
-  uint64_t* s_full = q_empty + 1;      // [2] per TMEM region
+  uint64_t* q_full = kv_free + 2;      // [2] per Q buffer (element e: buffer e % 2)
+  uint64_t* q_empty = q_full + 2;      // [2] commit after S(e)
+  uint64_t* s_full = q_empty + 2;      // [2] per TMEM region
   uint64_t* p_ready = s_full + 2;      // [2] 8 warps
   uint64_t* o_full = p_ready + 2;      // [2] commit
   uint64_t* o_empty = o_full + 2;      // [2] 4 warps
@@ -286,8 +311,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&o_full[i], 1);
       mbar_init(&o_empty[i], 4);
     }
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -303,7 +330,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       griddep_wait();
       const uint32_t id_pv = umma_idesc_bf16(BM, DH) | (1u << 16);
-      const uint64_t qd = umma_desc_sw128(smem_u32(sQ));
+
       // the CTA's valid items, walked twice in step: `ld` = next item whose K/V to load, `e` elements
       int g_ld = int(blockIdx.x), n_ld = 0;            // loads issued (items)
       auto load_next = [&]() -> bool {                 // K/V of the next valid item into buffer n_ld % 2
@@ -343,12 +370,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         return false;
       };
       struct El { int n_it, ta, len, head, qt; };
+      auto load_q = [&](int ee, const El& x) {        // Q tile of element ee -> Q buffer ee % 2
+        const int b = ee & 1;
+        if (ee >= 2) mbar_wait(&q_empty[b], ((ee - 2) >> 1) & 1);   // S(ee - 2) has read the buffer
+        mbar_arrive_expect_tx(&q_full[b], uint32_t(BM * 128));
+        tma_load_2d(sQ + b * BM * 128, &tmQKV, &q_full[b], x.head * DH, x.ta + x.qt * BM);
+      };
       auto issue_s = [&](int ee, const El& x) {       // S(ee) = Q K^T into TMEM region ee % 2
         const int rg = ee & 1;
-        if (ee > 0) mbar_wait(q_empty, (ee - 1) & 1);  // S(ee-1) has read the Q buffer
-        mbar_arrive_expect_tx(q_full, uint32_t(BM * 128));
-        tma_load_2d(sQ, &tmQKV, q_full, x.head * DH, x.ta + x.qt * BM);
-        mbar_wait(q_full, ee & 1);
+        const uint64_t qd = umma_desc_sw128(smem_u32(sQ + (ee & 1) * BM * 128));
+        mbar_wait(&q_full[ee & 1], (ee >> 1) & 1);
         if (x.qt == 0) mbar_wait(&kv_full[x.n_it & 1], (x.n_it >> 1) & 1);
         if (ee >= 2) mbar_wait(&o_empty[rg], ((ee - 2) >> 1) & 1);   // region's previous element drained
         tc_fence_after();
@@ -359,7 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_mma_bf16(tmem + uint32_t(256 * rg), qd + uint64_t(k * 2), kd + uint64_t(k * 2), umma_idesc_bf16(BM, uint32_t(L)),
                       k);
         tc_commit(&s_full[rg]);
-        tc_commit(q_empty);
+        tc_commit(&q_empty[ee & 1]);
       };
       auto issue_pv = [&](int ee, const El& x) {
         const int rg = ee & 1;
@@ -379,19 +410,32 @@ __global__ void __launch_bounds__(THREADS, 1)
           load_next();
         }
       };
-      El cur{}, nxt{};
+      // iteration e: Q of element e + 2 loads (its buffer freed by S(e)), S(e + 1) issues, then P V(e) once
+      // the softmax of e is done -- the Q load latency stays off the issue chain
+      El cur{}, nxt{}, nxt2{};
       bool have = next_elem();
-      if (have) cur = El{n_it, ta, len, head, qt};
+      if (have) {
+        cur = El{n_it, ta, len, head, qt};
+        load_q(0, cur);
+      }
+      bool more = have && next_elem();
+      if (more) {
+        nxt = El{n_it, ta, len, head, qt};
+        load_q(1, nxt);
+      }
       if (have) issue_s(0, cur);
       for (e = 0; have; ++e) {
-        const bool more = next_elem();
-        if (more) {
-          nxt = El{n_it, ta, len, head, qt};
-          issue_s(e + 1, nxt);
+        const bool more2 = more && next_elem();
+        if (more2) {
+          nxt2 = El{n_it, ta, len, head, qt};
+          load_q(e + 2, nxt2);
         }
+        if (more) issue_s(e + 1, nxt);
         issue_pv(e, cur);
         cur = nxt;
+        nxt = nxt2;
         have = more;
+        more = more2;
       }
     }
   } else if (warp >= 2) {
@@ -411,33 +455,52 @@ __global__ void __launch_bounds__(THREADS, 1)
         float* xs = xsum + rg * 2 * BM;
         mbar_wait(&s_full[rg], (e >> 1) & 1);
         tc_fence_after();
-        float m = -INFINITY;
-        for (int cc = 0; cc < half; cc += 32) {
-          uint32_t sv[32];
-          tmem_ld32(tl + uint32_t(c0 + cc), sv);
-          tmem_ld_wait_regs(sv);
+        // the warp's half row (96 or 128 columns) in two batches of 64 (two loads, one wait each; the
+        // 32 columns past a 96-column half are read and masked, their P not stored): the max, then P
+        constexpr int NB = 2;
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + cc + i < len) m = fmaxf(m, __uint_as_float(sv[i]));
+        for (int cb = 0; cb < 128; cb += 32 * NB) {
+          uint32_t sv[NB][32];
+#pragma unroll
+          for (int j = 0; j < NB; ++j) tmem_ld32(tl + uint32_t(c0 + cb + 32 * j), sv[j]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              asm volatile("" : "+r"(sv[j][i]));
+              const int c = cb + 32 * j + i;
+              if (c < half && c0 + c < len) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(sv[j][i]));
+            }
         }
+        float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         xm[hh * BM + r] = m;
         asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
         m = fmaxf(m, xm[(hh ^ 1) * BM + r]);
         const float mq = m * qs;
         float l = 0.f;
-        for (int cc = 0; cc < half; cc += 32) {
-          uint32_t sv[32], pk[16];
-          tmem_ld32(tl + uint32_t(c0 + cc), sv);
-          tmem_ld_wait_regs(sv);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int key = c0 + cc + 2 * i;
-            const float e0 = key < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i]), qs, -mq)) : 0.f;
-            const float e1 = key + 1 < len ? ex2_approx(fmaf(__uint_as_float(sv[2 * i + 1]), qs, -mq)) : 0.f;
-            l += e0 + e1;
-            pk[i] = pack_bf16x2(e0, e1);
+        for (int cb = 0; cb < 128; cb += 32 * NB) {
+          uint32_t sv[NB][32];
+#pragma unroll
+          for (int j = 0; j < NB; ++j) tmem_ld32(tl + uint32_t(c0 + cb + 32 * j), sv[j]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              asm volatile("" : "+r"(sv[j][2 * i]), "+r"(sv[j][2 * i + 1]));
+              const int c = cb + 32 * j + 2 * i, key = c0 + c;
+              const float e0 = (c < half && key < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i]), qs, -mq)) : 0.f;
+              const float e1 = (c + 1 < half && key + 1 < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i + 1]), qs, -mq)) : 0.f;
+              l += e0 + e1;
+              pk[i] = pack_bf16x2(e0, e1);
+            }
+            // P over S columns this warp has already read (c0 + (cb + 32 j) / 2 < c0 + cb + 64)
+            if (cb + 32 * j < half) tmem_st16(tl + uint32_t(c0 + (cb + 32 * j) / 2), pk);
           }
-          tmem_st16(tl + uint32_t(c0 + cc / 2), pk);
         }
         xs[hh * BM + r] = l;
         tmem_st_wait();

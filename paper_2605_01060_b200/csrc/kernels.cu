@@ -503,12 +503,12 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
 // 128 rows (8 warps x 16) are staged in turn.  The per-row arithmetic is the text-tiled kernel's:
 // 16-row query tiles and 16-key blocks aligned to the text start, mma.sync m16n8k16 with P split
 // hi+lo, online softmax over the key blocks in order (so long and short texts follow one rule).
-template <int DH>
-#ifndef ATT_LONG_WARPS
-#define ATT_LONG_WARPS 16
-#endif
+// W warps per CTA (query blocks of 16 W rows); the launcher splits the long texts into length classes so
+// the K/V buffers (and the CTAs per SM) fit the class: (64, 128], (128, 192], (192, 256] with 8 warps,
+// (256, 512] with 16 -- a 150-token text no longer takes a whole SM's shared memory sized for 512
+template <int DH, int W>
 struct LongAtt {
-  static constexpr int WARPS = ATT_LONG_WARPS;   // one 16-row query tile per warp
+  static constexpr int WARPS = W;                // one 16-row query tile per warp
   static constexpr int QROWS = 16 * WARPS;
   static constexpr int LDS = DH + 8;
   static constexpr int CH = DH / 8;
@@ -516,11 +516,12 @@ struct LongAtt {
   static size_t smem(int max_len) { return size_t(2 * kv_rows(max_len) + QROWS + 16) * LDS * 2; }
 };
 
-template <int DH>
-__global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel(
+template <int DH, int W>
+__global__ void __launch_bounds__(W * 32) attention_long_kernel(
     const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu, const int32_t* __restrict__ texts,
-    int32_t tok0, int heads, uint16_t* __restrict__ out, float qscale, int kv_rows, int max_handled) {
-  using A = LongAtt<DH>;
+    int32_t tok0, int heads, uint16_t* __restrict__ out, float qscale, int kv_rows, int min_handled,
+    int max_handled) {
+  using A = LongAtt<DH, W>;
   constexpr int LDS = A::LDS, CH = A::CH;
   extern __shared__ __align__(16) uint16_t att_sm[];
   uint16_t* sK = att_sm;                         // [kv_rows][LDS]
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(LongAtt<DH>::WARPS * 32) attention_long_kernel
   const int h = blockIdx.y;
   const int d = heads * DH, ld = 3 * d;
   const int32_t a = cu[txt] - tok0, len = cu[txt + 1] - cu[txt];
-  if (len > max_handled) return;                 // left to the tcgen05 long-text kernel (attn_long_tc.cu)
+  if (len > max_handled || len <= min_handled) return;   // another length class (or the tcgen05 kernel)
   const int nt = (len + 15) >> 4;
   for (int i = tid; i < len * CH; i += blockDim.x) {
     const int r = i / CH, c = i - r * CH;
@@ -786,11 +787,14 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
     attention_text_kernel<DH, HG><<<grid, TA::WARPS * 32, TA::smem(max_len), st>>>(                           \
         qkv, cu, tok0, ntok, win, heads, out, qscale, TA::rows(max_len));                                    \
     if (max_len > ATT_SHORT && d_long) {                                                                     \
-      using LA = LongAtt<DH>;                                                                                \
+      using LA8 = LongAtt<DH, 8>;                                                                            \
+      using LA16 = LongAtt<DH, 16>;                                                                          \
       static bool lattr_##DH = false;                                                                        \
       if (!lattr_##DH) {                                                                                     \
-        cudaFuncSetAttribute(attention_long_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
-                             int(LA::smem(512)));                                                            \
+        cudaFuncSetAttribute(attention_long_kernel<DH, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                             int(LA8::smem(256)));                                                           \
+        cudaFuncSetAttribute(attention_long_kernel<DH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                             int(LA16::smem(512)));                                                          \
         lattr_##DH = true;                                                                                   \
       }                                                                                                      \
       if (max_len > 512) return cudaErrorInvalidValue;                                                       \
@@ -801,11 +805,19 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
         cudaError_t e_ = launch_attn_long_tc(qkv, cu, d_long, n_long, tok0, ntok, heads, out, st);            \
         if (e_ != cudaSuccess) return e_;                                                                    \
       }                                                                                                      \
-      if (n_long > 0)                                                                                        \
-        attention_long_kernel<DH><<<dim3(unsigned(n_long), unsigned(heads)), LA::WARPS * 32,                  \
-                                    LA::smem(tc_ ? ATT_TILE_ROWS : max_len), st>>>(                          \
-            qkv, cu, d_long, tok0, heads, out, qscale, LA::kv_rows(tc_ ? ATT_TILE_ROWS : max_len),            \
-            tc_ ? ATT_TILE_ROWS : 1 << 30);                                                                   \
+      const int top_ = tc_ ? ATT_TILE_ROWS : max_len;                                                        \
+      const dim3 lg_{unsigned(n_long), unsigned(heads), 1u};                                                 \
+      for (int lo_ = ATT_SHORT; n_long > 0 && lo_ < top_;) {   /* length classes (lo_, hi_] */             \
+        const int hi_ = lo_ < 128 ? 128 : lo_ < 192 ? 192 : lo_ < 256 ? 256 : 512;                          \
+        const int cap_ = hi_ < top_ ? hi_ : top_;                                                            \
+        if (hi_ <= 256)                                                                                      \
+          attention_long_kernel<DH, 8><<<lg_, 8 * 32, LA8::smem(cap_), st>>>(                                  \
+              qkv, cu, d_long, tok0, heads, out, qscale, LA8::kv_rows(cap_), lo_, hi_);                        \
+        else                                                                                                 \
+          attention_long_kernel<DH, 16><<<lg_, 16 * 32, LA16::smem(cap_), st>>>(                               \
+              qkv, cu, d_long, tok0, heads, out, qscale, LA16::kv_rows(cap_), lo_, hi_);                       \
+        lo_ = hi_;                                                                                           \
+      }                                                                                                      \
     } else if (max_len > ATT_SHORT) {   /* list of long texts unknown: scalar per-(text, head) kernel */    \
       constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \
       attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W1), W1 * 32, 0, st>>>(                       \

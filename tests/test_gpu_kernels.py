@@ -123,11 +123,15 @@ def ref_attention(qkv, cu, heads, dh):
     return out, vmax
 
 
-@pytest.mark.parametrize("heads,dh,maxlen", [(12, 32, 128), (4, 16, 64), (12, 32, 20), (16, 64, 300), (12, 32, 65)])
+@pytest.mark.parametrize("heads,dh,maxlen", [(12, 32, 128), (4, 16, 64), (12, 32, 20), (16, 64, 300), (12, 32, 65),
+                                             (16, 64, 512), (12, 32, 257)])
 def test_attention_vs_torch(N, heads, dh, maxlen):
     rng = np.random.default_rng(heads * dh + maxlen)
     lens = rng.integers(1, maxlen + 1, size=97).astype(np.int32)
     lens[:6] = [1, 2, 31, min(33, maxlen), min(64, maxlen), min(65, maxlen)]   # tile/long kernel boundary
+    # the long kernel's length-class edges (64, 128], (128, 192], (192, 256], (256, 512]
+    edges = [e for e in (128, 129, 192, 193, 256, 257) if e <= maxlen]
+    lens[6:6 + len(edges)] = edges
     lens[-1] = maxlen
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     T = int(cu[-1])

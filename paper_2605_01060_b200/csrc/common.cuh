@@ -379,6 +379,17 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 // Instruction descriptor for kind::f16: D=f32, A=B=bf16, both K-major, shape M x N.
+// The same for a K-major operand staged with 64-byte swizzle (rows of 64 B = 32 bf16, 8-row atoms of 512 B):
+// layout type 4 = SWIZZLE_64B, SBO = 512 B.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr & 0x3FFFF) >> 4);     // start address  [0,14)
+  d |= uint64_t(1) << 16;                        // LBO (ignored for swizzled K-major) [16,30)
+  d |= uint64_t(512 >> 4) << 32;                 // SBO            [32,46)
+  d |= uint64_t(1) << 46;                        // version = 1    [46,48)
+  d |= uint64_t(4) << 61;                        // SWIZZLE_64B    [61,64)
+  return d;
+}
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4)            // c_format  = F32
          | (1u << 7)          // a_format  = BF16

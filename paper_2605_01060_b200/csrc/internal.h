@@ -72,6 +72,12 @@ cudaError_t init_tma_encoder();
 // Programmatic dependent launch for the GEMM-class kernels (env SURGE_PDL=0 disables).
 bool pdl_enabled();
 cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+cudaError_t make_tmap_bf16_k32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// k-block width of the cluster-pair LN GEMMs (ln_pair.cu): 64 (128-byte swizzle), or 32 (64-byte swizzle, twice
+// the ring stages: measured slower, bge-base FFN2 + LN 382 -> 431 ms per 500K texts)
+#ifndef LN_PAIR_KB
+#define LN_PAIR_KB 64
+#endif
 // Output map for the GEMM epilogue's TMA stores: box 32 rows x 32 columns, 64-byte swizzle.
 cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols);
 int gemm_bn_for(int N, int K, int epi);

@@ -33,8 +33,11 @@ template <int BNC, int CL>   // columns per CTA (d / CL), CTAs per cluster
 struct LnPairCfg {
   static constexpr int N_MMA = BNC <= 256 ? 1 : 2;            // 192 / 256: one MMA, 384: 2 x 192, 512: 2 x 256
   static constexpr int MMA_N = BNC / N_MMA;
-  static constexpr int A_STAGE = BM * 128;                    // 16 KB
-  static constexpr int B_STAGE = BNC * 128;                   // 48 / 64 KB
+  static constexpr int KB = LN_PAIR_KB;                       // k-block width (elements)
+  static constexpr int ROWB = KB * 2;                         // bytes per row of a k-block (= swizzle span)
+  static constexpr int A_STAGE = BM * ROWB;                   // 8 / 16 KB
+  static constexpr int B_STAGE = BNC * ROWB;                  // 24 / 32 KB (KB 32), 48 / 64 KB (KB 64)
+  static constexpr int B_BOX = KB == 32 ? 128 : 64;           // rows per B box (the weight maps, model.cu)
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int HEAD = 1024;
   static constexpr int STATS = 2 * 2 * CL * BM * 16;          // [tile parity][2 CL parts][128 rows] float4
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n0 = rank * BNC;
   const int t0 = int(blockIdx.x) / CL, dt = int(gridDim.x) / CL;
   const int m_tiles = (M + BM - 1) / BM;
-  const int num_kb = K / 64;
+  const int num_kb = K / T::KB;
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t pol_w = l2_policy_evict_last();
       griddep_wait();
       uint32_t c = 0;
-      constexpr int NBOX = 1 + BNC / 64;                  // A + this CTA's B rows in 64-row boxes
+      constexpr int NBOX = 1 + BNC / T::B_BOX;            // A + this CTA's B rows in B_BOX-row boxes
       for (int t = t0; t < m_tiles; t += dt)
         for (int kb = 0; kb < num_kb; ++kb, ++c) {
           const int s = int(c % STAGES);
@@ -158,10 +161,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(&empty[s], ph ^ 1);
             if (b == 0) {
               mbar_arrive_expect_tx(&full[s], uint32_t(T::STAGE));
-              tma_load_2d(sRing + s * T::STAGE, &tmA, &full[s], kb * 64, t * BM);
+              tma_load_2d(sRing + s * T::STAGE, &tmA, &full[s], kb * T::KB, t * BM);
             } else {
-              tma_load_2d_hint(sRing + s * T::STAGE + T::A_STAGE + (b - 1) * 64 * 128, &tmB, &full[s], kb * 64,
-                               n0 + (b - 1) * 64, pol_w);
+              tma_load_2d_hint(sRing + s * T::STAGE + T::A_STAGE + (b - 1) * T::B_BOX * T::ROWB, &tmB, &full[s],
+                               kb * T::KB, n0 + (b - 1) * T::B_BOX, pol_w);
             }
           }
         }
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     griddep_launch_dependents();
     // -------------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(BM, T::MMA_N);
-    const uint64_t r0 = umma_desc_sw128(smem_u32(sRing));
+    const uint64_t r0 = T::KB == 32 ? umma_desc_sw64(smem_u32(sRing)) : umma_desc_sw128(smem_u32(sRing));
     uint32_t c = 0;
     int it = 0;
     for (int t = t0; t < m_tiles; t += dt, ++it) {
@@ -184,11 +187,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint64_t ad = r0 + uint64_t((s * T::STAGE) >> 4);
           const uint64_t bd = r0 + uint64_t((s * T::STAGE + T::A_STAGE) >> 4);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < T::KB / 16; ++k)
 #pragma unroll
             for (int j = 0; j < T::N_MMA; ++j)
               tc_mma_bf16(tmem_base + j * T::MMA_N, ad + uint64_t(k * 2),
-                          bd + uint64_t((j * T::MMA_N * 128 + k * 32) >> 4), idesc, (kb | k) != 0);
+                          bd + uint64_t((j * T::MMA_N * T::ROWB + k * 32) >> 4), idesc, (kb | k) != 0);
           tc_commit(&empty[s]);
           if (kb == num_kb - 1) tc_commit(tfull);
         }
@@ -270,7 +273,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t st) {
 
 }  // namespace
 
-bool ln_pair_supported(int d, int k) { return (d == 768 || d == 1024) && k % 64 == 0 && k > 0; }
+bool ln_pair_supported(int d, int k) { return (d == 768 || d == 1024) && k % LN_PAIR_KB == 0 && k > 0; }
 
 cudaError_t launch_ln_pair(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0) return cudaSuccess;

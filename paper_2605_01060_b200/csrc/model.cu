@@ -209,8 +209,13 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
       SURGE_TRY(make_tmap_bf16(&L.tm_w1, L.w1, f, d, gemm_b_box_rows(int(f), int(d), EPI_BIAS_GELU)));
       SURGE_TRY(make_tmap_bf16(&L.tm_w2, L.w2, d, f, gemm_b_box_rows(int(d), int(f), ln_epi)));
       if (ln_pair_supported(int(d), int(d))) {
-        SURGE_TRY(make_tmap_bf16(&L.tm_wo_p64, L.wo, d, d, 64));
-        SURGE_TRY(make_tmap_bf16(&L.tm_w2_p64, L.w2, d, f, 64));
+        if (LN_PAIR_KB == 32) {          // 32-wide k-blocks, 128-row B boxes (ln_pair.cu)
+          SURGE_TRY(make_tmap_bf16_k32(&L.tm_wo_p64, L.wo, d, d, 128));
+          SURGE_TRY(make_tmap_bf16_k32(&L.tm_w2_p64, L.w2, d, f, 128));
+        } else {
+          SURGE_TRY(make_tmap_bf16(&L.tm_wo_p64, L.wo, d, d, 64));
+          SURGE_TRY(make_tmap_bf16(&L.tm_w2_p64, L.w2, d, f, 64));
+        }
       }
       if (mlp_fused_supported(int(d), int(f))) {
         SURGE_TRY(make_tmap_bf16(&L.tm_wo_mlp, L.wo, d, d, mlp_w2_box_rows(int(d))));
@@ -308,6 +313,12 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   SURGE_TRY(make_tmap_bf16(&tmO, ws.O, ntok, d, 128));
   SURGE_TRY(make_tmap_bf16(&tmX1, ws.X1, ntok, d, 128));
   SURGE_TRY(make_tmap_bf16(&tmH, ws.H, ntok, f, 128));
+  CUtensorMap tmO32, tmH32;                   // the cluster-pair LN GEMMs' A operands (LN_PAIR_KB = 32)
+  const bool kb32 = LN_PAIR_KB == 32 && ln_pair_ && ln_pair_supported(d, d);
+  if (kb32) {
+    SURGE_TRY(make_tmap_bf16_k32(&tmO32, ws.O, ntok, d, 128));
+    SURGE_TRY(make_tmap_bf16_k32(&tmH32, ws.H, ntok, f, 128));
+  }
   SURGE_TRY(make_tmap_store_bf16(&smX, ws.X, ntok, d));
   SURGE_TRY(make_tmap_store_bf16(&smQKV, ws.QKV, ntok, 3 * d));
   SURGE_TRY(make_tmap_store_bf16(&smX1, ws.X1, ntok, d));
@@ -403,6 +414,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_gemm(g, st));
     } else if (pair) {
       g.tmB = &L.tm_wo_p64;
+      if (kb32) g.tmA = &tmO32;
       SURGE_TRY(launch_ln_pair(g, st));
     } else {
       g.epi = EPI_BIAS_RES; g.C = reinterpret_cast<uint16_t*>(ws.V);
@@ -437,6 +449,7 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       SURGE_TRY(launch_gemm(g, st));
     } else if (pair2) {
       g.tmB = &L.tm_w2_p64;
+      if (kb32) g.tmA = &tmH32;
       SURGE_TRY(launch_ln_pair(g, st));
     } else {
       g.epi = EPI_BIAS_RES; g.C = reinterpret_cast<uint16_t*>(ws.V);

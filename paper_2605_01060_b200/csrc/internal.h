@@ -140,9 +140,29 @@ cudaError_t launch_window_index(const int32_t* cu, int64_t n_texts, int32_t tok0
                                 cudaStream_t st);
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
                              int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
-                             uint16_t* out, cudaStream_t st, const int32_t* d_long = nullptr, int32_t n_long = 0);
+                             uint16_t* out, cudaStream_t st, const int32_t* d_long = nullptr, int32_t n_long = 0,
+                             const int32_t* long_class_off = nullptr, int* n_launched = nullptr);
 // d_long: device int32[n_long], indices (relative to cu) of the texts longer than 64 tokens;
 // nullptr = unknown (all texts are scanned by the scalar per-(text, head) kernel).
+// long_class_off (host, ATT_LONG_CLASSES + 1 entries, optional): d_long is grouped by length class
+// (attn_long_class) and class c is d_long[off[c], off[c + 1]) -- each class is launched over exactly its
+// texts; without it every class launch covers all of d_long and CTAs of other classes exit at once.
+// n_launched (optional): kernels launched.
+constexpr int ATT_LONG_CLASSES = 4;   // (64, 128], (128, 192], (192, 256], (256, 512]
+inline int attn_long_class(int32_t len) { return len <= 128 ? 0 : len <= 192 ? 1 : len <= 256 ? 2 : 3; }
+// Stable counting sort of text indices by length class; off[0..ATT_LONG_CLASSES] = class offsets.
+template <typename LenOf>
+inline void group_long_by_class(std::vector<int32_t>& idx, LenOf len_of, int32_t (&off)[ATT_LONG_CLASSES + 1]) {
+  int32_t cnt[ATT_LONG_CLASSES] = {0, 0, 0, 0};
+  for (int32_t i : idx) ++cnt[attn_long_class(len_of(i))];
+  off[0] = 0;
+  for (int c = 0; c < ATT_LONG_CLASSES; ++c) off[c + 1] = off[c] + cnt[c];
+  std::vector<int32_t> out(idx.size());
+  int32_t pos[ATT_LONG_CLASSES];
+  for (int c = 0; c < ATT_LONG_CLASSES; ++c) pos[c] = off[c];
+  for (int32_t i : idx) out[size_t(pos[attn_long_class(len_of(i))]++)] = i;
+  idx.swap(out);
+}
 // Row LayerNorm: y[r] = LN(v[r]) * gamma + beta, v fp32 [rows x d] -> bf16 (d in {768, 1024}).
 cudaError_t launch_layernorm(const float* v, int64_t rows, int d, const float* gamma, const float* beta, float eps,
                              uint16_t* y, cudaStream_t st);

@@ -766,7 +766,9 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_tex
 
 cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_texts, int32_t tok0,
                              int32_t ntok, int32_t max_len, int32_t* win, bool win_ready, int heads, int head_dim,
-                             uint16_t* out, cudaStream_t st, const int32_t* d_long, int32_t n_long) {
+                             uint16_t* out, cudaStream_t st, const int32_t* d_long, int32_t n_long,
+                             const int32_t* long_class_off, int* n_launched) {
+  int nl_ = 0;
   if (n_texts <= 0 || ntok <= 0) return cudaSuccess;
   constexpr int HG = ATT_HEADS_PER_CTA;
   if (heads % HG) return cudaErrorInvalidValue;
@@ -774,6 +776,7 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
   const int32_t nwin = (ntok + 63) >> 6;
   if (!win_ready)
     window_index_kernel<<<unsigned((n_texts + 1 + 255) / 256), 256, 0, st>>>(cu, n_texts, tok0, ntok, win);
+  nl_ += win_ready ? 1 : 2;                           // (window index) + the short-text kernel
 #define SURGE_ATT(DH)                                                                                        \
   case DH: {                                                                                                 \
     using TA = TextAtt<DH, HG>;                                                                               \
@@ -804,24 +807,29 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
       if (n_long > 0 && tc_) {                                                                              \
         cudaError_t e_ = launch_attn_long_tc(qkv, cu, d_long, n_long, tok0, ntok, heads, out, st);            \
         if (e_ != cudaSuccess) return e_;                                                                    \
+        nl_ += 2;                                                                                            \
       }                                                                                                      \
       const int top_ = tc_ ? ATT_TILE_ROWS : max_len;                                                        \
-      const dim3 lg_{unsigned(n_long), unsigned(heads), 1u};                                                 \
-      for (int lo_ = ATT_SHORT; n_long > 0 && lo_ < top_;) {   /* length classes (lo_, hi_] */             \
-        const int hi_ = lo_ < 128 ? 128 : lo_ < 192 ? 192 : lo_ < 256 ? 256 : 512;                          \
+      for (int c_ = 0, lo_ = ATT_SHORT; n_long > 0 && lo_ < top_; ++c_) {   /* classes (lo_, hi_] */       \
+        const int hi_ = c_ == 0 ? 128 : c_ == 1 ? 192 : c_ == 2 ? 256 : 512;                                \
         const int cap_ = hi_ < top_ ? hi_ : top_;                                                            \
-        if (hi_ <= 256)                                                                                      \
-          attention_long_kernel<DH, 8><<<lg_, 8 * 32, LA8::smem(cap_), st>>>(                                  \
-              qkv, cu, d_long, tok0, heads, out, qscale, LA8::kv_rows(cap_), lo_, hi_);                        \
-        else                                                                                                 \
-          attention_long_kernel<DH, 16><<<lg_, 16 * 32, LA16::smem(cap_), st>>>(                               \
-              qkv, cu, d_long, tok0, heads, out, qscale, LA16::kv_rows(cap_), lo_, hi_);                       \
+        const int32_t* tl_ = long_class_off ? d_long + long_class_off[c_] : d_long;                          \
+        const int32_t nc_ = long_class_off ? long_class_off[c_ + 1] - long_class_off[c_] : n_long;          \
+        const dim3 gc_{unsigned(nc_), unsigned(heads), 1u};                                                  \
+        if (nc_ > 0 && hi_ <= 256)                                                                           \
+          attention_long_kernel<DH, 8><<<gc_, 8 * 32, LA8::smem(cap_), st>>>(                                  \
+              qkv, cu, tl_, tok0, heads, out, qscale, LA8::kv_rows(cap_), lo_, hi_);                           \
+        else if (nc_ > 0)                                                                                    \
+          attention_long_kernel<DH, 16><<<gc_, 16 * 32, LA16::smem(cap_), st>>>(                               \
+              qkv, cu, tl_, tok0, heads, out, qscale, LA16::kv_rows(cap_), lo_, hi_);                          \
+        nl_ += nc_ > 0 ? 1 : 0;                                                                              \
         lo_ = hi_;                                                                                           \
       }                                                                                                      \
     } else if (max_len > ATT_SHORT) {   /* list of long texts unknown: scalar per-(text, head) kernel */    \
       constexpr int W1 = AttCfg<DH>::WARPS;                                                                  \
       attention_kernel<DH><<<blocks_for_warps(n_texts * heads, W1), W1 * 32, 0, st>>>(                       \
           qkv, cu, n_texts, tok0, heads, out, qscale, ATT_SHORT + 1);                                        \
+      nl_ += 1;                                                                                              \
     }                                                                                                        \
   } break;
   switch (head_dim) {
@@ -831,6 +839,7 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
     default: return cudaErrorInvalidValue;
   }
 #undef SURGE_ATT
+  if (n_launched) *n_launched = nl_;
   return cudaGetLastError();
 }
 

@@ -326,7 +326,8 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
   const bool P = prof && prof->on;
   double sum_l2 = 0;
   int32_t max_len = s_.max_pos;     // unknown -> assume long texts may be present
-  std::vector<int32_t> long_texts;    // chunk-relative indices of texts longer than 64 tokens
+  std::vector<int32_t> long_texts;    // chunk-relative indices of texts longer than 64 tokens (by length class)
+  int32_t long_off[ATT_LONG_CLASSES + 1] = {0, 0, 0, 0, 0};
   // fused QKV + attention (EPI_QKV_ATTN) when every text of the chunk fits one 128-row tile
   std::vector<int32_t> tiles;
   int32_t n_tiles = -1;
@@ -350,8 +351,10 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       sum_l2 += double(li) * double(li);
       if (li > 64) long_texts.push_back(int32_t(i - s0));
     }
-    if (!long_texts.empty() && !att_fused)
+    if (!long_texts.empty() && !att_fused) {
+      group_long_by_class(long_texts, [&](int32_t i) { return host_cu[s0 + i + 1] - host_cu[s0 + i]; }, long_off);
       SURGE_TRY(ws.tables.upload(ws.long_idx, long_texts.data(), long_texts.size(), st));
+    }
   }
   const double M = ntok, D = d, F = f;
   cudaEvent_t ev = nullptr;
@@ -389,10 +392,12 @@ cudaError_t DeviceModel::encode_chunk(Workspace& ws, const int32_t* d_ids, const
       if (P) prof->end(KK_QKV, st, ev, 2 * M * 3 * D * D, 2 * (M * D + 3 * D * D + M * 3 * D));
       // K5: O = attention(QKV) per text
       if (P) prof->begin(st, &ev);
+      int n_att = 0;
       SURGE_TRY(launch_attention(ws.QKV, cu, n, tok0, ntok, max_len, ws.win, true, s_.heads, d / s_.heads, ws.O, st,
-                                 host_cu ? ws.long_idx : nullptr, int32_t(long_texts.size())));
+                                 host_cu ? ws.long_idx : nullptr, int32_t(long_texts.size()),
+                                 host_cu ? long_off : nullptr, &n_att));
       if (P) prof->end(KK_ATTN, st, ev, 4 * D * sum_l2, M * (3 * D * 2 + D * 2));
-      k += 2 + (max_len > 64 ? 1 : 0);
+      k += 1 + n_att;
     }
     if (tail_fused_ && mlp_fused_ && mlp_fused_supported(d, f)) {
       // K6 + K7 + K8 fused: X = LN_o(FFN(X1) + X1), X1 = LN_a(O Wo^T + bo + X) kept on chip

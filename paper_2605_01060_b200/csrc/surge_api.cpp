@@ -1445,6 +1445,8 @@ surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int6
   std::vector<int32_t> lng;
   for (int64_t i = 0; i < n_texts; ++i)
     if (hcu[i + 1] - hcu[i] > 64) lng.push_back(int32_t(i));
+  int32_t off[surge::ATT_LONG_CLASSES + 1];
+  surge::group_long_by_class(lng, [&](int32_t i) { return hcu[size_t(i) + 1] - hcu[size_t(i)]; }, off);
   int32_t* win = nullptr;
   int32_t* dl = nullptr;
   if (cudaMalloc(&win, (size_t(ntok) / 64 + 2) * 4) != cudaSuccess) return SURGE_E_OOM;
@@ -1452,7 +1454,7 @@ surge_status surge_op_attention(const uint16_t* d_qkv, const int32_t* d_cu, int6
   cudaError_t e = cudaMemcpy(dl, lng.data(), lng.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = surge::launch_attention(d_qkv, d_cu, n_texts, hcu[0], ntok, max_len, win, false, heads, head_dim, d_out, st,
-                                dl, int32_t(lng.size()));
+                                dl, int32_t(lng.size()), off);
   cudaError_t e2 = cudaStreamSynchronize(st);
   cudaFree(win);
   cudaFree(dl);

@@ -33,6 +33,26 @@ constexpr int OFF_Q = 3072;           // after the barriers (< 256) and the max 
 // Two size classes, launched over the same text list (a CTA whose text is of the other class exits at
 // once): texts of <= 256 tokens use 256 TMEM columns and 81 KB of shared memory, so two CTAs share an SM
 // and hide each other's load / softmax latency; longer texts take the whole TMEM (one CTA per SM).
+// 2^a, 2^b (a, b <= 0: scores minus the row max).  ATT_LONG_EXP16 (measured slower: C4 attention 1,743 -> 1,860 ms
+// per 50K texts, off): one ex2.approx.f16x2 for the pair (half
+// the MUFU operations; the arguments rounded to f16 move 2^x by <= 2^-11 ln2 relative near 0 -- below the
+// bf16 rounding P gets anyway -- and results below 2^-24 flush to 0); otherwise two ex2.approx.f32.
+#ifndef ATT_LONG_EXP16
+#define ATT_LONG_EXP16 0
+#endif
+__device__ __forceinline__ void exp2_pair(float a, float b, float& ea, float& eb) {
+#if ATT_LONG_EXP16
+  uint32_t hx;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hx) : "f"(fmaxf(b, -24.f)), "f"(fmaxf(a, -24.f)));
+  asm("ex2.approx.f16x2 %0, %0;" : "+r"(hx));
+  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(ea), "=f"(eb) : "r"(hx));
+#else
+  ea = ex2_approx(a);
+  eb = ex2_approx(b);
+#endif
+}
+
 template <int LMAX>
 struct LongCfg {
   static constexpr int OFF_K = OFF_Q + 2 * BM * 128;   // two Q buffers (query tile qt: buffer qt % 2)
@@ -203,8 +223,10 @@ __global__ void __launch_bounds__(THREADS, LMAX <= 256 ? 2 : 1)
           for (int i = 0; i < 16; ++i) {
             asm volatile("" : "+r"(sv[j][2 * i]), "+r"(sv[j][2 * i + 1]));
             const int c = cb + 32 * j + 2 * i, key = c0 + c;
-            const float e0 = (c < half && key < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i]), qs, -mq)) : 0.f;
-            const float e1 = (c + 1 < half && key + 1 < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i + 1]), qs, -mq)) : 0.f;
+            float e0, e1;
+            exp2_pair(fmaf(__uint_as_float(sv[j][2 * i]), qs, -mq), fmaf(__uint_as_float(sv[j][2 * i + 1]), qs, -mq), e0, e1);
+            e0 = (c < half && key < len) ? e0 : 0.f;
+            e1 = (c + 1 < half && key + 1 < len) ? e1 : 0.f;
             l += e0 + e1;
             pk[i] = pack_bf16x2(e0, e1);
           }
@@ -493,8 +515,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int i = 0; i < 16; ++i) {
               asm volatile("" : "+r"(sv[j][2 * i]), "+r"(sv[j][2 * i + 1]));
               const int c = cb + 32 * j + 2 * i, key = c0 + c;
-              const float e0 = (c < half && key < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i]), qs, -mq)) : 0.f;
-              const float e1 = (c + 1 < half && key + 1 < len) ? ex2_approx(fmaf(__uint_as_float(sv[j][2 * i + 1]), qs, -mq)) : 0.f;
+              float e0, e1;
+              exp2_pair(fmaf(__uint_as_float(sv[j][2 * i]), qs, -mq), fmaf(__uint_as_float(sv[j][2 * i + 1]), qs, -mq), e0,
+                        e1);
+              e0 = (c < half && key < len) ? e0 : 0.f;
+              e1 = (c + 1 < half && key + 1 < len) ? e1 : 0.f;
               l += e0 + e1;
               pk[i] = pack_bf16x2(e0, e1);
             }

@@ -259,6 +259,100 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* __restrict
   if (t < b) tokens(std::integral_constant<int, 1>{}, t);
 }
 
+// K3 for d = 384 with 16-byte accesses: one warp per text, each half-warp one token at a time (two tokens per
+// warp step), lane l of a half owning the 8-column groups l, l + 16, l + 32 -- every load and store
+// instruction of a half-warp covers 256 contiguous bytes of a row; the row reductions are 4-step half-warp
+// butterflies.  gamma, beta and the token-type row are held as packed bf16 pairs (they are bf16 values of the
+// weight blob, so the packing is exact).  v = word + pos + type, mean, biased variance, as embed_ln_kernel.
+// Measured slower than the 8-byte one-warp-per-token-pair kernel (11.2 vs 8.9 ms per 2M texts: 116 registers,
+// two CTAs per SM instead of three; the kernel is latency-bound on its two dependent row reductions, not on
+// load width), so EMB_V16 is off.
+#ifndef EMB_V16
+#define EMB_V16 0
+#endif
+template <int D>
+__global__ void __launch_bounds__(256) embed_ln16_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ cu,
+                                                         int64_t n_texts, int32_t tok0, const uint16_t* __restrict__ word,
+                                                         const uint16_t* __restrict__ pos,
+                                                         const uint16_t* __restrict__ type,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta, float eps,
+                                                         uint16_t* __restrict__ x) {
+  constexpr int PER = D / 128;                    // 16-byte groups per lane
+  static_assert(D % 128 == 0, "d");
+  const int64_t text = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, hl = lane & 15, hw = lane >> 4;
+  if (text >= n_texts) return;
+  const int32_t a = cu[text], b = cu[text + 1];
+  uint32_t gp[PER][4], bp[PER][4], tp[PER][4];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int g = hl + 16 * i;
+    const float4 g0 = reinterpret_cast<const float4*>(gamma)[2 * g], g1 = reinterpret_cast<const float4*>(gamma)[2 * g + 1];
+    const float4 b0 = reinterpret_cast<const float4*>(beta)[2 * g], b1 = reinterpret_cast<const float4*>(beta)[2 * g + 1];
+    gp[i][0] = pack_bf16x2(g0.x, g0.y); gp[i][1] = pack_bf16x2(g0.z, g0.w);
+    gp[i][2] = pack_bf16x2(g1.x, g1.y); gp[i][3] = pack_bf16x2(g1.z, g1.w);
+    bp[i][0] = pack_bf16x2(b0.x, b0.y); bp[i][1] = pack_bf16x2(b0.z, b0.w);
+    bp[i][2] = pack_bf16x2(b1.x, b1.y); bp[i][3] = pack_bf16x2(b1.z, b1.w);
+    const uint4 tt = reinterpret_cast<const uint4*>(type)[g];
+    tp[i][0] = tt.x; tp[i][1] = tt.y; tp[i][2] = tt.z; tp[i][3] = tt.w;
+  }
+  for (int32_t t0 = a; t0 < b; t0 += 2) {        // warp-uniform trip count: both halves run the shuffles
+    const int32_t t = t0 + hw;
+    const bool ok = t < b;
+    const int32_t tt = ok ? t : t0;
+    const int32_t id = ids[tt];
+    const uint4* wr = reinterpret_cast<const uint4*>(word + size_t(id) * D);
+    const uint4* pr = reinterpret_cast<const uint4*>(pos + size_t(tt - a) * D);
+    uint4 w4[PER], p4[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      w4[i] = __ldg(wr + hl + 16 * i);
+      p4[i] = __ldg(pr + hl + 16 * i);
+    }
+    float v[PER][8];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const uint32_t wv[4] = {w4[i].x, w4[i].y, w4[i].z, w4[i].w}, pv[4] = {p4[i].x, p4[i].y, p4[i].z, p4[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[i][2 * j] = bf16lo(wv[j]) + bf16lo(pv[j]) + bf16lo(tp[i][j]);
+        v[i][2 * j + 1] = bf16hi(wv[j]) + bf16hi(pv[j]) + bf16hi(tp[i][j]);
+        s += v[i][2 * j] + v[i][2 * j + 1];
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s * (1.0f / D);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float dv = v[i][k] - mean;
+        q += dv * dv;
+      }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float rstd = rsqrtf(q * (1.0f / D) + eps);
+    if (ok) {
+      uint4* xr = reinterpret_cast<uint4*>(x + size_t(t - tok0) * D);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        uint32_t o4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float y0 = (v[i][2 * j] - mean) * rstd * bf16lo(gp[i][j]) + bf16lo(bp[i][j]);
+          const float y1 = (v[i][2 * j + 1] - mean) * rstd * bf16hi(gp[i][j]) + bf16hi(bp[i][j]);
+          o4[j] = pack_bf16x2(y0, y1);
+        }
+        xr[hl + 16 * i] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------- K5 varlen attention
 // One warp per (text, head).  Lane j owns query row qb+j; the text's K/V rows for this head are
 // staged 32 at a time in shared memory as fp32 and read as broadcasts.  Scores of a 32-key tile
@@ -753,6 +847,10 @@ cudaError_t launch_embed_ln(const int32_t* ids, const int32_t* cu, int64_t n_tex
   case DD:                                                                                                   \
     embed_ln_kernel<DD><<<grid, 256, 0, st>>>(ids, cu, n_texts, tok0, word, pos, type, gamma, beta, eps, x); \
     break;
+  if (EMB_V16 && d == 384) {
+    embed_ln16_kernel<384><<<grid, 256, 0, st>>>(ids, cu, n_texts, tok0, word, pos, type, gamma, beta, eps, x);
+    return cudaGetLastError();
+  }
   switch (d) {
     SURGE_EMB(64)
     SURGE_EMB(384)

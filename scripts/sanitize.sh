@@ -13,9 +13,11 @@ for tool in memcheck racecheck synccheck; do
 done
 # the round-2 kernels (tcgen05 QKV + attention, cluster-pair LN GEMMs, long-text tcgen05 attention)
 for tool in memcheck synccheck; do
-  SURGE_ATT_LONG_TC=1 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --target-processes all \
-    python scripts/sanitize_new_kernels.py > gpurun_out/sanitize_new_$tool.log 2>&1
-  echo "new kernels $tool rc=$? $(grep -E 'ERROR SUMMARY|new kernels ok' gpurun_out/sanitize_new_$tool.log | tr '\n' ' ')"
+  for tc in 1 0; do
+    SURGE_ATT_LONG_TC=$tc timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --target-processes all \
+      python scripts/sanitize_new_kernels.py > gpurun_out/sanitize_new_${tool}_tc$tc.log 2>&1
+    echo "new kernels $tool long_tc=$tc rc=$? $(grep -E 'ERROR SUMMARY|new kernels ok' gpurun_out/sanitize_new_${tool}_tc$tc.log | tr '\n' ' ')"
+  done
 done
 TSAN=$(gcc -print-file-name=libtsan.so)
 SURGE_BUILD_OUT=varlib/tsan.so SURGE_BUILD_DIR=varlib/_b_tsan NVCC_EXTRA="-Xcompiler -fsanitize=thread,-g" \

@@ -1,6 +1,7 @@
 """Small runs of the round-2 kernels for compute-sanitizer (scripts/sanitize.sh): the tcgen05 QKV + attention
-kernel (MiniLM class), the cluster-pair LayerNorm GEMMs and the long-text tcgen05 attention (bge-base class,
-texts of 129..300 tokens, SURGE_ATT_LONG_TC=1 set by the caller)."""
+kernel (MiniLM class, head-split staging), the cluster-pair LayerNorm GEMMs and the long-text attention
+(bge-base class, texts of 20..512 tokens over every length-class edge: the tcgen05 kernels when the caller
+sets SURGE_ATT_LONG_TC=1, else the mma.sync kernel's length classes)."""
 import os
 import sys
 
@@ -34,7 +35,7 @@ lens = rng.integers(1, 129, size=40).astype(np.int32)
 ids = rng.integers(1000, mini.vocab_size, size=int(lens.sum())).astype(np.int32)
 a = encode(mini, lens, ids, SURGE_OPT_ATT_TC=1)
 base = ENCODERS["bgebase"]
-lens = np.array([130, 200, 300, 20, 64, 90], dtype=np.int32)
+lens = np.array([130, 200, 300, 20, 64, 90, 65, 128, 129, 192, 193, 256, 257, 512], dtype=np.int32)   # every length class
 ids = rng.integers(1000, base.vocab_size, size=int(lens.sum())).astype(np.int32)
 b = encode(base, lens, ids, SURGE_OPT_LN_PAIR=1)
 print("new kernels ok", bool(np.isfinite(a).all() and np.isfinite(b).all()))

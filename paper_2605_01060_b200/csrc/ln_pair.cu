@@ -16,6 +16,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "epi_ln.cuh"
@@ -32,14 +33,28 @@ constexpr int EPI_WARPS = 8;
 #endif
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 
+// LN_PAIR_SPLIT (384 columns per CTA, i.e. d = 768): the tile's mainloop runs as two passes over K -- output
+// columns [0, 128) (N = 128 MMAs) into the 128 TMEM columns the previous tile's LayerNorm does not use, then
+// columns [128, 384) (N = 256) once that LayerNorm has drained -- so the first pass overlaps the previous
+// tile's epilogue (the A k-blocks are streamed twice).  The 128-column region alternates between TMEM columns
+// [384, 512) (even tiles) and [0, 128) (odd tiles); the epilogue reads it through epi_ln's column remap.
+// Measured (bge-base, 500K texts): out-proj + LN 171.4 -> 171.6 ms, FFN2 + LN 397.5 -> 411.7 ms, so off.
+// The kernel is bound by the L2 -> SM weight stream, not by the epilogue: every CTA streams its 384 weight
+// rows per 128-row tile (64 KB per k-block per 792 MMA cycles = 81 B/clk/SM, above the ~42 B/clk/SM share of
+// the chip's TMA throughput); ncu: the epilogue warps wait on the accumulator, the MMA issuer on the ring.
+// The cure is more rows per weight byte (cta_group::2 pairs over 256 rows inside 4-CTA clusters), not built.
+#ifndef LN_PAIR_SPLIT
+#define LN_PAIR_SPLIT 0
+#endif
 template <int BNC, int CL>   // columns per CTA (d / CL), CTAs per cluster
 struct LnPairCfg {
+  static constexpr bool SPLIT = LN_PAIR_SPLIT && BNC == 384 && LN_PAIR_KB == 64;
   static constexpr int N_MMA = BNC <= 256 ? 1 : 2;            // 192 / 256: one MMA, 384: 2 x 192, 512: 2 x 256
   static constexpr int MMA_N = BNC / N_MMA;
   static constexpr int KB = LN_PAIR_KB;                       // k-block width (elements)
   static constexpr int ROWB = KB * 2;                         // bytes per row of a k-block (= swizzle span)
   static constexpr int A_STAGE = BM * ROWB;                   // 8 / 16 KB
-  static constexpr int B_STAGE = BNC * ROWB;                  // 24 / 32 KB (KB 32), 48 / 64 KB (KB 64)
+  static constexpr int B_STAGE = (SPLIT ? 256 : BNC) * ROWB;  // 24 / 32 KB (KB 32), 48 / 64 KB (KB 64); SPLIT 32 KB
   static constexpr int B_BOX = KB == 32 ? 128 : 64;           // rows per B box (the weight maps, model.cu)
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int HEAD = 1024;
@@ -106,11 +121,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [STAGES]
   uint64_t* empty = full + STAGES;                      // [STAGES]
   uint64_t* tfull = empty + STAGES;                     // accumulator complete (commit)
-  uint64_t* tempty = tfull + 1;                         // accumulator drained (8 epilogue warps)
+  uint64_t* tempty = tfull + 1;                         // accumulator drained (8 epilogue warps); SPLIT: [2], tile % 2
   // [2] the peer's 8 epilogue warps published tile it's statistics (barrier it % 2): two barriers, so the peer
   // (which may publish tile it + 1 before this CTA waits for tile it) can never complete a phase this CTA
   // has not observed yet
-  uint64_t* pstats = tempty + 1;
+  uint64_t* pstats = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pstats + 2);
   float4* stats = reinterpret_cast<float4*>(smem + T::HEAD);                  // [2][2 CL][128]
   float* s_bias = reinterpret_cast<float*>(smem + T::HEAD + T::STATS);
@@ -135,7 +150,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, EPI_WARPS);
+    mbar_init(&tempty[0], EPI_WARPS);
+    mbar_init(&tempty[1], EPI_WARPS);
     mbar_init(&pstats[0], (CL - 1) * EPI_WARPS);
     mbar_init(&pstats[1], (CL - 1) * EPI_WARPS);
     fence_barrier_init();
@@ -157,6 +173,31 @@ __global__ void __launch_bounds__(THREADS, 1)
       griddep_wait();
       uint32_t c = 0;
       constexpr int NBOX = 1 + BNC / T::B_BOX;            // A + this CTA's B rows in B_BOX-row boxes
+      if constexpr (T::SPLIT) {
+        uint32_t box = 0;                                 // running box index (boxes go round-robin)
+        for (int t = t0; t < m_tiles; t += dt)
+          for (int pass = 0; pass < 2; ++pass) {
+            const int nb = pass ? 4 : 2, brow = pass ? 128 : 0;   // 64-row B boxes of this pass
+            for (int kb = 0; kb < num_kb; ++kb, ++c) {
+              const int s = int(c % STAGES);
+              const uint32_t ph = (c / STAGES) & 1;
+              for (int b = 0; b <= nb; ++b, ++box) {
+                if (int(box % 3) != p) continue;
+                mbar_wait(&empty[s], ph ^ 1);
+                if (b == 0) {
+#if LN_PAIR_RES_PREFETCH
+                  if (pass == 0 && K <= 1024 && kb * 64 < BNC) tma_prefetch_2d(&tmR, n0 + kb * 64, t * BM);
+#endif
+                  mbar_arrive_expect_tx(&full[s], uint32_t(T::A_STAGE + nb * 64 * 128));
+                  tma_load_2d(sRing + s * T::STAGE, &tmA, &full[s], kb * 64, t * BM);
+                } else {
+                  tma_load_2d_hint(sRing + s * T::STAGE + T::A_STAGE + (b - 1) * 64 * 128, &tmB, &full[s], kb * 64,
+                                   n0 + brow + (b - 1) * 64, pol_w);
+                }
+              }
+            }
+          }
+      } else
       for (int t = t0; t < m_tiles; t += dt)
         for (int kb = 0; kb < num_kb; ++kb, ++c) {
           const int s = int(c % STAGES);
@@ -188,8 +229,37 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint64_t r0 = T::KB == 32 ? umma_desc_sw64(smem_u32(sRing)) : umma_desc_sw128(smem_u32(sRing));
     uint32_t c = 0;
     int it = 0;
+    if constexpr (T::SPLIT) {
+      constexpr uint32_t id128 = umma_idesc_bf16(BM, 128), id256 = umma_idesc_bf16(BM, 256);
+      for (int t = t0; t < m_tiles; t += dt, ++it) {
+        for (int pass = 0; pass < 2; ++pass) {
+          // pass 0: columns [0, 128) into the region tile it - 2 used (drained by its LayerNorm); pass 1:
+          // columns [128, 384) into [128, 384) once tile it - 1's LayerNorm has drained them
+          const int prev = pass ? it - 1 : it - 2;
+          if (prev >= 0) mbar_wait(&tempty[prev & 1], (prev >> 1) & 1);
+          tc_fence_after();
+          const uint32_t dcol = pass ? 128u : ((it & 1) ? 0u : 384u);
+          for (int kb = 0; kb < num_kb; ++kb, ++c) {
+            const int s = int(c % STAGES);
+            mbar_wait(&full[s], (c / STAGES) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t ad = r0 + uint64_t((s * T::STAGE) >> 4);
+              const uint64_t bd = r0 + uint64_t((s * T::STAGE + T::A_STAGE) >> 4);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc_mma_bf16(tmem_base + dcol, ad + uint64_t(k * 2), bd + uint64_t(k * 2), pass ? id256 : id128,
+                            (kb | k) != 0);
+              tc_commit(&empty[s]);
+              if (pass == 1 && kb == num_kb - 1) tc_commit(tfull);
+            }
+            __syncwarp();
+          }
+        }
+      }
+    } else
     for (int t = t0; t < m_tiles; t += dt, ++it) {
-      mbar_wait(tempty, (it & 1) ^ 1);
+      mbar_wait(&tempty[0], (it & 1) ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < num_kb; ++kb, ++c) {
         const int s = int(c % STAGES);
@@ -230,17 +300,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       const PairMerge<CL> mg{2 * rank, smem_u32(st), smem_u32(&pstats[it & 1]), &pstats[it & 1],
                              uint32_t((it >> 1) & 1), lane, rank};
       const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + n0};
-      ln_epilogue<BNC, BNC / 2, true, 0u, 0u, float, PairMerge<CL>>(
-          taddr, 0, rg, s_bias, s_gamma, s_beta, st, q, hh, lane, eps,
-          [&] {
-            mbar_wait(tfull, it & 1);
-            tc_fence_after();
-          },
-          [&](const uint32_t (&p)[16], int col) { store_row_64B(p, lane, C, int64_t(t) * BM + q * 32, M, N, n0 + col); },
-          LnNoOp{}, mg);
+      auto epi = [&](auto remap_lo, auto remap_base) {
+        ln_epilogue<BNC, BNC / 2, true, decltype(remap_lo)::value, decltype(remap_base)::value, float, PairMerge<CL>>(
+            taddr, 0, rg, s_bias, s_gamma, s_beta, st, q, hh, lane, eps,
+            [&] {
+              mbar_wait(tfull, it & 1);
+              tc_fence_after();
+            },
+            [&](const uint32_t (&p)[16], int col) { store_row_64B(p, lane, C, int64_t(t) * BM + q * 32, M, N, n0 + col); },
+            LnNoOp{}, mg);
+      };
+      if (T::SPLIT && !(it & 1))   // even tiles: columns [0, 128) live at TMEM [384, 512)
+        epi(std::integral_constant<uint32_t, 128u>{}, std::integral_constant<uint32_t, 384u>{});
+      else
+        epi(std::integral_constant<uint32_t, 0u>{}, std::integral_constant<uint32_t, 0u>{});
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
+      if (lane == 0) mbar_arrive(&tempty[T::SPLIT ? (it & 1) : 0]);
     }
   }
   tc_fence_before();

@@ -39,16 +39,38 @@ constexpr int THREADS = 128 + 32 * EPI_WARPS;
 // tile's epilogue (the A k-blocks are streamed twice).  The 128-column region alternates between TMEM columns
 // [384, 512) (even tiles) and [0, 128) (odd tiles); the epilogue reads it through epi_ln's column remap.
 // Measured (bge-base, 500K texts): out-proj + LN 171.4 -> 171.6 ms, FFN2 + LN 397.5 -> 411.7 ms, so off.
-// The kernel is bound by the L2 -> SM weight stream, not by the epilogue: every CTA streams its 384 weight
-// rows per 128-row tile (64 KB per k-block per 792 MMA cycles = 81 B/clk/SM, above the ~42 B/clk/SM share of
-// the chip's TMA throughput); ncu: the epilogue warps wait on the accumulator, the MMA issuer on the ring.
-// The cure is more rows per weight byte (cta_group::2 pairs over 256 rows inside 4-CTA clusters), not built.
+// The epilogue is not what bounds the kernel (ncu: the epilogue warps wait on the accumulator, the MMA issuer
+// on the ring: 64 KB per k-block per 792 MMA cycles); halving the per-CTA weight stream by multicast over two
+// M tiles (LN_PAIR_MT = 2) was slower too, so it is the ring's latency, not L2 bandwidth.
+// LN_PAIR_MT = 2: a cluster of 2 CL CTAs covers two 128-row M tiles; the two CTAs of the same column part
+// stream the same weight rows, so each loads half of every k-block's B boxes and multicasts them to both
+// (the L2 -> SM weight stream per CTA halves); a ring slot is refilled once both consumers released it.
+// Measured slower (bge-base FFN2 + LN 398 -> 427 ms per 500K texts, bge-large 588 -> 646 ms, with SM clocks
+// 1.43 -> 1.48 GHz: less power, the two M tiles lock-stepped), so 1.
+#ifndef LN_PAIR_MT
+#define LN_PAIR_MT 1
+#endif
+__device__ __forceinline__ void tma_load_2d_mc_hint(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0,
+                                                    int32_t c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc1(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 #ifndef LN_PAIR_SPLIT
 #define LN_PAIR_SPLIT 0
 #endif
 template <int BNC, int CL>   // columns per CTA (d / CL), CTAs per cluster
 struct LnPairCfg {
-  static constexpr bool SPLIT = LN_PAIR_SPLIT && BNC == 384 && LN_PAIR_KB == 64;
+  static constexpr bool SPLIT = LN_PAIR_SPLIT && BNC == 384 && LN_PAIR_KB == 64 && LN_PAIR_MT == 1;
   static constexpr int N_MMA = BNC <= 256 ? 1 : 2;            // 192 / 256: one MMA, 384: 2 x 192, 512: 2 x 256
   static constexpr int MMA_N = BNC / N_MMA;
   static constexpr int KB = LN_PAIR_KB;                       // k-block width (elements)
@@ -86,12 +108,13 @@ struct PairMerge {
   uint32_t bar_cta;     // this tile's pstats barrier (shared::cta address) in every CTA
   uint64_t* my_bar;
   uint32_t parity;
-  int lane, rank;
+  int lane, rank;       // rank = column part within the row's CL CTAs
+  int base = 0;         // cluster rank of the row group's part 0 (LN_PAIR_MT > 1: m_sub * CL)
   __device__ __forceinline__ int part_off() const { return off; }
   __device__ __forceinline__ void publish(int part, int row, float4 v) const {
 #pragma unroll
     for (int pr = 1; pr < CL; ++pr) {
-      const uint32_t peer = uint32_t((rank + pr) % CL);
+      const uint32_t peer = uint32_t(base + (rank + pr) % CL);
       asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
                        mapa_shared(stats_cta + uint32_t((part * 128 + row) * 16), peer)),
                    "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
@@ -102,13 +125,13 @@ struct PairMerge {
 #pragma unroll
       for (int pr = 1; pr < CL; ++pr)
         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                         mapa_shared(bar_cta, uint32_t((rank + pr) % CL)))
+                         mapa_shared(bar_cta, uint32_t(base + (rank + pr) % CL)))
                      : "memory");
   }
   __device__ __forceinline__ void wait() const { mbar_wait_acq_cluster(my_bar, parity); }
 };
 
-template <int BNC, int CL>
+template <int BNC, int CL, int MT>
 __global__ void __launch_bounds__(THREADS, 1)
     ln_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmR, int M, int N,
@@ -134,10 +157,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sRing = smem + T::FIXED;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = int(cluster_ctarank());
+  const int crank = int(cluster_ctarank());
+  const int rank = crank % CL, m_sub = crank / CL;   // column part; M tile within the cluster's MT
   const int n0 = rank * BNC;
-  const int t0 = int(blockIdx.x) / CL, dt = int(gridDim.x) / CL;
-  const int m_tiles = (M + BM - 1) / BM;
+  // M tiles: cluster u handles tiles MT u + m_sub, u = cluster index, stride = number of clusters; with MT > 1
+  // every CTA of the cluster runs the same number of units (a tile >= m_tiles is a dummy: its A rows are
+  // zero-filled by TMA, its stores and residual loads masked) because they share the weight stream
+  const int u0 = int(blockIdx.x) / (CL * MT), du = int(gridDim.x) / (CL * MT);
+  const int m_units = ((M + BM - 1) / BM + MT - 1) / MT;
+  const int m_tiles = m_units * MT;                     // loop bound on units (t = MT u + m_sub)
+  const int t0 = MT * u0 + m_sub, dt = MT * du;
+  uint16_t bmask = 0;                                   // CTAs sharing this CTA's weight rows
+#pragma unroll
+  for (int j = 0; j < MT; ++j) bmask |= uint16_t(1u << (rank + CL * j));
   const int num_kb = K / T::KB;
 
   if (threadIdx.x == 0) {
@@ -147,7 +179,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch_desc(&tmR);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MT);                         // released by every CTA the slot's B boxes land in
     }
     mbar_init(tfull, 1);
     mbar_init(&tempty[0], EPI_WARPS);
@@ -215,9 +247,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
               mbar_arrive_expect_tx(&full[s], uint32_t(T::STAGE));
               tma_load_2d(sRing + s * T::STAGE, &tmA, &full[s], kb * T::KB, t * BM);
-            } else {
+            } else if (MT == 1) {
               tma_load_2d_hint(sRing + s * T::STAGE + T::A_STAGE + (b - 1) * T::B_BOX * T::ROWB, &tmB, &full[s],
                                kb * T::KB, n0 + (b - 1) * T::B_BOX, pol_w);
+            } else if ((b - 1) % MT == m_sub) {   // this CTA's share of the B boxes, into both CTAs' rings
+              tma_load_2d_mc_hint(sRing + s * T::STAGE + T::A_STAGE + (b - 1) * T::B_BOX * T::ROWB, &tmB, &full[s],
+                                  kb * T::KB, n0 + (b - 1) * T::B_BOX, bmask, pol_w);
             }
           }
         }
@@ -274,7 +309,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int j = 0; j < T::N_MMA; ++j)
               tc_mma_bf16(tmem_base + j * T::MMA_N, ad + uint64_t(k * 2),
                           bd + uint64_t((j * T::MMA_N * T::ROWB + k * 32) >> 4), idesc, (kb | k) != 0);
-          tc_commit(&empty[s]);
+          if (MT == 1) tc_commit(&empty[s]);
+          else tc_commit_mc1(&empty[s], bmask);   // the slot is free here and in the CTA sharing its B boxes
           if (kb == num_kb - 1) tc_commit(tfull);
         }
         __syncwarp();
@@ -298,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool ok = row < M;
       float4* st = stats + (it & 1) * 2 * CL * BM;
       const PairMerge<CL> mg{2 * rank, smem_u32(st), smem_u32(&pstats[it & 1]), &pstats[it & 1],
-                             uint32_t((it >> 1) & 1), lane, rank};
+                             uint32_t((it >> 1) & 1), lane, rank, m_sub * CL};
       const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + n0};
       auto epi = [&](auto remap_lo, auto remap_base) {
         ln_epilogue<BNC, BNC / 2, true, decltype(remap_lo)::value, decltype(remap_base)::value, float, PairMerge<CL>>(
@@ -330,34 +366,43 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <int BNC, int CL>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t st) {
   using T = LnPairCfg<BNC, CL>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ln_pair_kernel<BNC, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t m_tiles = (g.M + BM - 1) / BM;
-  const int clusters = int(std::min<int64_t>(m_tiles, (sms > 0 ? sms : 148) / CL));
+  constexpr int MT = LN_PAIR_MT;
+  auto kern = ln_pair_kernel<BNC, CL, MT>;
+  static int max_clusters = 0;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(CL * clusters));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = size_t(T::SMEM);
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.x = CL * MT;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (max_clusters == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    if (e != cudaSuccess) return e;
+    if (CL * MT > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cfg.gridDim = dim3(unsigned(((sms > 0 ? sms : 148) / (CL * MT)) * CL * MT));
+    e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg);
+    if (e != cudaSuccess || max_clusters <= 0) return e != cudaSuccess ? e : cudaErrorLaunchOutOfResources;
+  }
+  const int64_t m_units = ((g.M + BM - 1) / BM + MT - 1) / MT;
+  const int clusters = int(std::min<int64_t>(m_units, max_clusters));
+  cfg.gridDim = dim3(unsigned(CL * MT * clusters));
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   const CUtensorMap tmR = g.tmR ? *g.tmR : *g.tmA;   // residual rows (L2 prefetch only)
-  return cudaLaunchKernelEx(&cfg, ln_pair_kernel<BNC, CL>, *g.tmA, *g.tmB, tmR, int(g.M), g.N, g.K, g.bias, g.res,
-                            g.gamma, g.beta, g.C, g.eps);
+  return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, tmR, int(g.M), g.N, g.K, g.bias, g.res, g.gamma, g.beta, g.C,
+                            g.eps);
 }
 
 }  // namespace

@@ -77,7 +77,7 @@ struct LnPairCfg {
   static constexpr int ROWB = KB * 2;                         // bytes per row of a k-block (= swizzle span)
   static constexpr int A_STAGE = BM * ROWB;                   // 8 / 16 KB
   static constexpr int B_STAGE = (SPLIT ? 256 : BNC) * ROWB;  // 24 / 32 KB (KB 32), 48 / 64 KB (KB 64); SPLIT 32 KB
-  static constexpr int B_BOX = KB == 32 ? 128 : 64;           // rows per B box (the weight maps, model.cu)
+  static constexpr int B_BOX = KB == 32 ? 128 : LN_PAIR_BBOX64 ? LN_PAIR_BBOX64 : BNC / 2;   // rows per B box (model.cu maps)
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int HEAD = 1024;
   static constexpr int STATS = 2 * 2 * CL * BM * 16;          // [tile parity][2 CL parts][128 rows] float4
@@ -86,6 +86,7 @@ struct LnPairCfg {
   static constexpr int STAGES = (227 * 1024 - FIXED) / STAGE;
   static constexpr int SMEM = FIXED + STAGES * STAGE;
   static_assert(STAGES >= 2, "ring");
+  static_assert(!SPLIT || B_BOX == 64, "the split mainloop loads 64-row weight boxes");
 };
 
 __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {

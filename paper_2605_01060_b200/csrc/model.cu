@@ -213,8 +213,9 @@ cudaError_t DeviceModel::init(const ModelShape& s, const uint16_t* blob, bool bl
           SURGE_TRY(make_tmap_bf16_k32(&L.tm_wo_p64, L.wo, d, d, 128));
           SURGE_TRY(make_tmap_bf16_k32(&L.tm_w2_p64, L.w2, d, f, 128));
         } else {
-          SURGE_TRY(make_tmap_bf16(&L.tm_wo_p64, L.wo, d, d, 64));
-          SURGE_TRY(make_tmap_bf16(&L.tm_w2_p64, L.w2, d, f, 64));
+          const uint32_t bb = LN_PAIR_BBOX64 ? LN_PAIR_BBOX64 : uint32_t(d / 4);   // = the kernel's BNC / 2
+          SURGE_TRY(make_tmap_bf16(&L.tm_wo_p64, L.wo, d, d, bb));
+          SURGE_TRY(make_tmap_bf16(&L.tm_w2_p64, L.w2, d, f, bb));
         }
       }
       if (mlp_fused_supported(int(d), int(f))) {

@@ -73,15 +73,14 @@ cudaError_t init_tma_encoder();
 bool pdl_enabled();
 cudaError_t make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 cudaError_t make_tmap_bf16_k32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
-// k-block width of the cluster-pair LN GEMMs (ln_pair.cu): 64 (128-byte swizzle), or 32 (64-byte swizzle, twice
-// the ring stages: measured slower, bge-base FFN2 + LN 382 -> 431 ms per 500K texts)
 // rows per weight (B) box of the cluster-pair LN GEMMs at 64-wide k-blocks: 64 (six / eight boxes per stage over
 // the three producer threads), 32, or 0 = BNC / 2 = d / 4 (two boxes per stage).  Measured (FFN2 + LN, bge-base /
 // bge-large per 500K / 200K texts): 64: 398 / 586 ms; d / 4: 403 / 622 ms; 32: 574 / 766 ms
 #ifndef LN_PAIR_BBOX64
-#ifndef LN_PAIR_BBOX64
 #define LN_PAIR_BBOX64 64
 #endif
+// k-block width of the cluster-pair LN GEMMs (ln_pair.cu): 64 (128-byte swizzle), or 32 (64-byte swizzle, twice
+// the ring stages: measured slower, bge-base FFN2 + LN 382 -> 431 ms per 500K texts)
 #ifndef LN_PAIR_KB
 #define LN_PAIR_KB 64
 #endif

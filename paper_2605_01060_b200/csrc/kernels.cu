@@ -597,6 +597,11 @@ __global__ void __launch_bounds__(TextAtt<DH, HG>::WARPS * 32) attention_text_ke
 // 128 rows (8 warps x 16) are staged in turn.  The per-row arithmetic is the text-tiled kernel's:
 // 16-row query tiles and 16-key blocks aligned to the text start, mma.sync m16n8k16 with P split
 // hi+lo, online softmax over the key blocks in order (so long and short texts follow one rule).
+// warps per CTA of the long-text kernel's classes <= 256 tokens (> 256: 16); C4 attention per 50K texts:
+// 4 warps 1,309 ms, 8 warps 1,238 ms, 12 warps 1,429 ms
+#ifndef ATT_LONG_WS
+#define ATT_LONG_WS 8
+#endif
 // W warps per CTA (query blocks of 16 W rows); the launcher splits the long texts into length classes so
 // the K/V buffers (and the CTAs per SM) fit the class: (64, 128], (128, 192], (192, 256] with 8 warps,
 // (256, 512] with 16 -- a 150-token text no longer takes a whole SM's shared memory sized for 512
@@ -888,11 +893,11 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
     attention_text_kernel<DH, HG><<<grid, TA::WARPS * 32, TA::smem(max_len), st>>>(                           \
         qkv, cu, tok0, ntok, win, heads, out, qscale, TA::rows(max_len));                                    \
     if (max_len > ATT_SHORT && d_long) {                                                                     \
-      using LA8 = LongAtt<DH, 8>;                                                                            \
+      using LA8 = LongAtt<DH, ATT_LONG_WS>;                                                                  \
       using LA16 = LongAtt<DH, 16>;                                                                          \
       static bool lattr_##DH = false;                                                                        \
       if (!lattr_##DH) {                                                                                     \
-        cudaFuncSetAttribute(attention_long_kernel<DH, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+        cudaFuncSetAttribute(attention_long_kernel<DH, ATT_LONG_WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              int(LA8::smem(256)));                                                           \
         cudaFuncSetAttribute(attention_long_kernel<DH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                              int(LA16::smem(512)));                                                          \
@@ -915,7 +920,7 @@ cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu, int64_t n_t
         const int32_t nc_ = long_class_off ? long_class_off[c_ + 1] - long_class_off[c_] : n_long;          \
         const dim3 gc_{unsigned(nc_), unsigned(heads), 1u};                                                  \
         if (nc_ > 0 && hi_ <= 256)                                                                           \
-          attention_long_kernel<DH, 8><<<gc_, 8 * 32, LA8::smem(cap_), st>>>(                                  \
+          attention_long_kernel<DH, ATT_LONG_WS><<<gc_, ATT_LONG_WS * 32, LA8::smem(cap_), st>>>(              \
               qkv, cu, tl_, tok0, heads, out, qscale, LA8::kv_rows(cap_), lo_, hi_);                           \
         else if (nc_ > 0)                                                                                    \
           attention_long_kernel<DH, 16><<<gc_, 16 * 32, LA16::smem(cap_), st>>>(                               \

@@ -394,8 +394,12 @@ def test_output_side_upload_and_resume(N, tmp_path):
             N.surge_destroy(h)
     st = O.LocalStorage(str(tmp_path))
     assert O.completed(st, "run") == {int(k) for k in wl.keys}
+    E = oenc.Encoder(ecfg, w)
     for key, ids, lens in wl:
-        assert np.array_equal(O.read_partition(st, "run", int(key)), direct[int(key)])
+        stored = O.read_partition(st, "run", int(key))
+        assert np.array_equal(stored, direct[int(key)])
+        # and against the oracle (every stored row of the toy run: P:165's k -> E_k map, rows in submission order)
+        compare(stored, E.encode_texts(texts_of(ids, lens)))
 
 
 def test_output_side_two_ranks_crash_and_resume(N, tmp_path):

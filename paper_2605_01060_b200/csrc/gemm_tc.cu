@@ -159,6 +159,13 @@ struct Sched {
 #define ATT_TR(i) do {} while (0)
 #endif
 
+// The MMA issuer's waits: with GEMM_MMA_SPIN the polling loop (the issuer is on the critical path), else the
+// default suspend-time-hint wait of common.cuh (A/B: within 0.2% of each other, so the default stays).
+#if defined(GEMM_MMA_SPIN) && defined(MBAR_SLEEP_ALL)
+#define mma_wait mbar_wait_spin
+#else
+#define mma_wait mbar_wait
+#endif
 template <int BN, int EPI, bool WS, bool PAIR, int DH = 0>
 __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
     constexpr uint32_t idesc = umma_idesc_bf16(T::UMMA_M, T::MMA_N);
     const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
     const uint64_t b_desc0 = umma_desc_sw128(smem_u32(WS ? sB : sBs));
-    if constexpr (WS) mbar_wait(bfull, 0);
+    if constexpr (WS) mma_wait(bfull, 0);
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
@@ -322,10 +329,10 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
       const uint32_t aph = (it / ACC) & 1;
 #ifdef ATT_TRACE
       long long _e0 = clock64();
-      mbar_wait(&tempty[acc], aph ^ 1);
+      mma_wait(&tempty[acc], aph ^ 1);
       mt_acc[8] += clock64() - _e0;
 #else
-      mbar_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
+      mma_wait(&tempty[acc], aph ^ 1);       // epilogue drained this accumulator buffer
 #endif
 #ifndef ATT_GATE
 #define ATT_GATE 2
@@ -339,8 +346,8 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
 #ifdef ATT_TRACE
         long long _g0 = clock64();
 #endif
-        if (ATT_GATE == 1 && it >= 1) mbar_wait(att_gate, (it - 1) & 1);
-        if (ATT_GATE == 2 && it >= 2) mbar_wait(att_gate, (it - 2) & 1);
+        if (ATT_GATE == 1 && it >= 1) mma_wait(att_gate, (it - 1) & 1);
+        if (ATT_GATE == 2 && it >= 2) mma_wait(att_gate, (it - 2) & 1);
 #ifdef ATT_TRACE
         mt_acc[0] += clock64() - _g0;
 #endif
@@ -350,10 +357,10 @@ __global__ void __launch_bounds__(TileCfg<BN, EPI, PAIR, DH>::THREADS, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
 #ifdef ATT_TRACE
         long long _f0 = clock64();
-        mbar_wait(&full[s], ph);
+        mma_wait(&full[s], ph);
         if (kb < 7) mt_acc[1 + kb] += clock64() - _f0;
 #else
-        mbar_wait(&full[s], ph);
+        mma_wait(&full[s], ph);
 #endif
         tc_fence_after();
         if (elect_one()) {

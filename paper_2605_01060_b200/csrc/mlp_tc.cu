@@ -141,6 +141,8 @@ __device__ const char* const g_mtl_names[M_N] = {"a_full(iss)", "g0_issued", "y0
     mbar_wait(bar, par);                        \
     tw[slot] += clock64() - _t0;                \
   } while (0)
+#elif defined(MLP_MMA_SPIN) && defined(MBAR_SLEEP_ALL)
+#define MW(bar, par, slot) mbar_wait_spin(bar, par)   // the MMA issuer polls (critical path), the rest sleep
 #else
 #define MW(bar, par, slot) mbar_wait(bar, par)
 #endif

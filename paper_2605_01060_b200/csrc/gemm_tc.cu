@@ -848,8 +848,22 @@ cudaError_t make_tmap_store_bf16(CUtensorMap* map, const void* ptr, uint64_t row
 // twice the MMA work per A byte of a 192-column slice) are implemented (WS && PAIR) but not
 // selected: with a single 384-column TMEM accumulator the epilogue serialises with the mainloop
 // and measured slower than 192-column single-CTA slices (QKV 109 vs 84 ms per 1M texts).
+// Streaming (non-weight-stationary, BN = 256) GEMMs of the bge classes as CTA pairs too: M = 256 per
+// cta_group::2 MMA, each CTA loading half of the 256 weight rows per k-block, so the weight bytes per output
+// row halve.  GELU GEMM (FFN1, GEMM_GELU_PAIR): bge-base 409 -> 369 ms per 500K texts, bge-large 531 -> 476 ms
+// per 200K (+2.9% / +3.1% texts/s).  Bias GEMM (the QKV projection of chunks with texts > 128 tokens,
+// GEMM_BIAS_PAIR): C4 bge-large 890 -> 775 ms per 50K long texts (+1.9% texts/s).
+#ifndef GEMM_GELU_PAIR
+#define GEMM_GELU_PAIR 1
+#endif
+#ifndef GEMM_BIAS_PAIR
+#define GEMM_BIAS_PAIR 1
+#endif
 bool gemm_use_pair(int N, int K, int epi) {
   if (K % 64 != 0) return false;
+  if (((GEMM_GELU_PAIR && epi == EPI_BIAS_GELU) || (GEMM_BIAS_PAIR && epi == EPI_BIAS)) &&
+      gemm_bn_for(N, K, epi) == 256 && !(TileCfg<256, EPI_BIAS>::stages(K, true) >= 3))
+    return true;
   return epi == EPI_BIAS_LN && N == 384;
 }
 

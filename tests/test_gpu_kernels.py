@@ -74,6 +74,7 @@ GEMM_CASES = [
     (50001, 1152, 384, 0), (50001, 1536, 384, 1), (50001, 384, 384, 2), (20001, 384, 1536, 2),
     # bge-base / bge-large class shapes (N1): streaming 256-column tiles, fp32 pre-LN epilogue (epi 3)
     (3001, 2304, 768, 0), (3001, 3072, 768, 1), (3001, 768, 768, 3), (3001, 768, 3072, 3), (777, 1024, 4096, 3),
+    (3001, 4096, 1024, 1), (255, 3072, 768, 1),
 ]
 
 

@@ -72,6 +72,9 @@ template <int BNC, int CL>   // columns per CTA (d / CL), CTAs per cluster
 struct LnPairCfg {
   static constexpr bool SPLIT = LN_PAIR_SPLIT && BNC == 384 && LN_PAIR_KB == 64 && LN_PAIR_MT == 1;
   static constexpr int N_MMA = BNC <= 256 ? 1 : 2;            // 192 / 256: one MMA, 384: 2 x 192, 512: 2 x 256
+  // TMEM accumulators: two when 2 BNC <= 512 columns (clusters of 3 / 4 CTAs at d = 768 / 1024), so the
+  // LayerNorm epilogue of tile t overlaps the mainloop of tile t + 1
+  static constexpr int ACC = (!SPLIT && 2 * BNC <= 512) ? 2 : 1;
   static constexpr int MMA_N = BNC / N_MMA;
   static constexpr int KB = LN_PAIR_KB;                       // k-block width (elements)
   static constexpr int ROWB = KB * 2;                         // bytes per row of a k-block (= swizzle span)
@@ -144,8 +147,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [STAGES]
   uint64_t* empty = full + STAGES;                      // [STAGES]
-  uint64_t* tfull = empty + STAGES;                     // accumulator complete (commit)
-  uint64_t* tempty = tfull + 1;                         // accumulator drained (8 epilogue warps); SPLIT: [2], tile % 2
+  uint64_t* tfull = empty + STAGES;                     // [ACC] accumulator complete (commit)
+  uint64_t* tempty = tfull + 2;                         // [ACC] accumulator drained (8 epilogue warps); SPLIT: [2], tile % 2
   // [2] the peer's 8 epilogue warps published tile it's statistics (barrier it % 2): two barriers, so the peer
   // (which may publish tile it + 1 before this CTA waits for tile it) can never complete a phase this CTA
   // has not observed yet
@@ -182,7 +185,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], MT);                         // released by every CTA the slot's B boxes land in
     }
-    mbar_init(tfull, 1);
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);
     mbar_init(&tempty[0], EPI_WARPS);
     mbar_init(&tempty[1], EPI_WARPS);
     mbar_init(&pstats[0], (CL - 1) * EPI_WARPS);
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_mma_bf16(tmem_base + dcol, ad + uint64_t(k * 2), bd + uint64_t(k * 2), pass ? id256 : id128,
                             (kb | k) != 0);
               tc_commit(&empty[s]);
-              if (pass == 1 && kb == num_kb - 1) tc_commit(tfull);
+              if (pass == 1 && kb == num_kb - 1) tc_commit(&tfull[0]);
             }
             __syncwarp();
           }
@@ -295,7 +299,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     } else
     for (int t = t0; t < m_tiles; t += dt, ++it) {
-      mbar_wait(&tempty[0], (it & 1) ^ 1);
+      const int acc = it % T::ACC;
+      const uint32_t aph = uint32_t(it / T::ACC) & 1;
+      const uint32_t d0 = tmem_base + uint32_t(acc * BNC);
+      mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < num_kb; ++kb, ++c) {
         const int s = int(c % STAGES);
@@ -308,11 +315,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int k = 0; k < T::KB / 16; ++k)
 #pragma unroll
             for (int j = 0; j < T::N_MMA; ++j)
-              tc_mma_bf16(tmem_base + j * T::MMA_N, ad + uint64_t(k * 2),
+              tc_mma_bf16(d0 + j * T::MMA_N, ad + uint64_t(k * 2),
                           bd + uint64_t((j * T::MMA_N * T::ROWB + k * 32) >> 4), idesc, (kb | k) != 0);
           if (MT == 1) tc_commit(&empty[s]);
           else tc_commit_mc1(&empty[s], bmask);   // the slot is free here and in the CTA sharing its B boxes
-          if (kb == num_kb - 1) tc_commit(tfull);
+          if (kb == num_kb - 1) tc_commit(&tfull[acc]);
         }
         __syncwarp();
       }
@@ -337,11 +344,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const PairMerge<CL> mg{2 * rank, smem_u32(st), smem_u32(&pstats[it & 1]), &pstats[it & 1],
                              uint32_t((it >> 1) & 1), lane, rank, m_sub * CL};
       const ResidualGlobal rg{res + size_t(ok ? row : 0) * N + n0};
+      const int acc = it % T::ACC;
+      const uint32_t aph = uint32_t(it / T::ACC) & 1;
       auto epi = [&](auto remap_lo, auto remap_base) {
         ln_epilogue<BNC, BNC / 2, true, decltype(remap_lo)::value, decltype(remap_base)::value, float, PairMerge<CL>>(
-            taddr, 0, rg, s_bias, s_gamma, s_beta, st, q, hh, lane, eps,
+            taddr + uint32_t(acc * BNC), 0, rg, s_bias, s_gamma, s_beta, st, q, hh, lane, eps,
             [&] {
-              mbar_wait(tfull, it & 1);
+              mbar_wait(&tfull[acc], aph);
               tc_fence_after();
             },
             [&](const uint32_t (&p)[16], int col) { store_row_64B(p, lane, C, int64_t(t) * BM + q * 32, M, N, n0 + col); },
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         epi(std::integral_constant<uint32_t, 0u>{}, std::integral_constant<uint32_t, 0u>{});
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[T::SPLIT ? (it & 1) : 0]);
+      if (lane == 0) mbar_arrive(&tempty[T::SPLIT ? (it & 1) : acc]);
     }
   }
   tc_fence_before();
@@ -414,13 +423,26 @@ cudaError_t launch_ln_pair(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0) return cudaSuccess;
   if (!ln_pair_supported(g.N, g.K)) return cudaErrorInvalidValue;
 #ifndef LN_PAIR_CL768
-#define LN_PAIR_CL768 2     // 4 measured 2x slower
+#define LN_PAIR_CL768 2     // out-projection (K = d): 2 CTAs x 384 columns
 #endif
 #ifndef LN_PAIR_CL1024
-#define LN_PAIR_CL1024 2   // 4-CTA clusters (256 columns, 4 stages) measured 1.7x slower
+#define LN_PAIR_CL1024 2   // out-projection: 2 x 512
 #endif
-  if (g.N == 768) return launch_t<768 / LN_PAIR_CL768, LN_PAIR_CL768>(g, st);
-  return launch_t<1024 / LN_PAIR_CL1024, LN_PAIR_CL1024>(g, st);
+  // FFN2 (K = 4 d): clusters of 3 / 4 CTAs x 256 columns, which leaves TMEM for two accumulators (the LayerNorm of
+  // tile t under the mainloop of tile t + 1): FFN2 + LN 392 -> 380 ms (bge-base, 500K texts), 584 -> 573 ms
+  // (bge-large, 200K); the out-projection (short K) measured slower that way (169 -> 181 / 217 -> 231 ms).
+#ifndef LN_PAIR_CL768_FFN2
+#define LN_PAIR_CL768_FFN2 3
+#endif
+#ifndef LN_PAIR_CL1024_FFN2
+#define LN_PAIR_CL1024_FFN2 4
+#endif
+  const bool ffn2 = g.K > g.N;
+  if (g.N == 768)
+    return ffn2 ? launch_t<768 / LN_PAIR_CL768_FFN2, LN_PAIR_CL768_FFN2>(g, st)
+                : launch_t<768 / LN_PAIR_CL768, LN_PAIR_CL768>(g, st);
+  return ffn2 ? launch_t<1024 / LN_PAIR_CL1024_FFN2, LN_PAIR_CL1024_FFN2>(g, st)
+              : launch_t<1024 / LN_PAIR_CL1024, LN_PAIR_CL1024>(g, st);
 }
 
 }  // namespace surge
